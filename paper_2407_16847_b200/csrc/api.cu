@@ -1,0 +1,415 @@
+// api.cu -- the C ABI of include/splat.h: argument validation, handle
+// lifetime, ACSR build orchestration and kernel dispatch.  No arithmetic of
+// the method lives here; every step runs in the kernels (acsr.cu, simt.cu,
+// tc_fused.cu) or the planner (plan.cpp).
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "kernels.h"
+#include "splat_internal.h"
+
+namespace splat {
+
+static thread_local char g_err[512] = "";
+static thread_local int g_launches = 0;
+
+splat_status set_error(splat_status st, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+void clear_error() { g_err[0] = 0; }
+void note_launches(int n) { g_launches = n; }
+
+static bool in_range(int v, int lo, int hi) { return v >= lo && v <= hi; }
+
+splat_status validate_pattern(const splat_pattern &p)
+{
+    const int N = p.seq_len;
+    if (!in_range(N, 1, 1 << 24))
+        return set_error(SPLAT_ERR_INVALID_ARG, "seq_len %d outside [1, 2^24]", N);
+    for (int r = 0; r < 7; ++r)
+        if (p.reserved[r] != 0) return set_error(SPLAT_ERR_INVALID_ARG, "reserved[%d] must be 0", r);
+    // which fields each kind reads; every other field must be 0
+    bool use_lohi = false, use_block = false, use_g = false, use_stride = false, use_radius = false,
+         use_causal = false;
+    switch (p.kind) {
+    case SPLAT_WINDOW: use_lohi = true; break;
+    case SPLAT_BLOCKED: use_block = true; break;
+    case SPLAT_STRIDED: use_stride = true; break;
+    case SPLAT_DILATED: use_stride = use_radius = true; break;
+    case SPLAT_GLOBAL_LOCAL: use_lohi = use_g = true; break;
+    case SPLAT_BIGBIRD: use_block = use_radius = true; break;
+    case SPLAT_STRIDED_LOCAL: use_stride = use_causal = true; break;
+    default: return set_error(SPLAT_ERR_INVALID_ARG, "unknown pattern kind %d", p.kind);
+    }
+    if (!use_lohi && (p.lo || p.hi)) return set_error(SPLAT_ERR_INVALID_ARG, "lo/hi unused by kind %d", p.kind);
+    if (!use_block && p.block) return set_error(SPLAT_ERR_INVALID_ARG, "block unused by kind %d", p.kind);
+    if (!use_g && p.n_global) return set_error(SPLAT_ERR_INVALID_ARG, "n_global unused by kind %d", p.kind);
+    if (!use_stride && p.stride) return set_error(SPLAT_ERR_INVALID_ARG, "stride unused by kind %d", p.kind);
+    if (!use_radius && p.radius) return set_error(SPLAT_ERR_INVALID_ARG, "radius unused by kind %d", p.kind);
+    if (!use_causal && p.causal) return set_error(SPLAT_ERR_INVALID_ARG, "causal unused by kind %d", p.kind);
+    if (use_lohi && !(in_range(p.lo, 0, N) && in_range(p.hi, 0, N)))
+        return set_error(SPLAT_ERR_INVALID_ARG, "window lo=%d hi=%d outside [0, N=%d]", p.lo, p.hi, N);
+    if (use_block && !in_range(p.block, 1, N))
+        return set_error(SPLAT_ERR_INVALID_ARG, "block %d outside [1, N=%d]", p.block, N);
+    if (use_stride && !in_range(p.stride, 1, N))
+        return set_error(SPLAT_ERR_INVALID_ARG, "stride %d outside [1, N=%d]", p.stride, N);
+    if (use_radius && !in_range(p.radius, 0, N))
+        return set_error(SPLAT_ERR_INVALID_ARG, "radius %d outside [0, N=%d]", p.radius, N);
+    if (use_g && !in_range(p.n_global, 0, N))
+        return set_error(SPLAT_ERR_INVALID_ARG, "n_global %d outside [0, N=%d]", p.n_global, N);
+    if (p.kind == SPLAT_GLOBAL_LOCAL && p.n_global == 1)
+        return set_error(SPLAT_ERR_UNSUPPORTED,
+                         "GLOBAL_LOCAL with n_global=1: canonical greedy runs pair column 0 with the window");
+    if (p.kind == SPLAT_BIGBIRD && p.block == 1)
+        return set_error(SPLAT_ERR_UNSUPPORTED, "BIGBIRD with block=1: canonical greedy runs differ");
+    if (p.kind == SPLAT_STRIDED_LOCAL && p.causal != 1)
+        return set_error(SPLAT_ERR_UNSUPPORTED, "STRIDED_LOCAL requires causal=1");
+    return SPLAT_OK;
+}
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+splat_status cuda_fail(cudaError_t e, const char *what)
+{
+    return set_error(e == cudaErrorMemoryAllocation ? SPLAT_ERR_OOM : SPLAT_ERR_CUDA, "%s: %s", what,
+                     cudaGetErrorString(e));
+}
+
+void free_device(splat_acsr_s *a)
+{
+    if (a->device < 0) return;
+    DeviceGuard g(a->device);
+    cudaFree(a->d_seg);
+    cudaFree(a->d_nseg);
+    cudaFree(a->d_row_ptr);
+    cudaFree(a->plan.d_qt_ptr);
+    cudaFree(a->plan.d_kv);
+    cudaFree(a->plan.d_order);
+}
+
+void finish_host_meta(splat_acsr_s *a)
+{
+    a->nnz = a->row_ptr_h[a->n];
+    int mx = 0;
+    for (int i = 0; i < a->n; ++i) mx = a->nseg_h[i] > mx ? a->nseg_h[i] : mx;
+    a->max_segs = mx;
+}
+
+DevAcsr dev_view(const splat_acsr_s *a)
+{
+    DevAcsr A;
+    A.seg = reinterpret_cast<const int4 *>(a->d_seg);
+    A.nseg = a->d_nseg;
+    A.row_ptr = a->d_row_ptr;
+    A.n = a->n;
+    A.nnz = a->nnz;
+    A.qt_ptr = a->plan.d_qt_ptr;
+    A.kv = a->plan.d_kv;
+    A.order = a->plan.d_order;
+    A.n_qt = a->plan.n_qt;
+    return A;
+}
+
+splat_status check_compute(splat_acsr a, int B, int H)
+{
+    clear_error();
+    if (!a) return set_error(SPLAT_ERR_INVALID_ARG, "null handle");
+    if (a->device < 0)
+        return set_error(SPLAT_ERR_INVALID_ARG, "host-only inspection handle: no device path (no CPU fallback)");
+    if (B < 1 || H < 1) return set_error(SPLAT_ERR_SHAPE, "B=%d H=%d must be >= 1", B, H);
+    if ((long long)B * H * a->n > (1LL << 31) - 1)
+        return set_error(SPLAT_ERR_SHAPE, "B*H*N exceeds 2^31-1 rows");
+    return SPLAT_OK;
+}
+
+splat_status check_d(splat_dtype dt, int d)
+{
+    if (dt == SPLAT_BF16) {
+        if (d != 64 && d != 128) return set_error(SPLAT_ERR_UNSUPPORTED, "bf16 path needs d in {64,128}, got %d", d);
+    } else if (dt == SPLAT_FP32) {
+        if (d < 1 || d > 256) return set_error(SPLAT_ERR_UNSUPPORTED, "fp32 path needs 1 <= d <= 256, got %d", d);
+    } else {
+        return set_error(SPLAT_ERR_INVALID_ARG, "unknown dtype %d", (int)dt);
+    }
+    return SPLAT_OK;
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+}  // namespace
+}  // namespace splat
+
+using namespace splat;
+
+extern "C" {
+
+splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, splat_acsr *out)
+{
+    clear_error();
+    if (!p || !out) return set_error(SPLAT_ERR_INVALID_ARG, "null pattern or out pointer");
+    *out = nullptr;
+    splat_status st = validate_pattern(*p);
+    if (st != SPLAT_OK) return st;
+    splat_acsr_s *a = new (std::nothrow) splat_acsr_s();
+    if (!a) return set_error(SPLAT_ERR_OOM, "host allocation failed");
+    a->pat = *p;
+    a->n = p->seq_len;
+    const int N = a->n;
+    a->seg_h.assign((size_t)N * 16, 0);
+    a->nseg_h.assign(N, 0);
+    a->row_ptr_h.assign((size_t)N + 1, 0);
+    if (device < 0) {
+        // host INSPECTION handle: same closed form, evaluated on the host
+        for (int i = 0; i < N; ++i) {
+            Seg s[4];
+            const int n = row_segments(*p, i, s);
+            int off = 0;
+            for (int k = 0; k < n; ++k) {
+                int32_t *g = &a->seg_h[(size_t)i * 16 + 4 * k];
+                g[0] = s[k].start; g[1] = s[k].step; g[2] = s[k].count; g[3] = off;
+                off += s[k].count;
+            }
+            for (int k = n; k < 4; ++k) a->seg_h[(size_t)i * 16 + 4 * k + 3] = off;
+            a->nseg_h[i] = (uint8_t)n;
+            a->row_ptr_h[i + 1] = a->row_ptr_h[i] + off;
+        }
+        finish_host_meta(a);
+        build_plan(*a);
+        *out = a;
+        return SPLAT_OK;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
+        delete a;
+        cudaGetLastError();
+        return set_error(SPLAT_ERR_INVALID_ARG, "device %d not available (%d devices)", device, ndev);
+    }
+    a->device = device;
+    DeviceGuard g(device);
+    cudaStream_t cs = (cudaStream_t)stream;
+    cudaError_t e;
+    if ((e = cudaMalloc(&a->d_seg, sizeof(int32_t) * 16 * (size_t)N)) != cudaSuccess ||
+        (e = cudaMalloc(&a->d_nseg, (size_t)N)) != cudaSuccess ||
+        (e = cudaMalloc(&a->d_row_ptr, sizeof(int64_t) * ((size_t)N + 1))) != cudaSuccess) {
+        free_device(a);
+        delete a;
+        return cuda_fail(e, "acsr allocation");
+    }
+    e = launch_acsr_build(*p, reinterpret_cast<int4 *>(a->d_seg), a->d_nseg, a->d_row_ptr, cs);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(a->seg_h.data(), a->d_seg, sizeof(int32_t) * 16 * (size_t)N, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(a->nseg_h.data(), a->d_nseg, (size_t)N, cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(a->row_ptr_h.data(), a->d_row_ptr, sizeof(int64_t) * ((size_t)N + 1),
+                            cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) {
+        free_device(a);
+        delete a;
+        return cuda_fail(e, "acsr build");
+    }
+    finish_host_meta(a);
+    build_plan(*a);
+    Plan &P = a->plan;
+    if ((e = cudaMalloc(&P.d_qt_ptr, sizeof(int32_t) * (P.n_qt + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_kv, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_order, sizeof(int32_t) * P.n_qt)) != cudaSuccess) {
+        free_device(a);
+        delete a;
+        return cuda_fail(e, "plan allocation");
+    }
+    e = cudaMemcpyAsync(P.d_qt_ptr, P.qt_ptr.data(), sizeof(int32_t) * (P.n_qt + 1), cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && P.n_entries > 0)
+        e = cudaMemcpyAsync(P.d_kv, P.kv.data(), sizeof(int32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(P.d_order, P.order.data(), sizeof(int32_t) * P.n_qt, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) {
+        free_device(a);
+        delete a;
+        return cuda_fail(e, "plan upload");
+    }
+    *out = a;
+    return SPLAT_OK;
+}
+
+splat_status splat_acsr_info(splat_acsr a, int32_t *n, int64_t *nnz, int32_t *max_segs, double *density)
+{
+    clear_error();
+    if (!a) return set_error(SPLAT_ERR_INVALID_ARG, "null handle");
+    if (n) *n = a->n;
+    if (nnz) *nnz = a->nnz;
+    if (max_segs) *max_segs = a->max_segs;
+    if (density) *density = (double)a->nnz / ((double)a->n * (double)a->n);
+    return SPLAT_OK;
+}
+
+splat_status splat_acsr_copy_meta(splat_acsr a, int32_t *seg, uint8_t *nseg, int64_t *row_ptr)
+{
+    clear_error();
+    if (!a) return set_error(SPLAT_ERR_INVALID_ARG, "null handle");
+    if (seg)
+        for (size_t i = 0; i < (size_t)a->n; ++i)
+            for (int k = 0; k < 4; ++k)
+                for (int c = 0; c < 3; ++c) seg[i * 12 + k * 3 + c] = a->seg_h[i * 16 + k * 4 + c];
+    if (nseg) memcpy(nseg, a->nseg_h.data(), (size_t)a->n);
+    if (row_ptr) memcpy(row_ptr, a->row_ptr_h.data(), sizeof(int64_t) * ((size_t)a->n + 1));
+    return SPLAT_OK;
+}
+
+splat_status splat_plan_info(splat_acsr a, int32_t *bm, int32_t *bn, int32_t *n_qtiles, int32_t *n_entries)
+{
+    clear_error();
+    if (!a) return set_error(SPLAT_ERR_INVALID_ARG, "null handle");
+    if (bm) *bm = a->plan.bm;
+    if (bn) *bn = a->plan.bn;
+    if (n_qtiles) *n_qtiles = a->plan.n_qt;
+    if (n_entries) *n_entries = a->plan.n_entries;
+    return SPLAT_OK;
+}
+
+splat_status splat_plan_copy(splat_acsr a, int32_t *qt_ptr, int32_t *kv, int32_t *order)
+{
+    clear_error();
+    if (!a) return set_error(SPLAT_ERR_INVALID_ARG, "null handle");
+    const Plan &P = a->plan;
+    if (qt_ptr) memcpy(qt_ptr, P.qt_ptr.data(), sizeof(int32_t) * (P.n_qt + 1));
+    if (kv && P.n_entries) memcpy(kv, P.kv.data(), sizeof(int32_t) * P.n_entries);
+    if (order) memcpy(order, P.order.data(), sizeof(int32_t) * P.n_qt);
+    return SPLAT_OK;
+}
+
+splat_status splat_acsr_destroy(splat_acsr a)
+{
+    clear_error();
+    if (!a) return SPLAT_OK;
+    free_device(a);
+    delete a;
+    return SPLAT_OK;
+}
+
+splat_status splat_rsddmm(splat_acsr a, const void *Q, const void *K, splat_dtype dt, int32_t B, int32_t H,
+                          int32_t d, float scale, float *S, void *stream)
+{
+    splat_status st = check_compute(a, B, H);
+    if (st == SPLAT_OK) st = check_d(dt, d);
+    if (st != SPLAT_OK) return st;
+    if (!Q || !K || !S) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(S)) return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
+    DeviceGuard g(a->device);
+    cudaError_t e = launch_rsddmm_simt(dev_view(a), Q, K, dt == SPLAT_BF16, B * H, d, scale, S, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "splat_rsddmm launch");
+    note_launches(1);
+    return SPLAT_OK;
+}
+
+splat_status splat_sparse_softmax(splat_acsr a, const float *S, void *P, splat_dtype p_dt, int32_t B, int32_t H,
+                                  void *stream)
+{
+    splat_status st = check_compute(a, B, H);
+    if (st != SPLAT_OK) return st;
+    if (p_dt != SPLAT_BF16 && p_dt != SPLAT_FP32) return set_error(SPLAT_ERR_INVALID_ARG, "unknown dtype %d", (int)p_dt);
+    if (!S || !P) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
+    if ((const void *)S == P) return set_error(SPLAT_ERR_INVALID_ARG, "P may not alias S");
+    DeviceGuard g(a->device);
+    cudaError_t e = launch_softmax(dev_view(a), S, P, p_dt == SPLAT_BF16, B * H, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "splat_sparse_softmax launch");
+    note_launches(1);
+    return SPLAT_OK;
+}
+
+splat_status splat_rspmm(splat_acsr a, const void *P, const void *V, splat_dtype dt, int32_t B, int32_t H,
+                         int32_t d, void *O, void *stream)
+{
+    splat_status st = check_compute(a, B, H);
+    if (st == SPLAT_OK) st = check_d(dt, d);
+    if (st != SPLAT_OK) return st;
+    if (!P || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
+    if (!aligned16(P) || !aligned16(V) || !aligned16(O)) return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
+    DeviceGuard g(a->device);
+    cudaError_t e = launch_rspmm_simt(dev_view(a), P, V, dt == SPLAT_BF16, B * H, d, O, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "splat_rspmm launch");
+    note_launches(1);
+    return SPLAT_OK;
+}
+
+splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const void *V, splat_dtype dt,
+                               int32_t B, int32_t H, int32_t d, float scale, void *O, void *stream)
+{
+    splat_status st = check_compute(a, B, H);
+    if (st == SPLAT_OK) st = check_d(dt, d);
+    if (st != SPLAT_OK) return st;
+    if (!Q || !K || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O))
+        return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
+    DeviceGuard g(a->device);
+    cudaError_t e;
+    int nl = 1;
+    if (dt == SPLAT_BF16)
+        e = launch_mhsa_tc(dev_view(a), Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
+    else
+        e = launch_mhsa_simt(dev_view(a), Q, K, V, false, B * H, d, scale, O, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "splat_sparse_mhsa launch");
+    note_launches(nl);
+    return SPLAT_OK;
+}
+
+splat_status splat_sparse_mhsa_host(splat_acsr a, const void *Qh, const void *Kh, const void *Vh, splat_dtype dt,
+                                    int32_t B, int32_t H, int32_t d, float scale, void *Oh, void *dQ, void *dK,
+                                    void *dV, void *dO, void *stream)
+{
+    splat_status st = check_compute(a, B, H);
+    if (st == SPLAT_OK) st = check_d(dt, d);
+    if (st != SPLAT_OK) return st;
+    if (!Qh || !Kh || !Vh || !Oh) return set_error(SPLAT_ERR_INVALID_ARG, "null host pointer");
+    const size_t bytes = (size_t)B * H * a->n * d * (dt == SPLAT_BF16 ? 2 : 4);
+    DeviceGuard g(a->device);
+    cudaStream_t cs = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(dQ, Qh, bytes, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dK, Kh, bytes, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dV, Vh, bytes, cudaMemcpyHostToDevice, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
+    st = splat_sparse_mhsa(a, dQ, dK, dV, dt, B, H, d, scale, dO, stream);
+    if (st != SPLAT_OK) return st;
+    e = cudaMemcpyAsync(Oh, dO, bytes, cudaMemcpyDeviceToHost, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
+    return SPLAT_OK;
+}
+
+double splat_flops(splat_acsr a, int32_t B, int32_t H, int32_t d)
+{
+    if (!a) return 0.0;
+    return 4.0 * (double)a->nnz * (double)d * (double)B * (double)H;
+}
+
+int32_t splat_last_launch_count(void) { return g_launches; }
+
+const char *splat_last_error(void) { return g_err; }
+
+}  // extern "C"

@@ -1,0 +1,42 @@
+// kernels.h -- launchers of the device kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "splat_internal.h"
+
+namespace splat {
+
+// Device view of a handle: what every kernel needs.
+struct DevAcsr {
+    const int4 *seg;        // [N][4]: (start, step, count, offset-in-row)
+    const uint8_t *nseg;    // [N]
+    const int64_t *row_ptr; // [N+1]
+    int n;
+    long long nnz;
+    // tile plan
+    const int32_t *qt_ptr;  // [n_qt+1]
+    const int32_t *kv;      // [n_entries]
+    const int32_t *order;   // [n_qt]
+    int n_qt;
+};
+
+cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, int64_t *row_ptr,
+                              cudaStream_t st);
+
+// SIMT kernels (fp32 path; any d <= 256)
+cudaError_t launch_rsddmm_simt(const DevAcsr &A, const void *Q, const void *K, bool bf16, int BH, int d,
+                               float scale, float *S, cudaStream_t st);
+cudaError_t launch_softmax(const DevAcsr &A, const float *S, void *P, bool p_bf16, int BH,
+                           cudaStream_t st);
+cudaError_t launch_rspmm_simt(const DevAcsr &A, const void *P, const void *V, bool bf16, int BH, int d,
+                              void *O, cudaStream_t st);
+cudaError_t launch_mhsa_simt(const DevAcsr &A, const void *Q, const void *K, const void *V, bool bf16,
+                             int BH, int d, float scale, void *O, cudaStream_t st);
+
+// sm_100a tensor-core kernels (bf16, d in {64, 128}); return cudaErrorNotSupported
+// when the configuration is outside what they implement.
+cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, int d,
+                           float scale, void *O, cudaStream_t st, int *n_launch);
+
+}  // namespace splat

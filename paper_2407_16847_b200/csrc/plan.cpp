@@ -1,0 +1,74 @@
+// plan.cpp -- host tile planner.
+//
+// From the ACSR runs of every row it derives, per 128-row query tile, the
+// 128-column key tiles touched by any row of the tile.  This is the B200
+// form of the paper's span specialisation (a row group only iterates
+// over [min start, max end] of its rows) applied at tile granularity, and of
+// the R-SDDMM thread-block arrangement (Sec. 7.2): every plan
+// entry is one dense 128x128 tcgen05 tile, FULL when every row of the query
+// tile contains every column of the key tile (no fast-index masking needed,
+// P:237) and PARTIAL otherwise.  Query tiles are ordered longest first
+// (LPT) for the persistent kernels.  The planner works on O(rows) metadata
+// only, never on per-nnz data.
+#include <algorithm>
+#include <numeric>
+
+#include "splat_internal.h"
+
+namespace splat {
+
+void build_plan(splat_acsr_s &a)
+{
+    Plan &P = a.plan;
+    const int N = a.n, bm = P.bm, bn = P.bn;
+    P.n_qt = (N + bm - 1) / bm;
+    P.n_kt = (N + bn - 1) / bn;
+    P.qt_ptr.assign(P.n_qt + 1, 0);
+    P.kv.clear();
+    std::vector<int32_t> stamp(P.n_kt, -1), fullc(P.n_kt, 0);
+    std::vector<int32_t> touched;
+    touched.reserve(P.n_kt);
+    for (int t = 0; t < P.n_qt; ++t) {
+        const int r0 = t * bm, r1 = std::min(N, r0 + bm), nrows = r1 - r0;
+        touched.clear();
+        auto touch = [&](int j) {
+            if (stamp[j] != t) {
+                stamp[j] = t;
+                fullc[j] = 0;
+                touched.push_back(j);
+            }
+        };
+        for (int i = r0; i < r1; ++i) {
+            const int32_t *sg = &a.seg_h[(size_t)i * 16];
+            for (int s = 0; s < a.nseg_h[i]; ++s) {
+                const int start = sg[4 * s], step = sg[4 * s + 1], count = sg[4 * s + 2];
+                const int last = start + step * (count - 1);
+                if (step == 1) {
+                    for (int j = start / bn; j <= last / bn; ++j) {
+                        touch(j);
+                        const int c0 = j * bn, c1 = std::min(N, c0 + bn) - 1;
+                        if (start <= c0 && c1 <= last) ++fullc[j];
+                    }
+                } else if (step < bn) {
+                    for (int j = start / bn; j <= last / bn; ++j) touch(j);
+                } else {
+                    for (int x = 0; x < count; ++x) touch((start + step * x) / bn);
+                }
+            }
+        }
+        std::sort(touched.begin(), touched.end());
+        for (int j : touched) {
+            const bool full = (j + 1) * bn <= N && fullc[j] == nrows;
+            P.kv.push_back(j | (full ? 0 : kPartialBit));
+        }
+        P.qt_ptr[t + 1] = (int32_t)P.kv.size();
+    }
+    P.n_entries = (int)P.kv.size();
+    P.order.resize(P.n_qt);
+    std::iota(P.order.begin(), P.order.end(), 0);
+    std::stable_sort(P.order.begin(), P.order.end(), [&](int x, int y) {
+        return (P.qt_ptr[x + 1] - P.qt_ptr[x]) > (P.qt_ptr[y + 1] - P.qt_ptr[y]);
+    });
+}
+
+}  // namespace splat

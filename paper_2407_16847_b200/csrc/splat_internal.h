@@ -1,0 +1,163 @@
+// splat_internal.h -- internal types of the SPLAT B200 library (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "splat.h"
+
+#if defined(__CUDACC__)
+#define SPLAT_HD __host__ __device__ __forceinline__
+#else
+#define SPLAT_HD inline
+#endif
+
+namespace splat {
+
+// Query-tile rows and key-tile columns of the tile plan (tcgen05 M = 128,
+// 128-column key tiles).
+constexpr int kBM = 128;
+constexpr int kBN = 128;
+constexpr int kPartialBit = 1 << 24;
+constexpr int kKvMask = (1 << 24) - 1;
+
+struct Seg {
+    int32_t start, step, count;
+};
+
+SPLAT_HD int imin(int a, int b) { return a < b ? a : b; }
+SPLAT_HD int imax(int a, int b) { return a > b ? a : b; }
+
+// Canonical affine runs of row i in closed form (
+// SURVEY §8(c) C-2b).  Equal, row by row, to the paper's construction --
+// 2x2 solve on the first two columns, extension while consecutive
+// columns pass the check of P:219, restart at the first failing column --
+// applied to the row's column set; a run of one column has step 1
+// (SPEC S:96).  Returns the number of runs written to s (<= 3).
+// Preconditions: pattern validated by validate_pattern(), 0 <= i < N.
+SPLAT_HD int row_segments(const splat_pattern &p, int i, Seg *s)
+{
+    const int N = p.seq_len;
+    int n = 0;
+#define SPLAT_ADD(st, sp, ct)                                   \
+    do {                                                        \
+        int c_ = (ct);                                          \
+        if (c_ > 0) {                                           \
+            s[n].start = (st);                                  \
+            s[n].step = c_ == 1 ? 1 : (sp);                     \
+            s[n].count = c_;                                    \
+            ++n;                                                \
+        }                                                       \
+    } while (0)
+    switch (p.kind) {
+    case SPLAT_WINDOW: {
+        int a = imax(0, i - p.lo), e = imin(N - 1, i + p.hi);
+        SPLAT_ADD(a, 1, e - a + 1);
+        break;
+    }
+    case SPLAT_BLOCKED: {
+        int b0 = (i / p.block) * p.block;
+        SPLAT_ADD(b0, 1, imin(p.block, N - b0));
+        break;
+    }
+    case SPLAT_STRIDED: {
+        int r = i % p.stride;
+        SPLAT_ADD(r, p.stride, (N - 1 - r) / p.stride + 1);
+        break;
+    }
+    case SPLAT_DILATED: {
+        int dl = p.stride;
+        int st = i - dl * imin(p.radius, i / dl);
+        int en = i + dl * imin(p.radius, (N - 1 - i) / dl);
+        SPLAT_ADD(st, dl, (en - st) / dl + 1);
+        break;
+    }
+    case SPLAT_GLOBAL_LOCAL: {
+        int g = p.n_global;
+        int a = imax(0, i - p.lo), e = imin(N - 1, i + p.hi);
+        if (i < g) {
+            SPLAT_ADD(0, 1, N);
+        } else if (a <= g) {
+            SPLAT_ADD(0, 1, imax(e, g - 1) + 1);
+        } else {
+            SPLAT_ADD(0, 1, g);
+            SPLAT_ADD(a, 1, e - a + 1);
+        }
+        break;
+    }
+    case SPLAT_BIGBIRD: {
+        int bs = p.block, nb = (N + bs - 1) / bs, qb = i / bs;
+        if (qb == 0 || qb == nb - 1) {
+            SPLAT_ADD(0, 1, N);
+            break;
+        }
+        // block runs: [0,0], [lo_b, hi_b] (sliding), [nb-1, nb-1]; merge neighbours
+        int lo_b = imax(0, qb - p.radius), hi_b = imin(nb - 1, qb + p.radius);
+        const int r1a = lo_b, r1b = hi_b, r2a = nb - 1;
+        const bool m01 = r1a <= 1, m12 = r2a <= r1b + 1;
+        if (m01 && m12) {
+            SPLAT_ADD(0, 1, N);
+        } else if (m01) {
+            SPLAT_ADD(0, 1, imin(N, (r1b + 1) * bs));
+            SPLAT_ADD(r2a * bs, 1, N - r2a * bs);
+        } else if (m12) {
+            SPLAT_ADD(0, 1, imin(N, bs));
+            SPLAT_ADD(r1a * bs, 1, N - r1a * bs);
+        } else {
+            SPLAT_ADD(0, 1, imin(N, bs));
+            SPLAT_ADD(r1a * bs, 1, imin(N, (r1b + 1) * bs) - r1a * bs);
+            SPLAT_ADD(r2a * bs, 1, N - r2a * bs);
+        }
+        break;
+    }
+    case SPLAT_STRIDED_LOCAL: {
+        int l = p.stride;
+        if (i < l || l == 1) {
+            SPLAT_ADD(0, 1, i + 1);
+        } else if (i / l == 1) {
+            SPLAT_ADD(i - l, 1, l + 1);
+        } else {
+            SPLAT_ADD(i % l, l, i / l);
+            SPLAT_ADD(i - l + 1, 1, l);
+        }
+        break;
+    }
+    default:
+        break;
+    }
+#undef SPLAT_ADD
+    return n;
+}
+
+struct Plan {
+    int bm = kBM, bn = kBN, n_qt = 0, n_entries = 0, n_kt = 0;
+    std::vector<int32_t> qt_ptr, kv, order;
+    int32_t *d_qt_ptr = nullptr, *d_kv = nullptr, *d_order = nullptr;
+};
+
+}  // namespace splat
+
+struct splat_acsr_s {
+    splat_pattern pat;
+    int device = -1;
+    int32_t n = 0;
+    int64_t nnz = 0;
+    int32_t max_segs = 0;
+    // host copies (always present)
+    std::vector<int32_t> seg_h;       // [N][4][4]: start, step, count, offset-in-row
+    std::vector<uint8_t> nseg_h;      // [N]
+    std::vector<int64_t> row_ptr_h;   // [N+1]
+    // device copies (device >= 0)
+    int32_t *d_seg = nullptr;         // [N][4][4] (int4 per run)
+    uint8_t *d_nseg = nullptr;
+    int64_t *d_row_ptr = nullptr;
+    splat::Plan plan;
+};
+
+namespace splat {
+splat_status set_error(splat_status st, const char *fmt, ...);
+void clear_error();
+void note_launches(int n);
+splat_status validate_pattern(const splat_pattern &p);
+void build_plan(splat_acsr_s &a);
+}  // namespace splat

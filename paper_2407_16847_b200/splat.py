@@ -1,0 +1,225 @@
+"""Thin ctypes binding of the C ABI in include/splat.h (libsplat.so).
+
+Argument marshalling only: names follow the C entry points; torch tensors are
+passed as raw device pointers together with the current CUDA stream.  Every
+step of the hot path runs in the library's CUDA kernels.  There is no CPU
+fallback: if libsplat.so is missing or fails to load, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsplat.so")
+
+SPLAT_MAX_SEGS = 4
+STATUS = {0: "SPLAT_OK", 1: "SPLAT_ERR_INVALID_ARG", 2: "SPLAT_ERR_NOT_REGULAR", 3: "SPLAT_ERR_SHAPE",
+          4: "SPLAT_ERR_UNSUPPORTED", 5: "SPLAT_ERR_CUDA", 6: "SPLAT_ERR_OOM"}
+SPLAT_BF16, SPLAT_FP32 = 0, 1
+KINDS = {"window": 0, "blocked": 1, "strided": 2, "dilated": 3, "global_local": 4, "bigbird": 5,
+         "strided_local": 6}
+
+# every symbol include/splat.h declares (tests check the library exports them all)
+EXPORTS = ("splat_acsr_build", "splat_acsr_info", "splat_acsr_copy_meta", "splat_plan_info",
+           "splat_plan_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
+           "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_flops", "splat_last_launch_count",
+           "splat_last_error")
+
+
+class SplatError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class splat_pattern(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("seq_len", C.c_int32), ("lo", C.c_int32), ("hi", C.c_int32),
+                ("block", C.c_int32), ("n_global", C.c_int32), ("stride", C.c_int32), ("radius", C.c_int32),
+                ("causal", C.c_int32), ("reserved", C.c_int32 * 7)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsplat.so (raises if it is missing: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `python -m paper_2407_16847_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+        P = C.POINTER
+        L.splat_acsr_build.argtypes = [P(splat_pattern), C.c_int, vp, P(vp)]
+        L.splat_acsr_info.argtypes = [vp, P(i32), P(i64), P(i32), P(C.c_double)]
+        L.splat_acsr_copy_meta.argtypes = [vp, vp, vp, vp]
+        L.splat_plan_info.argtypes = [vp, P(i32), P(i32), P(i32), P(i32)]
+        L.splat_plan_copy.argtypes = [vp, vp, vp, vp]
+        L.splat_acsr_destroy.argtypes = [vp]
+        L.splat_rsddmm.argtypes = [vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp]
+        L.splat_sparse_softmax.argtypes = [vp, vp, vp, C.c_int, i32, i32, vp]
+        L.splat_rspmm.argtypes = [vp, vp, vp, C.c_int, i32, i32, i32, vp, vp]
+        L.splat_sparse_mhsa.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp]
+        L.splat_sparse_mhsa_host.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp, vp, vp, vp,
+                                             vp, vp]
+        L.splat_flops.argtypes = [vp, i32, i32, i32]
+        L.splat_flops.restype = C.c_double
+        L.splat_last_launch_count.restype = i32
+        L.splat_last_error.restype = C.c_char_p
+        for name in EXPORTS:
+            if name not in ("splat_flops", "splat_last_error", "splat_last_launch_count"):
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise SplatError(st, lib().splat_last_error().decode())
+
+
+def to_c_pattern(p) -> splat_pattern:
+    """workloads.Pattern (or any object with its fields) -> splat_pattern."""
+    return splat_pattern(KINDS[p.kind], p.seq_len, p.lo, p.hi, p.block, p.n_global, p.stride, p.radius,
+                         p.causal)
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return SPLAT_BF16
+    if t.dtype == torch.float32:
+        return SPLAT_FP32
+    raise SplatError(1, f"unsupported dtype {t.dtype}")
+
+
+class Acsr:
+    """Owning wrapper of a ``splat_acsr`` handle (splat_acsr_build / _destroy)."""
+
+    def __init__(self, pattern, device: int = 0, stream=None):
+        self.pattern = pattern
+        self.device = device
+        h = C.c_void_p()
+        st = 0 if device < 0 else _stream(stream) if torch.cuda.is_available() else 0
+        _check(lib().splat_acsr_build(C.byref(to_c_pattern(pattern)), device, C.c_void_p(st), C.byref(h)))
+        self.handle = h
+        n, nnz, ms, dens = C.c_int32(), C.c_int64(), C.c_int32(), C.c_double()
+        _check(lib().splat_acsr_info(h, C.byref(n), C.byref(nnz), C.byref(ms), C.byref(dens)))
+        self.n, self.nnz, self.max_segs, self.density = n.value, nnz.value, ms.value, dens.value
+
+    def copy_meta(self):
+        """(seg [N,4,3] int32, nseg [N] uint8, row_ptr [N+1] int64) as CPU tensors."""
+        seg = torch.zeros((self.n, SPLAT_MAX_SEGS, 3), dtype=torch.int32)
+        nseg = torch.zeros(self.n, dtype=torch.uint8)
+        row_ptr = torch.zeros(self.n + 1, dtype=torch.int64)
+        _check(lib().splat_acsr_copy_meta(self.handle, seg.data_ptr(), nseg.data_ptr(), row_ptr.data_ptr()))
+        return seg, nseg, row_ptr
+
+    def plan_info(self):
+        bm, bn, nq, ne = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().splat_plan_info(self.handle, C.byref(bm), C.byref(bn), C.byref(nq), C.byref(ne)))
+        return bm.value, bn.value, nq.value, ne.value
+
+    def plan_copy(self):
+        _, _, nq, ne = self.plan_info()
+        qt_ptr = torch.zeros(nq + 1, dtype=torch.int32)
+        kv = torch.zeros(max(ne, 1), dtype=torch.int32)
+        order = torch.zeros(nq, dtype=torch.int32)
+        _check(lib().splat_plan_copy(self.handle, qt_ptr.data_ptr(), kv.data_ptr(), order.data_ptr()))
+        return qt_ptr, kv[:ne], order
+
+    def flops(self, B: int, H: int, d: int) -> float:
+        return lib().splat_flops(self.handle, B, H, d)
+
+    def destroy(self):
+        if self.handle:
+            lib().splat_acsr_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def splat_acsr_build(pattern, device: int = 0, stream=None) -> Acsr:
+    return Acsr(pattern, device, stream)
+
+
+def _bhnd(x: torch.Tensor):
+    if x.dim() == 4:
+        return x.shape
+    if x.dim() == 3:
+        return (1,) + tuple(x.shape)
+    raise SplatError(3, f"expected [B,H,N,d] or [BH,N,d], got {tuple(x.shape)}")
+
+
+def _check_qkv(a: Acsr, *ts):
+    B, H, N, d = _bhnd(ts[0])
+    for t in ts:
+        if tuple(_bhnd(t)) != (B, H, N, d) or not t.is_contiguous() or not t.is_cuda:
+            raise SplatError(3, "tensors must be contiguous CUDA tensors of one [B,H,N,d] shape")
+        if t.dtype != ts[0].dtype:
+            raise SplatError(1, "dtype mismatch")
+    if N != a.n:
+        raise SplatError(3, f"N={N} differs from the handle's {a.n}")
+    return B, H, d
+
+
+def splat_rsddmm(a: Acsr, Q, K, S, scale: float, stream=None):
+    B, H, d = _check_qkv(a, Q, K)
+    if S.dtype != torch.float32 or S.numel() != B * H * a.nnz or not S.is_contiguous():
+        raise SplatError(3, "S must be contiguous float32 [B,H,nnz]")
+    _check(lib().splat_rsddmm(a.handle, Q.data_ptr(), K.data_ptr(), _dt(Q), B, H, d, scale, S.data_ptr(),
+                              C.c_void_p(_stream(stream))))
+    return S
+
+
+def splat_sparse_softmax(a: Acsr, S, P, B: int, H: int, stream=None):
+    if S.dtype != torch.float32 or S.numel() != B * H * a.nnz or P.numel() != S.numel():
+        raise SplatError(3, "S float32 and P of B*H*nnz elements")
+    _check(lib().splat_sparse_softmax(a.handle, S.data_ptr(), P.data_ptr(), _dt(P), B, H,
+                                      C.c_void_p(_stream(stream))))
+    return P
+
+
+def splat_rspmm(a: Acsr, P, V, O, stream=None):
+    B, H, d = _check_qkv(a, V, O)
+    if P.dtype != V.dtype or P.numel() != B * H * a.nnz:
+        raise SplatError(3, "P must have V's dtype and B*H*nnz elements")
+    _check(lib().splat_rspmm(a.handle, P.data_ptr(), V.data_ptr(), _dt(V), B, H, d, O.data_ptr(),
+                             C.c_void_p(_stream(stream))))
+    return O
+
+
+def splat_sparse_mhsa(a: Acsr, Q, K, V, O, scale: float, stream=None):
+    B, H, d = _check_qkv(a, Q, K, V, O)
+    _check(lib().splat_sparse_mhsa(a.handle, Q.data_ptr(), K.data_ptr(), V.data_ptr(), _dt(Q), B, H, d, scale,
+                                   O.data_ptr(), C.c_void_p(_stream(stream))))
+    return O
+
+
+def splat_sparse_mhsa_host(a: Acsr, Qh, Kh, Vh, Oh, scale: float, dQ, dK, dV, dO, stream=None):
+    """Host-buffer variant: Qh/Kh/Vh/Oh are (pinned) CPU tensors, dQ.. device staging buffers."""
+    B, H, N, d = _bhnd(Qh)
+    for t in (Qh, Kh, Vh, Oh):
+        if t.is_cuda or not t.is_contiguous() or tuple(_bhnd(t)) != (B, H, N, d):
+            raise SplatError(3, "host tensors must be contiguous CPU tensors of one shape")
+    _check_qkv(a, dQ, dK, dV, dO)
+    _check(lib().splat_sparse_mhsa_host(a.handle, Qh.data_ptr(), Kh.data_ptr(), Vh.data_ptr(), _dt(Qh), B, H, d,
+                                        scale, Oh.data_ptr(), dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(),
+                                        dO.data_ptr(), C.c_void_p(_stream(stream))))
+    return Oh
+
+
+def last_launch_count() -> int:
+    return lib().splat_last_launch_count()

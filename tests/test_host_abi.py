@@ -1,0 +1,151 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol of
+include/splat.h, validates descriptors, and its host logic (closed-form ACSR
+runs -- the same function the GPU build kernel evaluates -- and the tile
+planner) agrees bit-exactly with the oracle.  No compute calls (no GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2407_16847_b200 import build as B
+from paper_2407_16847_b200 import splat as S
+from workloads import CONFIGS, Pattern
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    B.build()
+    S.lib()
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "splat.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(splat_[a-z_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol():
+    declared = header_symbols()
+    assert set(declared) == set(S.EXPORTS)
+    out = subprocess.check_output(["nm", "-D", "--defined-only", S.LIB_PATH]).decode()
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    for name in declared:
+        assert name in exported, name
+        assert hasattr(ctypes.CDLL(S.LIB_PATH), name)
+
+
+def test_library_has_sm100a_code():
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", S.LIB_PATH]).decode()
+    assert "sm_100a" in out
+
+
+def _err(pattern):
+    with pytest.raises(S.SplatError) as e:
+        S.Acsr(pattern, device=-1)
+    return e.value.status
+
+
+def test_descriptor_validation():
+    assert _err(Pattern("window", 0, lo=1, hi=1)) == 1               # N < 1
+    assert _err(Pattern("window", 16, lo=17, hi=1)) == 1              # > N
+    assert _err(Pattern("blocked", 16, block=0)) == 1                 # <= 0
+    assert _err(Pattern("strided", 16, stride=3, block=2)) == 1       # unused field set
+    assert _err(Pattern("global_local", 16, lo=2, hi=2, n_global=1)) == 4   # degenerate greedy (R-11)
+    assert _err(Pattern("bigbird", 16, block=1, radius=1)) == 4
+    assert _err(Pattern("strided_local", 16, stride=4, causal=0)) == 4
+
+
+def test_host_handle_rejects_compute():
+    a = S.Acsr(Pattern("window", 64, lo=2, hi=2), device=-1)
+    L = S.lib()
+    st = L.splat_sparse_mhsa(a.handle, 16, 16, 16, 0, 1, 1, 64, 1.0, 16, None)
+    assert st == 1 and b"no CPU fallback" in L.splat_last_error()
+
+
+def compare_meta_with_oracle(p):
+    a = S.Acsr(p, device=-1)
+    seg, nseg, row_ptr = a.copy_meta()
+    oseg, onseg, orow, rc = O.acsr(p, max_seg=4)
+    assert rc == 0
+    assert np.array_equal(nseg.numpy().astype(np.int32), onseg), p
+    assert np.array_equal(seg.numpy(), oseg), p
+    assert np.array_equal(row_ptr.numpy(), orow), p
+    assert a.nnz == orow[-1] and a.max_segs == onseg.max()
+    return a
+
+
+@pytest.mark.parametrize("cfg", CONFIGS[:4], ids=lambda c: c.name)
+def test_closed_form_meta_bit_exact_configs(cfg):
+    compare_meta_with_oracle(cfg.pattern)
+
+
+def small_patterns(N):
+    for lo in range(0, N + 1, max(1, N // 5)):
+        for hi in range(0, N + 1, max(1, N // 4)):
+            yield Pattern("window", N, lo=lo, hi=hi)
+    for w in range(1, N + 1):
+        yield Pattern("blocked", N, block=w)
+        yield Pattern("strided", N, stride=w)
+        yield Pattern("strided_local", N, stride=w, causal=1)
+        if w >= 2:
+            yield Pattern("bigbird", N, block=w, radius=1)
+    for dl in range(1, N + 1, 3):
+        yield Pattern("dilated", N, stride=dl, radius=min(2, N))
+    for g in (0, min(2, N), N // 3):
+        if g != 1:
+            yield Pattern("global_local", N, lo=min(3, N), hi=min(5, N), n_global=g)
+
+
+@pytest.mark.parametrize("N", [1, 3, 17, 64])
+def test_closed_form_meta_bit_exact_exhaustive(N):
+    for p in small_patterns(N):
+        compare_meta_with_oracle(p)
+
+
+def plan_reference(m, bm, bn):
+    """Tiles touched / FULL from the oracle's explicit mask (independent of the planner)."""
+    N = m.shape[0]
+    out = []
+    for t in range((N + bm - 1) // bm):
+        rows = m[t * bm:(t + 1) * bm]
+        ents = []
+        for j in range((N + bn - 1) // bn):
+            blk = rows[:, j * bn:(j + 1) * bn]
+            if blk.any():
+                full = blk.shape[1] == bn and bool(blk.all())
+                ents.append((j, full))
+        out.append(ents)
+    return out
+
+
+@pytest.mark.parametrize("p", [Pattern("window", 700, lo=64, hi=64), Pattern("global_local", 1000, lo=128, hi=128, n_global=32),
+                               Pattern("bigbird", 1024, block=64, radius=1), Pattern("strided_local", 1100, stride=128, causal=1),
+                               Pattern("strided", 600, stride=7), Pattern("dilated", 900, stride=3, radius=50),
+                               Pattern("blocked", 640, block=96), Pattern("window", 300, lo=299, hi=0)],
+                         ids=lambda p: p.kind)
+def test_tile_plan_matches_mask(p):
+    a = S.Acsr(p, device=-1)
+    bm, bn, nq, ne = a.plan_info()
+    qt_ptr, kv, order = a.plan_copy()
+    ref = plan_reference(O.mask(p), bm, bn)
+    assert nq == len(ref)
+    for t in range(nq):
+        ents = [(int(e) & 0xFFFFFF, not (int(e) >> 24) & 1) for e in kv[qt_ptr[t]:qt_ptr[t + 1]]]
+        assert ents == ref[t], (p, t)
+    # LPT order: a permutation, by non-increasing number of key tiles
+    cnt = (qt_ptr[1:] - qt_ptr[:-1]).numpy()
+    assert sorted(order.tolist()) == list(range(nq))
+    assert all(cnt[order[i]] >= cnt[order[i + 1]] for i in range(nq - 1))
+
+
+def test_density_and_flops():
+    p = CONFIGS[1].pattern
+    a = S.Acsr(p, device=-1)
+    assert abs(a.density - a.nnz / p.seq_len ** 2) < 1e-15
+    assert a.flops(8, 12, 64) == 4.0 * a.nnz * 64 * 96
