@@ -206,12 +206,9 @@ def run_ours(args, cfg):
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
 
+    from paper_2407_16847_b200.shard import bh_range
     B, H = cfg.B, cfg.H
-    if args.scaling == "strong" and ws > 1:
-        assert (B * H) % ws == 0
-        bh = range(rank * B * H // ws, (rank + 1) * B * H // ws)
-    else:
-        bh = range(rank * B * H, (rank + 1) * B * H)          # weak: own batch per rank
+    bh = bh_range(B * H, rank, ws, args.scaling if ws > 1 else "weak")
     nbh = len(bh)
     dt = cfg.torch_dtype
     host = [make_tensor(cfg.index, t, 1, 1, cfg.N, cfg.d, dt, bh).view(1, nbh, cfg.N, cfg.d).pin_memory()

@@ -213,7 +213,8 @@ splat_status splat_rspmm(splat_acsr a, const void *P, const void *V, splat_dtype
  *     O[b,h] = softmax( M (x) scale * Q[b,h] K[b,h]^T ) V[b,h]
  *   Q, K, V, O   device [B,H,N,d] of dtype dt (O written; empty rows -> 0)
  *   d            as for splat_rsddmm
- *   scale        score scale (configs use 1/sqrt(d); 1.0 reproduces Eq. 1)
+ *   scale        score scale, positive and finite (configs use 1/sqrt(d);
+ *                1.0 reproduces Eq. 1); else SPLAT_ERR_INVALID_ARG
  * SPLAT_BF16 runs the sm_100a tensor-core kernel (TMA + tcgen05 + TMEM,
  * online softmax, fp32 accumulation); SPLAT_FP32 runs the SIMT fp32 kernel.
  * ------------------------------------------------------------------------- */

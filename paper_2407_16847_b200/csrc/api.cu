@@ -368,6 +368,7 @@ splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const
     if (!Q || !K || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
     if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O))
         return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
+    if (!(scale > 0.f) || scale == INFINITY) return set_error(SPLAT_ERR_INVALID_ARG, "scale must be positive and finite");
     DeviceGuard g(a->device);
     cudaError_t e;
     int nl = 1;

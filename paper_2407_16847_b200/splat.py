@@ -64,7 +64,7 @@ def lib():
         L.splat_rspmm.argtypes = [vp, vp, vp, C.c_int, i32, i32, i32, vp, vp]
         L.splat_sparse_mhsa.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp]
         L.splat_sparse_mhsa_host.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp, vp, vp, vp,
-                                             vp, vp]
+                                             vp]
         L.splat_flops.argtypes = [vp, i32, i32, i32]
         L.splat_flops.restype = C.c_double
         L.splat_last_launch_count.restype = i32
