@@ -27,6 +27,8 @@ from __future__ import annotations
 import argparse
 import json
 import math
+
+import numpy as np
 import os
 import statistics
 import sys
@@ -118,61 +120,71 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle (cpu_baseline / reference arm)
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg, seconds_target: float = 15.0, min_rows: int = 64):
-    """Bounded sample of the workload for the oracle: rows [0, R) of (b,h)=0.
-
-    R is chosen from the nnz per row so that the fp64 oracle needs about
-    ``seconds_target`` seconds at ~0.5 GFLOP/s per thread."""
+def oracle_sample(cfg, seconds_target: float = 15.0):
+    """Bounded sample of the workload for the oracle: the first H_s (b,h) slices
+    (all rows), plus rows [0, R) of one more slice, sized so the fp64 oracle
+    needs about ``seconds_target`` s at ~1 GFLOP/s per thread (measured rate of
+    the oracle on the GPU box).  Returns (full_heads, extra_rows, flops, threads)."""
     from oracle import oracle as O
-    seg, nseg, row_ptr, _ = O.acsr(cfg.pattern) if cfg.N <= 8192 else (None, None, None, None)
     threads = O.default_threads()
-    budget = seconds_target * 0.5e9 * threads
-    if row_ptr is None:       # large N: nnz per row from the row count bound
-        per_row = 4.0 * cfg.d * (cfg.pattern.lo + 1)
-        rows = int(min(cfg.N, max(min_rows, budget // per_row)))
-        flops = None
-    else:
-        rows = cfg.N
-        for r in range(1, cfg.N + 1):
-            if 4.0 * cfg.d * float(row_ptr[r]) > budget:
-                rows = max(min_rows, r)
+    budget = seconds_target * 1.0e9 * threads
+    if cfg.N <= 8192:
+        row_ptr = O.acsr(cfg.pattern)[2]
+    else:                     # nnz per row from the (causal) window bound, exact for WINDOW(lo, 0)
+        per = np.minimum(np.arange(cfg.N) + 1, cfg.pattern.lo + 1)
+        row_ptr = np.concatenate([[0], np.cumsum(per)])
+    per_head = 4.0 * cfg.d * float(row_ptr[-1])
+    full = int(min(cfg.BH, budget // per_head))
+    rows = 0
+    if full < cfg.BH:
+        rest = budget - full * per_head
+        for r in range(0, cfg.N + 1, 64):
+            if 4.0 * cfg.d * float(row_ptr[r]) > rest:
                 break
-        flops = 4.0 * cfg.d * float(row_ptr[rows])
-    return rows, flops, threads
+            rows = r
+    flops = full * per_head + 4.0 * cfg.d * float(row_ptr[rows])
+    return full, rows, flops, threads
 
 
-def time_oracle(cfg, rows: int, flops, threads: int, reps: int = 1):
+def time_oracle(cfg, full: int, rows: int, threads: int, reps: int = 1):
     from oracle import oracle as O
-    q = make_tensor(cfg.index, 0, 1, 1, cfg.N, cfg.d, cfg.torch_dtype, range(0, 1))[0]
-    k = make_tensor(cfg.index, 1, 1, 1, cfg.N, cfg.d, cfg.torch_dtype, range(0, 1))[0]
-    v = make_tensor(cfg.index, 2, 1, 1, cfg.N, cfg.d, cfg.torch_dtype, range(0, 1))[0]
-    if flops is None:
-        # count the nnz of the sampled rows with the oracle's own enumeration
-        flops = 4.0 * cfg.d * float(sum(len(O.row_cols(cfg.pattern, i)) for i in range(rows)))
+    n_sl = full + (1 if rows else 0)
+    qkv = [make_tensor(cfg.index, t, 1, 1, cfg.N, cfg.d, cfg.torch_dtype, range(0, n_sl)) for t in (0, 1, 2)]
     ts = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        O.attention(cfg.pattern, q, k, v, cfg.scale, rows=(0, rows), nthreads=threads)
+        for bh in range(full):
+            O.attention(cfg.pattern, qkv[0][bh], qkv[1][bh], qkv[2][bh], cfg.scale, nthreads=threads)
+        if rows:
+            O.attention(cfg.pattern, qkv[0][full], qkv[1][full], qkv[2][full], cfg.scale, rows=(0, rows),
+                        nthreads=threads)
         ts.append(time.perf_counter() - t0)
-    return flops, ts
+    return ts
+
+
+def sample_text(cfg, full, rows, threads):
+    s = f"{full} of {cfg.BH} (b,h) slices of {cfg.name} (N={cfg.N}, d={cfg.d}), all rows"
+    if rows:
+        s += f", + rows [0,{rows}) of slice {full}"
+    return s + f"; fp64 oracle, {threads} threads"
 
 
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    rows, flops, threads = oracle_sample(cfg, seconds_target=min(8.0, 150.0 / max(1, args.steps + args.warmup)))
-    flops, ts = time_oracle(cfg, rows, flops, threads, reps=args.steps + args.warmup)
+    full, rows, flops, threads = oracle_sample(cfg, seconds_target=min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    ts = time_oracle(cfg, full, rows, threads, reps=args.steps + args.warmup)
     ts = ts[args.warmup:]
     sec = sum(ts) / len(ts)
     value = flops / sec / 1e12
-    sample = f"rows [0,{rows}) of (b,h)=0 of {cfg.name} (N={cfg.N}, d={cfg.d}), fp64 oracle, {threads} threads"
+    sample = sample_text(cfg, full, rows, threads)
     line = {
         "impl": "reference", "metric": "fused sparse-MHSA nnz-counted TFLOP/s", "value": value,
         "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "B": cfg.B, "H": cfg.H, "N": cfg.N, "d": cfg.d,
-                   "pattern": cfg.pattern.__dict__, "sample_rows": rows},
+                   "pattern": cfg.pattern.__dict__, "sample": sample},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -303,11 +315,11 @@ def run_ours(args, cfg):
         "clocks": clk.result(),
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rows, oflops, threads = oracle_sample(cfg, seconds_target=args.cpu_seconds)
-        oflops, ts = time_oracle(cfg, rows, oflops, threads, reps=1)
+        full, rows, oflops, threads = oracle_sample(cfg, seconds_target=args.cpu_seconds)
+        ts = time_oracle(cfg, full, rows, threads, reps=1)
         line["cpu_baseline"] = {
             "value": oflops / ts[0] / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-            "sample": f"rows [0,{rows}) of (b,h)=0 of {cfg.name}; {ts[0]:.1f} s fp64"}
+            "sample": sample_text(cfg, full, rows, threads) + f"; {ts[0]:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
