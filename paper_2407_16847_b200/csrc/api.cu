@@ -110,6 +110,9 @@ void free_device(splat_acsr_s *a)
     cudaFree(a->plan.d_qt_ptr);
     cudaFree(a->plan.d_kv);
     cudaFree(a->plan.d_order);
+    cudaFree(a->plan.d_pair_ptr);
+    cudaFree(a->plan.d_pair_ent);
+    cudaFree(a->plan.d_pair_order);
 }
 
 void finish_host_meta(splat_acsr_s *a)
@@ -132,6 +135,12 @@ DevAcsr dev_view(const splat_acsr_s *a)
     A.kv = a->plan.d_kv;
     A.order = a->plan.d_order;
     A.n_qt = a->plan.n_qt;
+    A.pair_ptr = a->plan.d_pair_ptr;
+    A.pair_ent = a->plan.d_pair_ent;
+    A.pair_order = a->plan.d_pair_order;
+    A.n_pairs = a->plan.n_pairs;
+    A.n_buckets = a->plan.n_buckets;
+    for (int b = 0; b <= a->plan.n_buckets && b <= kMaxBuckets; ++b) A.bucket_start[b] = a->plan.bucket_start[b];
     return A;
 }
 
@@ -239,7 +248,10 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
     Plan &P = a->plan;
     if ((e = cudaMalloc(&P.d_qt_ptr, sizeof(int32_t) * (P.n_qt + 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_kv, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_order, sizeof(int32_t) * P.n_qt)) != cudaSuccess) {
+        (e = cudaMalloc(&P.d_order, sizeof(int32_t) * P.n_qt)) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_pair_ptr, sizeof(int32_t) * (P.n_pairs + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_pair_ent, sizeof(int32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_pair_order, sizeof(int32_t) * P.n_pairs)) != cudaSuccess) {
         free_device(a);
         delete a;
         return cuda_fail(e, "plan allocation");
@@ -249,6 +261,12 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
         e = cudaMemcpyAsync(P.d_kv, P.kv.data(), sizeof(int32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_order, P.order.data(), sizeof(int32_t) * P.n_qt, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(P.d_pair_ptr, P.pair_ptr.data(), sizeof(int32_t) * (P.n_pairs + 1), cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && P.n_pair_entries > 0)
+        e = cudaMemcpyAsync(P.d_pair_ent, P.pair_ent.data(), sizeof(int32_t) * P.n_pair_entries, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(P.d_pair_order, P.pair_order.data(), sizeof(int32_t) * P.n_pairs, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) {
         free_device(a);

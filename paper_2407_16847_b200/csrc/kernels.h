@@ -19,6 +19,12 @@ struct DevAcsr {
     const int32_t *kv;      // [n_entries]
     const int32_t *order;   // [n_qt]
     int n_qt;
+    // query-tile pairs (fused kernel)
+    const int32_t *pair_ptr;    // [n_pairs+1]
+    const int32_t *pair_ent;    // kv | kUseA | kUseB | kPartA | kPartB
+    const int32_t *pair_order;  // [n_pairs], bucketed longest first
+    int n_pairs, n_buckets;
+    int bucket_start[kMaxBuckets + 1];
 };
 
 cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, int64_t *row_ptr,

@@ -69,6 +69,44 @@ void build_plan(splat_acsr_s &a)
     std::stable_sort(P.order.begin(), P.order.end(), [&](int x, int y) {
         return (P.qt_ptr[x + 1] - P.qt_ptr[x]) > (P.qt_ptr[y + 1] - P.qt_ptr[y]);
     });
+
+    // ---- pairs of adjacent query tiles (2p, 2p+1): union of the two sorted key-tile
+    // lists, each entry flagged with which tile uses it and whether it is PARTIAL there.
+    P.n_pairs = (P.n_qt + 1) / 2;
+    P.pair_ptr.assign(P.n_pairs + 1, 0);
+    P.pair_ent.clear();
+    for (int p = 0; p < P.n_pairs; ++p) {
+        const int ta = 2 * p, tb = 2 * p + 1;
+        int ia = P.qt_ptr[ta], ea = P.qt_ptr[ta + 1];
+        int ib = tb < P.n_qt ? P.qt_ptr[tb] : 0, eb = tb < P.n_qt ? P.qt_ptr[tb + 1] : 0;
+        while (ia < ea || ib < eb) {
+            const int ka = ia < ea ? (P.kv[ia] & kKvMask) : 0x7fffffff;
+            const int kb = ib < eb ? (P.kv[ib] & kKvMask) : 0x7fffffff;
+            const int k = std::min(ka, kb);
+            int ent = k;
+            if (ka == k) { ent |= kUseA | ((P.kv[ia] & kPartialBit) ? kPartA : 0); ++ia; }
+            if (kb == k) { ent |= kUseB | ((P.kv[ib] & kPartialBit) ? kPartB : 0); ++ib; }
+            P.pair_ent.push_back(ent);
+        }
+        P.pair_ptr[p + 1] = (int32_t)P.pair_ent.size();
+    }
+    P.n_pair_entries = (int)P.pair_ent.size();
+    // order: cost buckets (floor(log2(union length))) longest first; the persistent
+    // kernel walks the units of a bucket head-major so K/V of one (b,h) stay in L2.
+    auto bucket = [&](int p) {
+        int len = P.pair_ptr[p + 1] - P.pair_ptr[p], b = 0;
+        while (len > 1) { len >>= 1; ++b; }
+        return b;
+    };
+    P.pair_order.resize(P.n_pairs);
+    std::iota(P.pair_order.begin(), P.pair_order.end(), 0);
+    std::stable_sort(P.pair_order.begin(), P.pair_order.end(),
+                     [&](int x, int y) { return bucket(x) > bucket(y); });
+    P.bucket_start.clear();
+    for (int i = 0; i < P.n_pairs; ++i)
+        if (i == 0 || bucket(P.pair_order[i]) != bucket(P.pair_order[i - 1])) P.bucket_start.push_back(i);
+    P.bucket_start.push_back(P.n_pairs);
+    P.n_buckets = (int)P.bucket_start.size() - 1;
 }
 
 }  // namespace splat

@@ -129,10 +129,19 @@ SPLAT_HD int row_segments(const splat_pattern &p, int i, Seg *s)
     return n;
 }
 
+// Pair-plan entry flags (the fused kernel runs two adjacent query tiles A = 2p
+// and B = 2p+1 against the union of their key-tile lists, sharing K/V loads).
+constexpr int kUseA = 1 << 24, kUseB = 1 << 25, kPartA = 1 << 26, kPartB = 1 << 27;
+constexpr int kMaxBuckets = 24;
+
 struct Plan {
     int bm = kBM, bn = kBN, n_qt = 0, n_entries = 0, n_kt = 0;
-    std::vector<int32_t> qt_ptr, kv, order;
+    std::vector<int32_t> qt_ptr, kv, order;          // per query tile (ABI: splat_plan_copy)
+    // query-tile pairs
+    int n_pairs = 0, n_pair_entries = 0, n_buckets = 0;
+    std::vector<int32_t> pair_ptr, pair_ent, pair_order, bucket_start;
     int32_t *d_qt_ptr = nullptr, *d_kv = nullptr, *d_order = nullptr;
+    int32_t *d_pair_ptr = nullptr, *d_pair_ent = nullptr, *d_pair_order = nullptr;
 };
 
 }  // namespace splat

@@ -3,25 +3,33 @@
 // Computes O = softmax(M (x) scale*Q K^T) V per (b, h) (PAPER Eq. 1)
 // without writing S or P to HBM.  The paper launches R-SDDMM, softmax and
 // R-SpMM as separate kernels with HBM buffers in between (Listing 4,
-// P:700-711); here one persistent kernel walks the tile plan:
+// P:700-711); here one persistent kernel walks the tile plan (plan.cpp).
 //
-//   work unit  = (b*H+h, 128-row query tile t), LPT order, CTAs round-robin
-//   per unit   : for each 128-column key tile j listed for t (span):
-//     TMA warp  : K_j, V_j  -> 128B-swizzled SMEM rings (3-D tensor maps,
-//                 out-of-range rows zero-filled)
-//     MMA warp  : S_j = Q K_j^T  (tcgen05.mma kind::f16, M=128 N=128, fp32
-//                 accumulator in TMEM, double-buffered), then O += P_j V_j
-//                 (M=128 N=d, V as an MN-major operand)
-//     4 softmax warps (one query row per thread, TMEM lane = row):
-//                 tcgen05.ld S_j -> fast-index mask on PARTIAL tiles (A-7:
-//                 column c of run (start, step, count) iff (c-start) % step
-//                 == 0 and 0 <= (c-start)/step < count) -> online max / sum
-//                 with exp2 (log2 e folded into the scale) -> P_j (bf16) into
-//                 SMEM in the UMMA K-major layout; O in TMEM is rescaled
-//                 only when the running max grows by more than 2^8.
-//   epilogue   : O / l -> bf16 -> HBM.
+//   work unit : (b*H+h, pair of adjacent 128-row query tiles A = 2p, B = 2p+1),
+//               processed against the UNION of the two key-tile lists (span
+//               specialisation, at tile granularity), so one K/V load
+//               serves both tiles.  Units are walked in cost buckets, longest
+//               first, head-major inside a bucket (K/V of a head stay in L2).
+//   warp 0    : TMA producer -- Q_A, Q_B, then K_e, V_e of every union entry e
+//               into 128B-swizzled SMEM rings (3-D tensor maps [BH, N, d],
+//               out-of-range rows zero-filled).
+//   warp 1    : tcgen05.mma issuer (one thread).  Per entry e and tile g that
+//               uses it: O_g += P_g(prev) V_prev (A operand P from TMEM, V an
+//               MN-major SMEM operand), then S_g = Q_g K_e^T (both K-major,
+//               M=128 N=128 K=16 steps, fp32 accumulator in TMEM).
+//   warps 4-7 / 8-11 : softmax of tile A / tile B (ping-pong: one group's
+//               exponentials overlap the other group's MMAs).  Thread = query
+//               row = TMEM lane.  tcgen05.ld S -> fast-index mask on PARTIAL
+//               entries (reading A-7: column c of run (start, step, count) iff
+//               (c-start) % step == 0 and 0 <= (c-start)/step < count),
+//               fully-masked 32-column chunks skip the exponentials -> running
+//               max (FMNMX3), exp2 with log2(e) folded into the scale (FFMA2 +
+//               MUFU.EX2), row sum (FADD2) -> P as packed bf16 written back over
+//               S in TMEM (tcgen05.st).  O is rescaled in TMEM only when the
+//               running max grows by more than 2^8 (stale-max trick).
+//   epilogue  : O / l -> bf16 -> HBM.
 //
-// TMEM: S buffers at columns [0,128) and [128,256), O at [256, 256+d).
+// TMEM (512 columns): S_A [0,128), S_B [128,256), O_A [256,256+d), O_B [256+d, 256+2d).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -36,25 +44,22 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kThreads = 192;          // warp 0 TMA, warp 1 MMA, warps 2..5 softmax
-constexpr int kTileBytes64 = 128 * 128; // one [128 rows x 64 bf16] swizzle-128B sub-tile (16 KB)
-constexpr float kRescaleThresh = 8.0f;  // log2 units
+constexpr int kThreads = 384;            // 3 warpgroups: [TMA, MMA, -, -], softmax A, softmax B
+constexpr int kTileBytes64 = 128 * 128;  // [128 rows x 64 bf16] swizzle-128B sub-tile (16 KB)
+constexpr float kRescaleThresh = 8.0f;   // log2 units
 
 template <int D>
 struct Cfg {
-    static constexpr int kChunks = D / 64;                  // 64-column sub-tiles along d
-    static constexpr int kTileBytes = kChunks * kTileBytes64; // one Q/K/V tile
-    static constexpr int QS = D == 64 ? 2 : 1;
-    static constexpr int KS = D == 64 ? 3 : 2;
-    static constexpr int PS = 2;
-    static constexpr int kPBytes = 2 * kTileBytes64;        // 128 x 128 bf16
+    static constexpr int kChunks = D / 64;
+    static constexpr int kTileBytes = kChunks * kTileBytes64;
+    static constexpr int QS = D == 64 ? 2 : 1;   // Q buffers per tile group
+    static constexpr int KS = D == 64 ? 3 : 2;   // K and V ring depth
     static constexpr int OFF_Q = 0;
-    static constexpr int OFF_K = OFF_Q + QS * kTileBytes;
+    static constexpr int OFF_K = OFF_Q + 2 * QS * kTileBytes;
     static constexpr int OFF_V = OFF_K + KS * kTileBytes;
-    static constexpr int OFF_P = OFF_V + KS * kTileBytes;
-    static constexpr int OFF_BAR = OFF_P + PS * kPBytes;
-    static constexpr int NBAR = 2 * QS + 4 * KS + 8;
-    static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;   // + alignment slack
+    static constexpr int OFF_BAR = OFF_V + KS * kTileBytes;
+    static constexpr int NBAR = 4 * QS + 4 * KS + 6;
+    static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
 };
 
 struct Params {
@@ -64,9 +69,25 @@ struct Params {
     __nv_bfloat16 *O;
 };
 
+// unit u -> (pair, bh): buckets in order; inside a bucket, head-major.
+__device__ __forceinline__ void unit_at(const DevAcsr &A, int BH, int u, int &pair, int &bh)
+{
+    for (int b = 0; b < A.n_buckets; ++b) {
+        const int nb = A.bucket_start[b + 1] - A.bucket_start[b];
+        const int ub = nb * BH;
+        if (u < ub) {
+            bh = u / nb;
+            pair = A.pair_order[A.bucket_start[b] + u % nb];
+            return;
+        }
+        u -= ub;
+    }
+    pair = 0;
+    bh = 0;
+}
+
 __device__ __forceinline__ void set_bits(uint32_t (&m)[4], int lo, int hi)
 {
-    // set bits [lo, hi] (0 <= lo <= hi < 128)
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
         const int a = max(lo, 32 * w), b = min(hi, 32 * w + 31);
@@ -78,6 +99,51 @@ __device__ __forceinline__ void set_bits(uint32_t (&m)[4], int lo, int hi)
     }
 }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c)
+{
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint64_t pack2(float lo, float hi)
+{
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+
+__device__ __forceinline__ void unpack2(uint64_t v, float &lo, float &hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c)
+{
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b)
+{
+    uint64_t d;
+    asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// TS-MMA: D[tmem] (+)= A[tmem] * B[smem]; A (M=128 x K=16 bf16) packed two per 32-bit column.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -87,27 +153,26 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
-    uint64_t *q_full = bars, *q_empty = bars + C::QS;
-    uint64_t *k_full = q_empty + C::QS, *k_empty = k_full + C::KS;
+    uint64_t *q_full = bars;                     // [2][QS]
+    uint64_t *q_empty = q_full + 2 * C::QS;      // [2][QS]
+    uint64_t *k_full = q_empty + 2 * C::QS, *k_empty = k_full + C::KS;
     uint64_t *v_full = k_empty + C::KS, *v_empty = v_full + C::KS;
-    uint64_t *s_full = v_empty + C::KS, *s_empty = s_full + 2;
-    uint64_t *p_full = s_empty + 2, *p_empty = p_full + 2;
+    uint64_t *s_full = v_empty + C::KS;          // [2]
+    uint64_t *p_full = s_full + 2;               // [2]
+    uint64_t *epi = p_full + 2;                  // [2]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + C::NBAR);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevAcsr &A = prm.A;
-    const int n_units = A.n_qt * prm.BH;
+    const int n_units = A.n_pairs * prm.BH;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < C::QS; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
+        for (int i = 0; i < 2 * C::QS; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
         for (int i = 0; i < C::KS; ++i) {
             mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
+            mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 2);
         }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4);
-            mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1);
-        }
+        for (int g = 0; g < 2; ++g) { mbar_init(&s_full[g], 1); mbar_init(&p_full[g], 4); mbar_init(&epi[g], 1); }
         fence_mbar_init();
         tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
     }
@@ -120,38 +185,45 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            int qi = 0, ki = 0, vi = 0;
-            uint32_t qph = 0, kph = 0, vph = 0;
-            int qcnt = 0, kcnt = 0, vcnt = 0;
+            int qi[2] = {0, 0}, qc[2] = {0, 0};
+            uint32_t qph[2] = {0, 0};
+            int ki = 0, kc = 0;
+            uint32_t kph = 0;
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const int t = A.order[u / prm.BH], bh = u % prm.BH;
-                if (qcnt >= C::QS) mbar_wait(&q_empty[qi], qph ^ 1);
-                mbar_expect_tx(&q_full[qi], C::kTileBytes);
+                int pair, bh;
+                unit_at(A, prm.BH, u, pair, bh);
+                for (int g = 0; g < 2; ++g) {
+                    const int t = 2 * pair + g;
+                    if (t >= A.n_qt) break;
+                    const int slot = g * C::QS + qi[g];
+                    if (qc[g] >= C::QS) mbar_wait(&q_empty[slot], qph[g] ^ 1);
+                    mbar_expect_tx(&q_full[slot], C::kTileBytes);
 #pragma unroll
-                for (int c = 0; c < C::kChunks; ++c)
-                    tma_load_3d(smem + C::OFF_Q + qi * C::kTileBytes + c * kTileBytes64, &tmQ, &q_full[qi], 64 * c,
-                                t * 128, bh);
-                ++qcnt;
-                if (++qi == C::QS) { qi = 0; qph ^= 1; }
-                const int e0 = A.qt_ptr[t], e1 = A.qt_ptr[t + 1];
+                    for (int c = 0; c < C::kChunks; ++c)
+                        tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ, &q_full[slot],
+                                    64 * c, t * 128, bh);
+                    ++qc[g];
+                    if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
+                }
+                const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
                 for (int e = e0; e < e1; ++e) {
-                    const int kv = A.kv[e] & kKvMask;
-                    if (kcnt >= C::KS) mbar_wait(&k_empty[ki], kph ^ 1);
+                    const int kv = A.pair_ent[e] & kKvMask;
+                    if (kc >= C::KS) {
+                        mbar_wait(&k_empty[ki], kph ^ 1);
+                        mbar_wait(&v_empty[ki], kph ^ 1);
+                    }
                     mbar_expect_tx(&k_full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
                         tma_load_3d(smem + C::OFF_K + ki * C::kTileBytes + c * kTileBytes64, &tmK, &k_full[ki],
                                     64 * c, kv * 128, bh);
-                    ++kcnt;
-                    if (++ki == C::KS) { ki = 0; kph ^= 1; }
-                    if (vcnt >= C::KS) mbar_wait(&v_empty[vi], vph ^ 1);
-                    mbar_expect_tx(&v_full[vi], C::kTileBytes);
+                    mbar_expect_tx(&v_full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
-                        tma_load_3d(smem + C::OFF_V + vi * C::kTileBytes + c * kTileBytes64, &tmV, &v_full[vi],
+                        tma_load_3d(smem + C::OFF_V + ki * C::kTileBytes + c * kTileBytes64, &tmV, &v_full[ki],
                                     64 * c, kv * 128, bh);
-                    ++vcnt;
-                    if (++vi == C::KS) { vi = 0; vph ^= 1; }
+                    ++kc;
+                    if (++ki == C::KS) { ki = 0; kph ^= 1; }
                 }
             }
         }
@@ -161,128 +233,169 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             constexpr uint32_t idS = idesc_bf16(128, 128, false);
             constexpr uint32_t idO = idesc_bf16(128, D, true);
             const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
-            const uint32_t sV = smem_u32(smem + C::OFF_V), sP = smem_u32(smem + C::OFF_P);
-            int qi = 0, ki = 0, vi = 0;
-            uint32_t qph = 0, kph = 0, vph = 0;
-            uint32_t s_use[2] = {0, 0}, p_use[2] = {0, 0};
-            int sb = 0;   // next S buffer
-            uint32_t pv_count = 0;   // PVs issued so far (global P-buffer alternation, as the softmax's)
-            auto issue_pv = [&](bool first) {
-                const int pb = pv_count & 1;
-                ++pv_count;
-                mbar_wait(&p_full[pb], p_use[pb] & 1);
-                mbar_wait(&v_full[vi], vph);
-                tc_fence_after();
-                const uint32_t pbase = sP + pb * C::kPBytes, vbase = sV + vi * C::kTileBytes;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t a = sdesc_sw128(pbase + (kk >> 2) * kTileBytes64 + (kk & 3) * 32, 16, 1024);
-                    const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);
-                    mma_bf16_ss(tmem + 256, a, b, idO, (first && kk == 0) ? 0u : 1u);
-                }
-                mma_commit(&v_empty[vi]);
-                mma_commit(&p_empty[pb]);
-                ++p_use[pb];
-                if (++vi == C::KS) { vi = 0; vph ^= 1; }
-            };
+            const uint32_t sV = smem_u32(smem + C::OFF_V);
+            int qi[2] = {0, 0};
+            uint32_t qph[2] = {0, 0};
+            int ki = 0;
+            uint32_t kph = 0;
+            uint32_t pcnt[2] = {0, 0};   // p_full phases consumed per group
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const int t = A.order[u / prm.BH];
-                const int e0 = A.qt_ptr[t], n = A.qt_ptr[t + 1] - e0;
-                mbar_wait(&q_full[qi], qph);
-                const uint32_t qbase = sQ + qi * C::kTileBytes;
-                for (int j = 0; j < n; ++j) {
+                int pair, bh;
+                unit_at(A, prm.BH, u, pair, bh);
+                const bool hasB = 2 * pair + 1 < A.n_qt;
+                const int ng = hasB ? 2 : 1;
+                uint32_t qbase[2];
+                for (int g = 0; g < ng; ++g) {
+                    const int slot = g * C::QS + qi[g];
+                    mbar_wait(&q_full[slot], qph[g]);
+                    qbase[g] = sQ + slot * C::kTileBytes;
+                }
+                tc_fence_after();
+                bool pend[2] = {false, false}, first_pv[2] = {true, true}, other_uses[2] = {false, false};
+                int pv_stage[2] = {0, 0};
+                const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
+                auto issue_pv = [&](int g) {
+                    mbar_wait(&p_full[g], pcnt[g] & 1);
+                    ++pcnt[g];
+                    tc_fence_after();
+                    const int vs = pv_stage[g];
+                    const uint32_t vbase = sV + vs * C::kTileBytes;
+                    const uint32_t ptm = tmem + g * 128;      // P_g packed in S_g columns [0, 64)
+                    const uint32_t otm = tmem + 256 + g * D;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);
+                        mma_bf16_ts(otm, ptm + kk * 8, b, idO, (first_pv[g] && kk == 0) ? 0u : 1u);
+                    }
+                    first_pv[g] = false;
+                    mma_commit(&v_empty[vs]);
+                    if (!other_uses[g]) mbar_arrive(&v_empty[vs]);   // the other tile skips this entry
+                    pend[g] = false;
+                };
+                for (int e = e0; e < e1; ++e) {
+                    const int ent = A.pair_ent[e];
                     mbar_wait(&k_full[ki], kph);
-                    if (s_use[sb] > 0) mbar_wait(&s_empty[sb], (s_use[sb] - 1) & 1);
+                    mbar_wait(&v_full[ki], kph);
                     tc_fence_after();
                     const uint32_t kbase = sK + ki * C::kTileBytes;
+                    for (int g = 0; g < ng; ++g) {
+                        if (pend[g]) issue_pv(g);
+                        if (ent & (g == 0 ? kUseA : kUseB)) {
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;
-                        mma_bf16_ss(tmem + sb * 128, sdesc_sw128(qbase + off, 16, 1024),
-                                    sdesc_sw128(kbase + off, 16, 1024), idS, kk > 0 ? 1u : 0u);
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;
+                                mma_bf16_ss(tmem + g * 128, sdesc_sw128(qbase[g] + off, 16, 1024),
+                                            sdesc_sw128(kbase + off, 16, 1024), idS, kk > 0 ? 1u : 0u);
+                            }
+                            mma_commit(&s_full[g]);
+                            pend[g] = true;
+                            pv_stage[g] = ki;
+                            other_uses[g] = (ent & (g == 0 ? kUseB : kUseA)) != 0 && hasB;
+                        }
                     }
                     mma_commit(&k_empty[ki]);
-                    mma_commit(&s_full[sb]);
-                    ++s_use[sb];
-                    sb ^= 1;
                     if (++ki == C::KS) { ki = 0; kph ^= 1; }
-                    if (j == n - 1) {
-                        mma_commit(&q_empty[qi]);
-                        if (++qi == C::QS) { qi = 0; qph ^= 1; }
-                    }
-                    if (j > 0) issue_pv(j - 1 == 0);
                 }
-                issue_pv(n == 1);
+                for (int g = 0; g < ng; ++g) {
+                    if (pend[g]) issue_pv(g);
+                    mma_commit(&epi[g]);
+                    const int slot = g * C::QS + qi[g];
+                    mma_commit(&q_empty[slot]);
+                    if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
+                }
             }
         }
-    } else {
+    } else if (warp >= 4) {
         // ------------------------------------------------------------ softmax warps
-        const int quad = warp & 3;              // TMEM lane quadrant this warp may access
+        const int g = (warp - 4) >> 2;          // tile group: 0 = A, 1 = B
+        const int quad = warp & 3;              // TMEM lane quadrant of this warp
         const int r = quad * 32 + lane;         // row within the query tile
-        const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
-        const uint32_t sP = smem_u32(smem + C::OFF_P);
-        uint32_t s_use[2] = {0, 0}, p_use[2] = {0, 0};
-        int sb = 0;
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const uint32_t s_tm = tmem + lane_off + g * 128;
+        const uint32_t o_tm = tmem + lane_off + 256 + g * D;
+        const int use_bit = g == 0 ? kUseA : kUseB, part_bit = g == 0 ? kPartA : kPartB;
+        const float c2 = prm.scale_log2;
+        uint32_t s_cnt = 0, e_cnt = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const int t = A.order[u / prm.BH], bh = u % prm.BH;
-            const int e0 = A.qt_ptr[t], n = A.qt_ptr[t + 1] - e0;
+            int pair, bh;
+            unit_at(A, prm.BH, u, pair, bh);
+            const int t = 2 * pair + g;
+            if (t >= A.n_qt) continue;
             const int row = t * 128 + r;
-            int4 g[3];
-            int ns = 0;
+            int4 sg0 = make_int4(0, 1, 0, 0), sg1 = sg0, sg2 = sg0;
             if (row < A.n) {
-                ns = A.nseg[row];
-#pragma unroll
-                for (int s = 0; s < 3; ++s) g[s] = A.seg[(size_t)row * 4 + s];
+                const int ns = A.nseg[row];
+                if (ns > 0) sg0 = A.seg[(size_t)row * 4 + 0];
+                if (ns > 1) sg1 = A.seg[(size_t)row * 4 + 1];
+                if (ns > 2) sg2 = A.seg[(size_t)row * 4 + 2];
             }
             float m_run = -INFINITY, l_run = 0.f;
-            for (int j = 0; j < n; ++j) {
-                const int ent = A.kv[e0 + j];
+            bool first = true;
+            const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
+            for (int e = e0; e < e1; ++e) {
+                const int ent = A.pair_ent[e];
+                if (!(ent & use_bit)) continue;
                 const int kv0 = (ent & kKvMask) * 128;
-                const bool partial = (ent & kPartialBit) != 0;
                 float s[128];
-                mbar_wait(&s_full[sb], s_use[sb] & 1);
+                mbar_wait(&s_full[g], s_cnt & 1);
+                ++s_cnt;
                 tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld32(lane_addr + sb * 128 + c * 32, s + 32 * c);
+                for (int c = 0; c < 4; ++c) tmem_ld32(s_tm + c * 32, s + 32 * c);
                 tmem_wait_ld();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&s_empty[sb]);
-                ++s_use[sb];
-                const int pb = sb;   // P buffer follows the S buffer parity (= j & 1 within the stream)
-                sb ^= 1;
-                if (partial) {
+                uint32_t live = 0xF;     // 32-column chunks with any valid entry in this warp
+                if (ent & part_bit) {
                     uint32_t mk[4] = {0, 0, 0, 0};
+                    const int4 sgs[3] = {sg0, sg1, sg2};
 #pragma unroll
                     for (int q = 0; q < 3; ++q) {
-                        if (q < ns) {
-                            const int start = g[q].x, step = g[q].y, cnt = g[q].z;
-                            const int last = start + step * (cnt - 1);
-                            const int lo = max(start, kv0), hi = min(last, kv0 + 127);
-                            if (lo <= hi) {
-                                if (step == 1) {
-                                    set_bits(mk, lo - kv0, hi - kv0);
-                                } else {
+                        const int start = sgs[q].x, step = sgs[q].y, cnt = sgs[q].z;
+                        if (cnt <= 0) continue;
+                        const int last = start + step * (cnt - 1);
+                        const int lo = max(start, kv0), hi = min(last, kv0 + 127);
+                        if (lo > hi) continue;
+                        if (step == 1) {
+                            set_bits(mk, lo - kv0, hi - kv0);
+                        } else {
 #pragma unroll
-                                    for (int w = 0; w < 4; ++w) {
-                                        const int a = max(lo, kv0 + 32 * w), b = min(hi, kv0 + 32 * w + 31);
-                                        const int first = start + ((a - start + step - 1) / step) * step;
-                                        uint32_t bits = 0;
-                                        for (int c = first; c <= b; c += step) bits |= 1u << (c - kv0 - 32 * w);
-                                        mk[w] |= bits;
-                                    }
-                                }
+                            for (int w = 0; w < 4; ++w) {
+                                const int a = max(lo, kv0 + 32 * w), b = min(hi, kv0 + 32 * w + 31);
+                                const int f = start + ((a - start + step - 1) / step) * step;
+                                uint32_t bits = 0;
+                                for (int c = f; c <= b; c += step) bits |= 1u << (c - kv0 - 32 * w);
+                                mk[w] |= bits;
                             }
                         }
                     }
+                    live = 0;
 #pragma unroll
-                    for (int x = 0; x < 128; ++x)
-                        if (!((mk[x >> 5] >> (x & 31)) & 1u)) s[x] = -INFINITY;
+                    for (int w = 0; w < 4; ++w) {
+                        if (__any_sync(0xffffffffu, mk[w] != 0)) live |= 1u << w;
+#pragma unroll
+                        for (int x = 0; x < 32; ++x)
+                            s[32 * w + x] = ((mk[w] >> x) & 1u) ? s[32 * w + x] : -INFINITY;
+                    }
                 }
-                float mx = s[0];
+                // row max (3-input max tree)
+                float mx = -INFINITY;
 #pragma unroll
-                for (int x = 1; x < 128; ++x) mx = fmaxf(mx, s[x]);
-                mx *= prm.scale_log2;
+                for (int w = 0; w < 4; ++w) {
+                    if (live & (1u << w)) {
+                        float a0 = fmax3(s[32 * w + 0], s[32 * w + 1], s[32 * w + 2]);
+                        float a1 = fmax3(s[32 * w + 3], s[32 * w + 4], s[32 * w + 5]);
+                        float a2 = fmax3(s[32 * w + 6], s[32 * w + 7], s[32 * w + 8]);
+                        float a3 = fmax3(s[32 * w + 9], s[32 * w + 10], s[32 * w + 11]);
+#pragma unroll
+                        for (int x = 12; x < 32; x += 8) {
+                            a0 = fmax3(a0, s[32 * w + x + 0], s[32 * w + x + 1]);
+                            a1 = fmax3(a1, s[32 * w + x + 2], s[32 * w + x + 3]);
+                            a2 = fmax3(a2, s[32 * w + x + 4], s[32 * w + x + 5]);
+                            a3 = fmax3(a3, s[32 * w + x + 6], s[32 * w + x + 7]);
+                        }
+                        mx = fmax3(mx, fmax3(a0, a1, a2), a3);
+                    }
+                }
+                mx *= c2;
                 float alpha = 1.f;
                 bool resc = false;
                 if (mx > m_run + kRescaleThresh) {
@@ -293,73 +406,85 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     m_run = mx;
                     l_run *= alpha;
                 }
-                const float mref = m_run == -INFINITY ? 0.f : m_run;
-                float ls = 0.f;
-                // P buffer must be free: PV of its previous use complete
-                if (p_use[pb] > 0) mbar_wait(&p_empty[pb], (p_use[pb] - 1) & 1);
-                const uint32_t prow = sP + pb * C::kPBytes + r * 128;
-#pragma unroll
-                for (int c16 = 0; c16 < 16; ++c16) {
-                    uint32_t w[4];
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        const float p0 = ex2(fmaf(s[c16 * 8 + 2 * h], prm.scale_log2, -mref));
-                        const float p1 = ex2(fmaf(s[c16 * 8 + 2 * h + 1], prm.scale_log2, -mref));
-                        ls += p0 + p1;
-                        w[h] = pack_bf16(p0, p1);
-                    }
-                    const uint32_t addr = prow + (c16 >> 3) * kTileBytes64 + (((c16 & 7) ^ (r & 7)) << 4);
-                    st_shared_v4(addr, w[0], w[1], w[2], w[3]);
-                }
-                l_run += ls;
-                fence_proxy_async_smem();
-                // rescale O (TMEM) when some row of this warp moved its max by > 2^8
-                if (__any_sync(0xffffffffu, resc) && j > 0) {
-                    const int pprev = pb ^ 1;   // PV_{j-1} used the other P buffer
-                    mbar_wait(&p_empty[pprev], (p_use[pprev] - 1) & 1);
-                    tc_fence_after();
+                if (!first && __any_sync(0xffffffffu, resc)) {
+                    // O holds PV up to the previous entry (complete: s_full tracks it)
 #pragma unroll
                     for (int c = 0; c < D / 32; ++c) {
                         float o[32];
-                        tmem_ld32(lane_addr + 256 + c * 32, o);
+                        tmem_ld32(o_tm + c * 32, o);
                         tmem_wait_ld();
 #pragma unroll
                         for (int x = 0; x < 32; ++x) o[x] *= alpha;
-                        tmem_st32(lane_addr + 256 + c * 32, o);
+                        tmem_st32(o_tm + c * 32, o);
                     }
-                    tmem_wait_st();
                 }
-                ++p_use[pb];
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&p_full[pb]);
-            }
-            // epilogue: wait for the last PV, O / l -> bf16 -> HBM
-            {
-                const int pl = (sb ^ 1);     // buffer of the last P
-                mbar_wait(&p_empty[pl], (p_use[pl] - 1) & 1);
-                tc_fence_after();
-                const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-                __nv_bfloat16 *orow = prm.O + ((size_t)bh * prm.N + row) * D;
+                const float mref = m_run == -INFINITY ? 0.f : m_run;
+                const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
+                uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
-                for (int c = 0; c < D / 32; ++c) {
-                    float o[32];
-                    tmem_ld32(lane_addr + 256 + c * 32, o);
-                    tmem_wait_ld();
-                    if (row < prm.N) {
+                for (int h = 0; h < 2; ++h) {           // two halves of 64 columns -> 32 packed P columns
+                    uint32_t pw[32];
 #pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            uint4 w;
-                            w.x = pack_bf16(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
-                            w.y = pack_bf16(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
-                            w.z = pack_bf16(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
-                            w.w = pack_bf16(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
-                            *reinterpret_cast<uint4 *>(orow + c * 32 + 8 * v) = w;
+                    for (int w2 = 0; w2 < 2; ++w2) {
+                        const int w = 2 * h + w2;
+                        if (live & (1u << w)) {
+#pragma unroll
+                            for (int x = 0; x < 32; x += 4) {
+                                const uint64_t z0 = ffma2(pack2(s[32 * w + x], s[32 * w + x + 1]), cc, mm);
+                                const uint64_t z1 = ffma2(pack2(s[32 * w + x + 2], s[32 * w + x + 3]), cc, mm);
+                                float a, b, c, d;
+                                unpack2(z0, a, b);
+                                unpack2(z1, c, d);
+                                a = ex2(a); b = ex2(b); c = ex2(c); d = ex2(d);
+                                acc0 = fadd2(acc0, pack2(a, b));
+                                acc1 = fadd2(acc1, pack2(c, d));
+                                pw[16 * w2 + x / 2] = pack_bf16(a, b);
+                                pw[16 * w2 + x / 2 + 1] = pack_bf16(c, d);
+                            }
+                        } else {
+#pragma unroll
+                            for (int x = 0; x < 16; ++x) pw[16 * w2 + x] = 0u;
                         }
                     }
+                    // P (bf16 pairs) over S columns [32h, 32h+32): chunk h's S values are already in registers
+                    tmem_st32(s_tm + 32 * h, reinterpret_cast<const float *>(pw));
                 }
+                {
+                    float a, b, c, d;
+                    unpack2(acc0, a, b);
+                    unpack2(acc1, c, d);
+                    l_run += (a + b) + (c + d);
+                }
+                tmem_wait_st();
                 tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[g]);
+                first = false;
             }
+            // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
+            mbar_wait(&epi[g], e_cnt & 1);
+            ++e_cnt;
+            tc_fence_after();
+            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+            __nv_bfloat16 *orow = prm.O + ((size_t)bh * prm.N + row) * D;
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                float o[32];
+                tmem_ld32(o_tm + c * 32, o);
+                tmem_wait_ld();
+                if (row < prm.N) {
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        uint4 w4;
+                        w4.x = pack_bf16(inv == 0.f ? 0.f : o[8 * v + 0] * inv, inv == 0.f ? 0.f : o[8 * v + 1] * inv);
+                        w4.y = pack_bf16(inv == 0.f ? 0.f : o[8 * v + 2] * inv, inv == 0.f ? 0.f : o[8 * v + 3] * inv);
+                        w4.z = pack_bf16(inv == 0.f ? 0.f : o[8 * v + 4] * inv, inv == 0.f ? 0.f : o[8 * v + 5] * inv);
+                        w4.w = pack_bf16(inv == 0.f ? 0.f : o[8 * v + 6] * inv, inv == 0.f ? 0.f : o[8 * v + 7] * inv);
+                        *reinterpret_cast<uint4 *>(orow + c * 32 + 8 * v) = w4;
+                    }
+                }
+            }
+            tc_fence_before();
         }
     }
     __syncthreads();
@@ -430,7 +555,7 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     p.N = A.n;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.O = reinterpret_cast<__nv_bfloat16 *>(O);
-    const long long units = (long long)A.n_qt * BH;
+    const long long units = (long long)A.n_pairs * BH;
     const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
     mhsa_tc_kernel<D><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, p);
     return cudaGetLastError();
