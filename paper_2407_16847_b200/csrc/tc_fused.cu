@@ -184,6 +184,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
         if (lane == 0) {
             int qi[2] = {0, 0}, qc[2] = {0, 0};
             uint32_t qph[2] = {0, 0};
@@ -192,9 +193,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 int pair, bh;
                 unit_at(A, prm.BH, u, pair, bh);
+#pragma unroll
                 for (int g = 0; g < 2; ++g) {
                     const int t = 2 * pair + g;
-                    if (t >= A.n_qt) break;
+                    if (t >= A.n_qt) continue;
                     const int slot = g * C::QS + qi[g];
                     if (qc[g] >= C::QS) mbar_wait(&q_empty[slot], qph[g] ^ 1);
                     mbar_expect_tx(&q_full[slot], C::kTileBytes);
@@ -229,6 +231,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(128, 128, false);
             constexpr uint32_t idO = idesc_bf16(128, D, true);
@@ -245,7 +248,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const bool hasB = 2 * pair + 1 < A.n_qt;
                 const int ng = hasB ? 2 : 1;
                 uint32_t qbase[2];
-                for (int g = 0; g < ng; ++g) {
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    if (g >= ng) continue;
                     const int slot = g * C::QS + qi[g];
                     mbar_wait(&q_full[slot], qph[g]);
                     qbase[g] = sQ + slot * C::kTileBytes;
@@ -278,7 +283,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     mbar_wait(&v_full[ki], kph);
                     tc_fence_after();
                     const uint32_t kbase = sK + ki * C::kTileBytes;
-                    for (int g = 0; g < ng; ++g) {
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        if (g >= ng) continue;
                         if (pend[g]) issue_pv(g);
                         if (ent & (g == 0 ? kUseA : kUseB)) {
 #pragma unroll
@@ -296,7 +303,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     mma_commit(&k_empty[ki]);
                     if (++ki == C::KS) { ki = 0; kph ^= 1; }
                 }
-                for (int g = 0; g < ng; ++g) {
+#pragma unroll
+                for (int g = 0; g < 2; ++g) {
+                    if (g >= ng) continue;
                     if (pend[g]) issue_pv(g);
                     mma_commit(&epi[g]);
                     const int slot = g * C::QS + qi[g];
@@ -307,6 +316,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ softmax warps
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
         const int g = (warp - 4) >> 2;          // tile group: 0 = A, 1 = B
         const int quad = warp & 3;              // TMEM lane quadrant of this warp
         const int r = quad * 32 + lane;         // row within the query tile
