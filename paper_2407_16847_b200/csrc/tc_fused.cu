@@ -184,7 +184,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
         if (lane == 0) {
             int qi[2] = {0, 0}, qc[2] = {0, 0};
             uint32_t qph[2] = {0, 0};
@@ -231,7 +230,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(128, 128, false);
             constexpr uint32_t idO = idesc_bf16(128, D, true);
@@ -316,7 +314,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ softmax warps
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
         const int g = (warp - 4) >> 2;          // tile group: 0 = A, 1 = B
         const int quad = warp & 3;              // TMEM lane quadrant of this warp
         const int r = quad * 32 + lane;         // row within the query tile
@@ -346,16 +343,14 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const int ent = A.pair_ent[e];
                 if (!(ent & use_bit)) continue;
                 const int kv0 = (ent & kKvMask) * 128;
-                float s[128];
                 mbar_wait(&s_full[g], s_cnt & 1);
                 ++s_cnt;
                 tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld32(s_tm + c * 32, s + 32 * c);
-                tmem_wait_ld();
+                const bool partial = (ent & part_bit) != 0;
+                uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
                 uint32_t live = 0xF;     // 32-column chunks with any valid entry in this warp
-                if (ent & part_bit) {
-                    uint32_t mk[4] = {0, 0, 0, 0};
+                if (partial) {
+                    mk[0] = mk[1] = mk[2] = mk[3] = 0u;
                     const int4 sgs[3] = {sg0, sg1, sg2};
 #pragma unroll
                     for (int q = 0; q < 3; ++q) {
@@ -379,28 +374,29 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     }
                     live = 0;
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
+                    for (int w = 0; w < 4; ++w)
                         if (__any_sync(0xffffffffu, mk[w] != 0)) live |= 1u << w;
-#pragma unroll
-                        for (int x = 0; x < 32; ++x)
-                            s[32 * w + x] = ((mk[w] >> x) & 1u) ? s[32 * w + x] : -INFINITY;
-                    }
                 }
-                // row max (3-input max tree)
+                // pass 1: row max over the live chunks (3-input max tree)
                 float mx = -INFINITY;
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
                     if (live & (1u << w)) {
-                        float a0 = fmax3(s[32 * w + 0], s[32 * w + 1], s[32 * w + 2]);
-                        float a1 = fmax3(s[32 * w + 3], s[32 * w + 4], s[32 * w + 5]);
-                        float a2 = fmax3(s[32 * w + 6], s[32 * w + 7], s[32 * w + 8]);
-                        float a3 = fmax3(s[32 * w + 9], s[32 * w + 10], s[32 * w + 11]);
+                        float v[32];
+                        tmem_ld32(s_tm + 32 * w, v);
+                        tmem_wait_ld();
+                        if (partial) {
+#pragma unroll
+                            for (int x = 0; x < 32; ++x) v[x] = ((mk[w] >> x) & 1u) ? v[x] : -INFINITY;
+                        }
+                        float a0 = fmax3(v[0], v[1], v[2]), a1 = fmax3(v[3], v[4], v[5]);
+                        float a2 = fmax3(v[6], v[7], v[8]), a3 = fmax3(v[9], v[10], v[11]);
 #pragma unroll
                         for (int x = 12; x < 32; x += 8) {
-                            a0 = fmax3(a0, s[32 * w + x + 0], s[32 * w + x + 1]);
-                            a1 = fmax3(a1, s[32 * w + x + 2], s[32 * w + x + 3]);
-                            a2 = fmax3(a2, s[32 * w + x + 4], s[32 * w + x + 5]);
-                            a3 = fmax3(a3, s[32 * w + x + 6], s[32 * w + x + 7]);
+                            a0 = fmax3(a0, v[x + 0], v[x + 1]);
+                            a1 = fmax3(a1, v[x + 2], v[x + 3]);
+                            a2 = fmax3(a2, v[x + 4], v[x + 5]);
+                            a3 = fmax3(a3, v[x + 6], v[x + 7]);
                         }
                         mx = fmax3(mx, fmax3(a0, a1, a2), a3);
                     }
@@ -431,17 +427,27 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const float mref = m_run == -INFINITY ? 0.f : m_run;
                 const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
                 uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
+                // pass 2: exponentials; chunks 2h, 2h+1 -> P columns [32h, 32h+32) (their S is read first)
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {           // two halves of 64 columns -> 32 packed P columns
+                for (int h = 0; h < 2; ++h) {
                     uint32_t pw[32];
+                    float v[2][32];
+#pragma unroll
+                    for (int w2 = 0; w2 < 2; ++w2)
+                        if (live & (1u << (2 * h + w2))) tmem_ld32(s_tm + 32 * (2 * h + w2), v[w2]);
+                    tmem_wait_ld();
 #pragma unroll
                     for (int w2 = 0; w2 < 2; ++w2) {
                         const int w = 2 * h + w2;
                         if (live & (1u << w)) {
+                            if (partial) {
+#pragma unroll
+                                for (int x = 0; x < 32; ++x) v[w2][x] = ((mk[w] >> x) & 1u) ? v[w2][x] : -INFINITY;
+                            }
 #pragma unroll
                             for (int x = 0; x < 32; x += 4) {
-                                const uint64_t z0 = ffma2(pack2(s[32 * w + x], s[32 * w + x + 1]), cc, mm);
-                                const uint64_t z1 = ffma2(pack2(s[32 * w + x + 2], s[32 * w + x + 3]), cc, mm);
+                                const uint64_t z0 = ffma2(pack2(v[w2][x], v[w2][x + 1]), cc, mm);
+                                const uint64_t z1 = ffma2(pack2(v[w2][x + 2], v[w2][x + 3]), cc, mm);
                                 float a, b, c, d;
                                 unpack2(z0, a, b);
                                 unpack2(z1, c, d);
@@ -456,7 +462,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                             for (int x = 0; x < 16; ++x) pw[16 * w2 + x] = 0u;
                         }
                     }
-                    // P (bf16 pairs) over S columns [32h, 32h+32): chunk h's S values are already in registers
                     tmem_st32(s_tm + 32 * h, reinterpret_cast<const float *>(pw));
                 }
                 {
