@@ -44,7 +44,7 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kThreads = 320;            // warp 0 TMA, warp 1 MMA, warps 2-5 softmax A, 6-9 softmax B
+constexpr int kThreads = 384;            // WG0: warp 0 TMA, warp 1 MMA; WG1: softmax A; WG2: softmax B
 constexpr int kTileBytes64 = 128 * 128;  // [128 rows x 64 bf16] swizzle-128B sub-tile (16 KB)
 constexpr float kRescaleThresh = 8.0f;   // log2 units
 
@@ -58,8 +58,7 @@ struct Cfg {
     static constexpr int OFF_K = OFF_Q + 2 * QS * kTileBytes;
     static constexpr int OFF_V = OFF_K + KS * kTileBytes;
     static constexpr int OFF_BAR = OFF_V + KS * kTileBytes;
-    static constexpr int NBAR = 4 * QS + 4 * KS + 8;
-    static constexpr bool SEP = D == 64;        // P in its own TMEM columns
+    static constexpr int NBAR = 4 * QS + 4 * KS + 10;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
 };
 
@@ -145,29 +144,31 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         : "memory");
 }
 
-// Column mask of one row for key tile [kv0, kv0+128): bit x of mk[x/32] set iff column
-// kv0+x lies in one of the row's runs (fast-index predicate, reading A-7).
-__device__ __forceinline__ void row_mask(const int4 &sg0, const int4 &sg1, const int4 &sg2, int kv0,
-                                         uint32_t (&mk)[4])
+// Column mask of one row for the 64 columns [c0, c0+64): bit x of mk[x/32] set iff column
+// c0+x lies in one of the row's runs (fast-index predicate, reading A-7).
+__device__ __forceinline__ void row_mask64(const int4 &sg0, const int4 &sg1, const int4 &sg2, int c0,
+                                           uint32_t (&mk)[2])
 {
-    mk[0] = mk[1] = mk[2] = mk[3] = 0u;
+    mk[0] = mk[1] = 0u;
     const int4 sgs[3] = {sg0, sg1, sg2};
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         const int start = sgs[q].x, step = sgs[q].y, cnt = sgs[q].z;
         if (cnt <= 0) continue;
         const int last = start + step * (cnt - 1);
-        const int lo = max(start, kv0), hi = min(last, kv0 + 127);
+        const int lo = max(start, c0), hi = min(last, c0 + 63);
         if (lo > hi) continue;
-        if (step == 1) {
-            set_bits(mk, lo - kv0, hi - kv0);
-        } else {
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                const int a = max(lo, kv0 + 32 * w), b = min(hi, kv0 + 32 * w + 31);
+        for (int w = 0; w < 2; ++w) {
+            const int a = max(lo, c0 + 32 * w), b = min(hi, c0 + 32 * w + 31);
+            if (a > b) continue;
+            if (step == 1) {
+                const int n = b - a + 1;
+                mk[w] |= (n == 32 ? 0xffffffffu : ((1u << n) - 1u)) << (a - c0 - 32 * w);
+            } else {
                 const int f = start + ((a - start + step - 1) / step) * step;
                 uint32_t bits = 0;
-                for (int c = f; c <= b; c += step) bits |= 1u << (c - kv0 - 32 * w);
+                for (int c = f; c <= b; c += step) bits |= 1u << (c - c0 - 32 * w);
                 mk[w] |= bits;
             }
         }
@@ -208,15 +209,11 @@ __device__ __forceinline__ void exp32(const float *v, uint64_t cc, uint64_t mm, 
 }
 
 template <int D>
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kThreads, 1)
 mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const Params prm)
 {
     using C = Cfg<D>;
-    // SEP: P has its own TMEM columns (d = 64: S 2x128 + O 2x64 + P 2x64 = 512), so S is
-    // released as soon as the softmax has loaded it and the next S = Q K^T overlaps the
-    // exponentials.  Otherwise (d = 128: S 2x128 + O 2x128 = 512) P overwrites S.
-    constexpr bool SEP = C::SEP;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
@@ -224,10 +221,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     uint64_t *q_empty = q_full + 2 * C::QS;      // [2][QS]
     uint64_t *k_full = q_empty + 2 * C::QS, *k_empty = k_full + C::KS;
     uint64_t *v_full = k_empty + C::KS, *v_empty = v_full + C::KS;
-    uint64_t *s_full = v_empty + C::KS;          // [2]  MMA -> softmax: S_g ready
-    uint64_t *s_empty = s_full + 2;              // [2]  softmax -> MMA: S_g loaded (SEP only)
-    uint64_t *p_full = s_empty + 2;              // [2]  softmax -> MMA: P_g written, O_g rescaled
-    uint64_t *pv_done = p_full + 2;              // [2]  MMA -> softmax: PV_g complete
+    uint64_t *s_full = v_empty + C::KS;          // [2 groups][2 halves]  MMA -> softmax: S slot ready
+    uint64_t *p_full = s_full + 4;               // [2][2]  softmax -> MMA: P written (and O rescaled)
+    uint64_t *pv_done = p_full + 4;              // [2]     MMA -> softmax: PV complete
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + C::NBAR);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -238,12 +234,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         for (int i = 0; i < 2 * C::QS; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
         for (int i = 0; i < C::KS; ++i) {
             mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 2);
+            mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
         }
-        for (int g = 0; g < 2; ++g) {
-            mbar_init(&s_full[g], 1); mbar_init(&s_empty[g], 4);
-            mbar_init(&p_full[g], 4); mbar_init(&pv_done[g], 1);
-        }
+        for (int i = 0; i < 4; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
+        for (int g = 0; g < 2; ++g) mbar_init(&pv_done[g], 1);
         fence_mbar_init();
         tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
     }
@@ -301,8 +295,13 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
+        // Work of tile group g on key tile e is two half-steps (64 key columns each) using TMEM
+        // slot (g, h): S = Q_g K_e[64h:64h+64]^T (N = 64), then O_g += P V_e[64h:64h+64] with P
+        // (bf16) written by the softmax over the first 32 columns of the same slot.  Order per
+        // entry: for h, for g: [PV of the slot's previous half-step, S of this half-step], so each
+        // group always has the next S computed while its softmax works on the current one.
         if (lane == 0) {
-            constexpr uint32_t idS = idesc_bf16(128, 128, false);
+            constexpr uint32_t idS = idesc_bf16(128, 64, false);
             constexpr uint32_t idO = idesc_bf16(128, D, true);
             const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
             const uint32_t sV = smem_u32(smem + C::OFF_V);
@@ -310,8 +309,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             uint32_t qph0 = 0, qph1 = 0;
             int ki = 0;
             uint32_t kph = 0;
-            uint32_t pcnt0 = 0, pcnt1 = 0;     // p_full phases consumed
-            uint32_t scnt0 = 0, scnt1 = 0;     // QKs issued (s_empty phases, SEP)
+            uint32_t pc00 = 0, pc01 = 0, pc10 = 0, pc11 = 0;   // p_full uses per (group, half)
+            int outst[C::KS];                                  // PVs still to issue per V stage
+#pragma unroll
+            for (int i = 0; i < C::KS; ++i) outst[i] = 0;
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 int pair, bh;
                 unit_at(A, prm.BH, u, pair, bh);
@@ -319,71 +320,66 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const int slot0 = qi0, slot1 = C::QS + qi1;
                 mbar_wait(&q_full[slot0], qph0);
                 if (hasB) mbar_wait(&q_full[slot1], qph1);
-                tc_fence_after();
                 const uint32_t qb0 = sQ + slot0 * C::kTileBytes, qb1 = sQ + slot1 * C::kTileBytes;
-                bool pend0 = false, pend1 = false, first0 = true, first1 = true, oth0 = false, oth1 = false;
-                int vs0 = 0, vs1 = 0;
-#define SPLAT_ISSUE_PV(G)                                                                          \
-    do {                                                                                           \
-        mbar_wait(&p_full[G], pcnt##G & 1);                                                        \
-        ++pcnt##G;                                                                                 \
-        tc_fence_after();                                                                          \
-        const uint32_t vbase = sV + vs##G * C::kTileBytes;                                         \
-        const uint32_t ptm = tmem + (SEP ? 384 + G * 64 : G * 128);                                \
-        const uint32_t otm = tmem + 256 + G * D;                                                   \
-        _Pragma("unroll") for (int kk = 0; kk < 8; ++kk)                                           \
-        {                                                                                          \
-            const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);                 \
-            mma_bf16_ts(otm, ptm + kk * 8, b, idO, (first##G && kk == 0) ? 0u : 1u);               \
-        }                                                                                          \
-        first##G = false;                                                                          \
-        mma_commit(&v_empty[vs##G]);                                                               \
-        if (!oth##G) mbar_arrive(&v_empty[vs##G]);                                                 \
-        mma_commit(&pv_done[G]);                                                                   \
-        pend##G = false;                                                                           \
+                bool pd00 = false, pd01 = false, pd10 = false, pd11 = false;   // pending PV per (g, h)
+                int vs00 = 0, vs01 = 0, vs10 = 0, vs11 = 0;                   // its V stage
+                uint32_t vp00 = 0, vp01 = 0, vp10 = 0, vp11 = 0;              // its v_full parity
+                bool first0 = true, first1 = true;
+#define SPLAT_PV(G, H)                                                                                   \
+    do {                                                                                                 \
+        mbar_wait(&p_full[2 * G + H], pc##G##H & 1);                                                     \
+        ++pc##G##H;                                                                                      \
+        mbar_wait(&v_full[vs##G##H], vp##G##H);                                                          \
+        tc_fence_after();                                                                                \
+        const uint32_t vbase = sV + vs##G##H * C::kTileBytes + H * 4 * 2048;                             \
+        const uint32_t ptm = tmem + G * 128 + H * 64;                                                    \
+        _Pragma("unroll") for (int kk = 0; kk < 4; ++kk)                                                 \
+        {                                                                                                \
+            const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);                       \
+            mma_bf16_ts(tmem + 256 + G * D, ptm + kk * 8, b, idO, (first##G && kk == 0) ? 0u : 1u);      \
+        }                                                                                                \
+        first##G = false;                                                                                \
+        mma_commit(&pv_done[G]);                                                                         \
+        if (--outst[vs##G##H] == 0) mma_commit(&v_empty[vs##G##H]);                                     \
+        pd##G##H = false;                                                                                \
     } while (0)
-#define SPLAT_ISSUE_QK(G, QB)                                                                      \
-    do {                                                                                           \
-        if (SEP && scnt##G > 0) mbar_wait(&s_empty[G], (scnt##G - 1) & 1);                         \
-        tc_fence_after();                                                                          \
-        _Pragma("unroll") for (int kk = 0; kk < D / 16; ++kk)                                      \
-        {                                                                                          \
-            const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;                         \
-            mma_bf16_ss(tmem + G * 128, sdesc_sw128(QB + off, 16, 1024), sdesc_sw128(kbase + off, 16, 1024), \
-                        idS, kk > 0 ? 1u : 0u);                                                    \
-        }                                                                                          \
-        mma_commit(&s_full[G]);                                                                    \
-        ++scnt##G;                                                                                 \
+#define SPLAT_QK(G, H, QB)                                                                               \
+    do {                                                                                                 \
+        tc_fence_after();                                                                                \
+        _Pragma("unroll") for (int kk = 0; kk < D / 16; ++kk)                                            \
+        {                                                                                                \
+            const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;                               \
+            mma_bf16_ss(tmem + G * 128 + H * 64, sdesc_sw128(QB + off, 16, 1024),                        \
+                        sdesc_sw128(kbase + H * 8192 + off, 16, 1024), idS, kk > 0 ? 1u : 0u);           \
+        }                                                                                                \
+        mma_commit(&s_full[2 * G + H]);                                                                  \
+        pd##G##H = true;                                                                                 \
+        vs##G##H = ki;                                                                                   \
+        vp##G##H = kph;                                                                                  \
     } while (0)
                 const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
                 for (int e = e0; e < e1; ++e) {
                     const int ent = A.pair_ent[e];
                     const bool u0 = (ent & kUseA) != 0, u1 = hasB && (ent & kUseB) != 0;
+                    // a group that skips this key tile flushes its pending PVs now (frees V stages)
+                    if (!u0) { if (pd00) SPLAT_PV(0, 0); if (pd01) SPLAT_PV(0, 1); }
+                    if (!u1) { if (pd10) SPLAT_PV(1, 0); if (pd11) SPLAT_PV(1, 1); }
+                    outst[ki] = 2 * ((u0 ? 1 : 0) + (u1 ? 1 : 0));
                     mbar_wait(&k_full[ki], kph);
-                    mbar_wait(&v_full[ki], kph);
                     const uint32_t kbase = sK + ki * C::kTileBytes;
-                    if (SEP) {
-                        // S for this entry first (overlaps the softmax of the previous one), then PVs
-                        if (u0) SPLAT_ISSUE_QK(0, qb0);
-                        if (u1) SPLAT_ISSUE_QK(1, qb1);
-                        if (pend0) SPLAT_ISSUE_PV(0);
-                        if (pend1) SPLAT_ISSUE_PV(1);
-                    } else {
-                        // P aliases S: PV of the previous entry must precede the next S
-                        if (pend0) SPLAT_ISSUE_PV(0);
-                        if (u0) SPLAT_ISSUE_QK(0, qb0);
-                        if (pend1) SPLAT_ISSUE_PV(1);
-                        if (u1) SPLAT_ISSUE_QK(1, qb1);
-                    }
-                    if (u0) { pend0 = true; vs0 = ki; oth0 = u1; }
-                    if (u1) { pend1 = true; vs1 = ki; oth1 = u0; }
+                    if (u0) { if (pd00) SPLAT_PV(0, 0); SPLAT_QK(0, 0, qb0); }
+                    if (u1) { if (pd10) SPLAT_PV(1, 0); SPLAT_QK(1, 0, qb1); }
+                    if (u0) { if (pd01) SPLAT_PV(0, 1); SPLAT_QK(0, 1, qb0); }
+                    if (u1) { if (pd11) SPLAT_PV(1, 1); SPLAT_QK(1, 1, qb1); }
                     mma_commit(&k_empty[ki]);
                     if (++ki == C::KS) { ki = 0; kph ^= 1; }
                 }
-                if (pend0) SPLAT_ISSUE_PV(0);
-                if (pend1) SPLAT_ISSUE_PV(1);
-#undef SPLAT_ISSUE_PV
-#undef SPLAT_ISSUE_QK
+                if (pd00) SPLAT_PV(0, 0);
+                if (pd10) SPLAT_PV(1, 0);
+                if (pd01) SPLAT_PV(0, 1);
+                if (pd11) SPLAT_PV(1, 1);
+#undef SPLAT_PV
+#undef SPLAT_QK
                 mma_commit(&q_empty[slot0]);
                 if (++qi0 == C::QS) { qi0 = 0; qph0 ^= 1; }
                 if (hasB) {
@@ -392,18 +388,17 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 }
             }
         }
-    } else {
-        // ------------------------------------------------------------ softmax warps (2..5: A, 6..9: B)
-        const int g = (warp - 2) >> 2;          // tile group: 0 = A, 1 = B
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ softmax warps (4..7: A, 8..11: B)
+        const int g = (warp - 4) >> 2;          // tile group: 0 = A, 1 = B
         const int quad = warp & 3;              // TMEM lane quadrant of this warp
         const int r = quad * 32 + lane;         // row within the query tile
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t s_tm = tmem + lane_off + g * 128;
         const uint32_t o_tm = tmem + lane_off + 256 + g * D;
-        const uint32_t p_tm = tmem + lane_off + (SEP ? 384 + g * 64 : g * 128);
         const int use_bit = g == 0 ? kUseA : kUseB, part_bit = g == 0 ? kPartA : kPartB;
         const float c2 = prm.scale_log2;
-        uint32_t s_cnt = 0, k_cnt = 0;   // S tiles consumed; PVs requested (= p_full arrivals)
+        uint32_t j = 0;                          // half-steps done by this group (global)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int pair, bh;
             unit_at(A, prm.BH, u, pair, bh);
@@ -418,37 +413,31 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (ns > 2) sg2 = A.seg[(size_t)row * 4 + 2];
             }
             float m_run = -INFINITY, l_run = 0.f;
-            bool first = true;
+            const uint32_t j_first = j;
             const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
             for (int e = e0; e < e1; ++e) {
                 const int ent = A.pair_ent[e];
                 if (!(ent & use_bit)) continue;
-                const int kv0 = (ent & kKvMask) * 128;
                 const bool partial = (ent & part_bit) != 0;
-                uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
-                uint32_t live = 0xF;     // 32-column chunks with any valid entry in this warp
-                if (partial) {
-                    row_mask(sg0, sg1, sg2, kv0, mk);
-                    live = 0;
 #pragma unroll
-                    for (int w = 0; w < 4; ++w)
-                        if (__any_sync(0xffffffffu, mk[w] != 0)) live |= 1u << w;
-                }
-                mbar_wait(&s_full[g], s_cnt & 1);
-                ++s_cnt;
-                tc_fence_after();
-                float mx = -INFINITY;
-                float sv[SEP ? 128 : 1];
-                if constexpr (SEP) {
-                    // one pass: S -> registers, release S to the MMA warp right away
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) tmem_ld32(s_tm + 32 * w, sv + 32 * w);
+                for (int h = 0; h < 2; ++h, ++j) {
+                    const int c0 = (ent & kKvMask) * 128 + 64 * h;
+                    uint32_t mk[2] = {~0u, ~0u};
+                    uint32_t live = 3;       // 32-column chunks with any valid entry in this warp
+                    if (partial) {
+                        row_mask64(sg0, sg1, sg2, c0, mk);
+                        live = (__any_sync(0xffffffffu, mk[0] != 0) ? 1u : 0u) |
+                               (__any_sync(0xffffffffu, mk[1] != 0) ? 2u : 0u);
+                    }
+                    float sv[64];
+                    mbar_wait(&s_full[2 * g + h], (j >> 1) & 1);
+                    tc_fence_after();
+                    tmem_ld32(s_tm + 64 * h, sv);
+                    tmem_ld32(s_tm + 64 * h + 32, sv + 32);
                     tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&s_empty[g]);
+                    float mx = -INFINITY;
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
+                    for (int w = 0; w < 2; ++w) {
                         if (live & (1u << w)) {
                             if (partial) {
 #pragma unroll
@@ -458,114 +447,60 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                             mx = fmax3(mx, max32(sv + 32 * w), -INFINITY);
                         }
                     }
-                } else {
-                    // pass 1 of 2 (registers are short at d = 128): row max
+                    mx *= c2;
+                    float alpha = 1.f;
+                    bool resc = false;
+                    if (mx > m_run + kRescaleThresh) {
+                        if (m_run != -INFINITY) {
+                            alpha = ex2(m_run - mx);
+                            resc = true;
+                        }
+                        m_run = mx;
+                        l_run *= alpha;
+                    }
+                    if (j > j_first && __any_sync(0xffffffffu, resc)) {
+                        // every earlier PV of this tile must have landed in O before rescaling it
+                        mbar_wait(&pv_done[g], (j - 1) & 1);
+                        tc_fence_after();
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        if (live & (1u << w)) {
-                            float v[32];
-                            tmem_ld32(s_tm + 32 * w, v);
+                        for (int c = 0; c < D / 32; ++c) {
+                            float o[32];
+                            tmem_ld32(o_tm + c * 32, o);
                             tmem_wait_ld();
-                            if (partial) {
 #pragma unroll
-                                for (int x = 0; x < 32; ++x) v[x] = ((mk[w] >> x) & 1u) ? v[x] : -INFINITY;
-                            }
-                            mx = fmax3(mx, max32(v), -INFINITY);
+                            for (int x = 0; x < 32; ++x) o[x] *= alpha;
+                            tmem_st32(o_tm + c * 32, o);
                         }
                     }
-                }
-                mx *= c2;
-                float alpha = 1.f;
-                bool resc = false;
-                if (mx > m_run + kRescaleThresh) {
-                    if (m_run != -INFINITY) {
-                        alpha = ex2(m_run - mx);
-                        resc = true;
-                    }
-                    m_run = mx;
-                    l_run *= alpha;
-                }
-                if (SEP && k_cnt > 0) {
-                    // P_g buffer and O_g: the previous PV of this group must be complete
-                    mbar_wait(&pv_done[g], (k_cnt - 1) & 1);
-                    tc_fence_after();
-                }
-                if (!first && __any_sync(0xffffffffu, resc)) {
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
-                        float o[32];
-                        tmem_ld32(o_tm + c * 32, o);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int x = 0; x < 32; ++x) o[x] *= alpha;
-                        tmem_st32(o_tm + c * 32, o);
-                    }
-                }
-                const float mref = m_run == -INFINITY ? 0.f : m_run;
-                const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
-                uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
-                if constexpr (SEP) {
-                    // one 32-column chunk at a time -> 16 packed P columns
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        uint32_t pw[16];
-                        if (live & (1u << w)) {
-                            exp32(sv + 32 * w, cc, mm, acc0, acc1, pw);
-                        } else {
-#pragma unroll
-                            for (int x = 0; x < 16; ++x) pw[x] = 0u;
-                        }
-                        tmem_st16(p_tm + 16 * w, pw);
-                    }
-                } else
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                    const float mref = m_run == -INFINITY ? 0.f : m_run;
+                    const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
+                    uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
                     uint32_t pw[32];
-                    float v[SEP ? 1 : 2][32];
-                    if constexpr (!SEP) {
-                        // pass 2: chunks 2h, 2h+1 are read before P columns [32h, 32h+32) overwrite them
 #pragma unroll
-                        for (int w2 = 0; w2 < 2; ++w2)
-                            if (live & (1u << (2 * h + w2))) tmem_ld32(s_tm + 32 * (2 * h + w2), v[w2]);
-                        tmem_wait_ld();
-                    }
-#pragma unroll
-                    for (int w2 = 0; w2 < 2; ++w2) {
-                        const int w = 2 * h + w2;
+                    for (int w = 0; w < 2; ++w) {
                         if (live & (1u << w)) {
-                            float *x32;
-                            if constexpr (SEP) {
-                                x32 = sv + 32 * w;
-                            } else {
-                                x32 = v[w2];
-                                if (partial) {
-#pragma unroll
-                                    for (int x = 0; x < 32; ++x) x32[x] = ((mk[w] >> x) & 1u) ? x32[x] : -INFINITY;
-                                }
-                            }
-                            exp32(x32, cc, mm, acc0, acc1, pw + 16 * w2);
+                            exp32(sv + 32 * w, cc, mm, acc0, acc1, pw + 16 * w);
                         } else {
 #pragma unroll
-                            for (int x = 0; x < 16; ++x) pw[16 * w2 + x] = 0u;
+                            for (int x = 0; x < 16; ++x) pw[16 * w + x] = 0u;
                         }
                     }
-                    tmem_st32(p_tm + 32 * h, reinterpret_cast<const float *>(pw));
+                    // P (bf16 pairs) over the first 32 columns of the slot (S already in registers)
+                    tmem_st32(s_tm + 64 * h, reinterpret_cast<const float *>(pw));
+                    {
+                        float a, b, c, d;
+                        unpack2(acc0, a, b);
+                        unpack2(acc1, c, d);
+                        l_run += (a + b) + (c + d);
+                    }
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&p_full[2 * g + h]);
                 }
-                {
-                    float a, b, c, d;
-                    unpack2(acc0, a, b);
-                    unpack2(acc1, c, d);
-                    l_run += (a + b) + (c + d);
-                }
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&p_full[g]);
-                ++k_cnt;
-                first = false;
             }
             // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
-            mbar_wait(&pv_done[g], (k_cnt - 1) & 1);
+            mbar_wait(&pv_done[g], (j - 1) & 1);
             tc_fence_after();
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
             __nv_bfloat16 *orow = prm.O + ((size_t)bh * prm.N + row) * D;
