@@ -34,6 +34,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -67,6 +68,7 @@ struct Params {
     int BH, N;
     float scale_log2;
     __nv_bfloat16 *O;
+    int dbg;        // profiling aid only (SPLAT_TC_DEBUG): 1 = no MMAs issued, 2 = no softmax math
 };
 
 // unit u -> (pair, bh): buckets in order; inside a bucket, head-major.
@@ -84,19 +86,6 @@ __device__ __forceinline__ void unit_at(const DevAcsr &A, int BH, int u, int &pa
     }
     pair = 0;
     bh = 0;
-}
-
-__device__ __forceinline__ void set_bits(uint32_t (&m)[4], int lo, int hi)
-{
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-        const int a = max(lo, 32 * w), b = min(hi, 32 * w + 31);
-        if (a <= b) {
-            const int n = b - a + 1;
-            const uint32_t bits = n == 32 ? 0xffffffffu : ((1u << n) - 1u);
-            m[w] |= bits << (a - 32 * w);
-        }
-    }
 }
 
 __device__ __forceinline__ float fmax3(float a, float b, float c)
@@ -336,7 +325,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         _Pragma("unroll") for (int kk = 0; kk < 4; ++kk)                                                 \
         {                                                                                                \
             const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);                       \
-            mma_bf16_ts(tmem + 256 + G * D, ptm + kk * 8, b, idO, (first##G && kk == 0) ? 0u : 1u);      \
+            if (!(prm.dbg & 1)) mma_bf16_ts(tmem + 256 + G * D, ptm + kk * 8, b, idO, (first##G && kk == 0) ? 0u : 1u); \
         }                                                                                                \
         first##G = false;                                                                                \
         mma_commit(&pv_done[G]);                                                                         \
@@ -349,8 +338,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         _Pragma("unroll") for (int kk = 0; kk < D / 16; ++kk)                                            \
         {                                                                                                \
             const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;                               \
-            mma_bf16_ss(tmem + G * 128 + H * 64, sdesc_sw128(QB + off, 16, 1024),                        \
-                        sdesc_sw128(kbase + H * 8192 + off, 16, 1024), idS, kk > 0 ? 1u : 0u);           \
+            if (!(prm.dbg & 1))                                                                          \
+                mma_bf16_ss(tmem + G * 128 + H * 64, sdesc_sw128(QB + off, 16, 1024),                    \
+                            sdesc_sw128(kbase + H * 8192 + off, 16, 1024), idS, kk > 0 ? 1u : 0u);       \
         }                                                                                                \
         mma_commit(&s_full[2 * G + H]);                                                                  \
         pd##G##H = true;                                                                                 \
@@ -476,6 +466,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
                     uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
                     uint32_t pw[32];
+                    if (prm.dbg & 2) live = 0;
 #pragma unroll
                     for (int w = 0; w < 2; ++w) {
                         if (live & (1u << w)) {
@@ -592,6 +583,11 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     p.N = A.n;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.O = reinterpret_cast<__nv_bfloat16 *>(O);
+    static const int dbg = [] {
+        const char *e = getenv("SPLAT_TC_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    p.dbg = dbg;
     const long long units = (long long)A.n_pairs * BH;
     const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
     mhsa_tc_kernel<D><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, p);
