@@ -490,7 +490,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     if (lane == 0) mbar_arrive(&p_full[2 * g + h]);
                 }
             }
-            // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
+            // epilogue: wait for the last two PVs of this tile (phase parity is only unambiguous one
+            // phase ahead: S of step j implies PV j-2 done), then O / l -> bf16 -> HBM
+            if (j >= 2) mbar_wait(&pv_done[g], (j - 2) & 1);
             mbar_wait(&pv_done[g], (j - 1) & 1);
             tc_fence_after();
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
