@@ -389,6 +389,17 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const int use_bit = g == 0 ? kUseA : kUseB, part_bit = g == 0 ? kPartA : kPartB;
         const float c2 = prm.scale_log2;
         uint32_t j = 0;                          // half-steps done by this group (global)
+        // pv_done phases are consumed strictly in order (a parity wait is only unambiguous while
+        // the barrier is at most one phase ahead): PV k is consumed before P of step k+2 is
+        // handed over, which bounds the lead, and at the end of each tile.
+        uint32_t pv_seen = 0;
+#define WAIT_PV(k)                                                                                       \
+    do {                                                                                                 \
+        if (pv_seen <= (uint32_t)(k)) {                                                                  \
+            mbar_wait(&pv_done[g], (k) & 1);                                                             \
+            pv_seen = (k) + 1;                                                                           \
+        }                                                                                                \
+    } while (0)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int pair, bh;
             unit_at(A, prm.BH, u, pair, bh);
@@ -450,7 +461,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     }
                     if (j > j_first && __any_sync(0xffffffffu, resc)) {
                         // every earlier PV of this tile must have landed in O before rescaling it
-                        mbar_wait(&pv_done[g], (j - 1) & 1);
+                        WAIT_PV(j - 1);
                         tc_fence_after();
 #pragma unroll
                         for (int c = 0; c < D / 32; ++c) {
@@ -484,16 +495,15 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         unpack2(acc1, c, d);
                         l_run += (a + b) + (c + d);
                     }
+                    if (j > 0) WAIT_PV(j - 1);
                     tmem_wait_st();
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&p_full[2 * g + h]);
                 }
             }
-            // epilogue: wait for the last two PVs of this tile (phase parity is only unambiguous one
-            // phase ahead: S of step j implies PV j-2 done), then O / l -> bf16 -> HBM
-            if (j >= 2) mbar_wait(&pv_done[g], (j - 2) & 1);
-            mbar_wait(&pv_done[g], (j - 1) & 1);
+            // epilogue: wait for the last PV of this tile, then O / l -> bf16 -> HBM
+            WAIT_PV(j - 1);
             tc_fence_after();
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
             __nv_bfloat16 *orow = prm.O + ((size_t)bh * prm.N + row) * D;
@@ -516,6 +526,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             }
             tc_fence_before();
         }
+#undef WAIT_PV
     }
     __syncthreads();
     if (warp == 1) {
