@@ -244,7 +244,8 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
         for i in range(args.steps):
-            flush.fill_(float(i))                           # evict L2 (256 MiB > 126 MB)
+            if not args.no_flush:
+                flush.fill_(float(i))                       # evict L2 (256 MiB > 126 MB)
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
@@ -307,7 +308,7 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": cfg.dtype if cfg.dtype != "fp32" else "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "B": B, "H": H, "N": cfg.N, "d": cfg.d, "bh_per_rank": nbh,
                    "pattern": cfg.pattern.__dict__, "nnz_per_head": acsr.nnz, "density": acsr.density,
-                   "l2": "flushed before every timed step (256 MiB write)", "parallelism": f"bh-shard x{ws}"},
+                   "l2": "warm (diagnostic --no-flush)" if args.no_flush else "flushed before every timed step (256 MiB write)", "parallelism": f"bh-shard x{ws}"},
         "roofline": roof,
         "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
@@ -338,6 +339,7 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

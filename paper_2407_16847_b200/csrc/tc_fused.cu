@@ -71,6 +71,17 @@ struct Params {
     int dbg;        // profiling aid only (SPLAT_TC_DEBUG): 1 = no MMAs issued, 2 = no softmax math
 };
 
+// Profiling aid (SPLAT_TC_DEBUG & 4): clock64 timestamps of pipeline events in CTA 0.
+__device__ unsigned long long g_trace[4][2048];
+__device__ int g_trace_n[4];
+#define TRACE(R, TAG)                                                                                    \
+    do {                                                                                                 \
+        if ((prm.dbg & 4) && blockIdx.x == 0) {                                                          \
+            const int i_ = g_trace_n[R]++;                                                               \
+            if (i_ < 2048) g_trace[R][i_] = ((unsigned long long)(TAG) << 48) | (clock64() & 0xffffffffffffull); \
+        }                                                                                                \
+    } while (0)
+
 // unit u -> (pair, bh): buckets in order; inside a bucket, head-major.
 __device__ __forceinline__ void unit_at(const DevAcsr &A, int BH, int u, int &pair, int &bh)
 {
@@ -267,6 +278,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         mbar_wait(&k_empty[ki], kph ^ 1);
                         mbar_wait(&v_empty[ki], kph ^ 1);
                     }
+                    TRACE(0, 1);
                     mbar_expect_tx(&k_full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
@@ -310,27 +322,31 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 mbar_wait(&q_full[slot0], qph0);
                 if (hasB) mbar_wait(&q_full[slot1], qph1);
                 const uint32_t qb0 = sQ + slot0 * C::kTileBytes, qb1 = sQ + slot1 * C::kTileBytes;
-                bool pd00 = false, pd01 = false, pd10 = false, pd11 = false;   // pending PV per (g, h)
-                int vs00 = 0, vs01 = 0, vs10 = 0, vs11 = 0;                   // its V stage
-                uint32_t vp00 = 0, vp01 = 0, vp10 = 0, vp11 = 0;              // its v_full parity
+                // one pending PV per group: (slot h, V stage, v_full parity)
+                bool pd0 = false, pd1 = false;
+                int ph0 = 0, ph1 = 0, vs0 = 0, vs1 = 0;
+                uint32_t vp0 = 0, vp1 = 0;
                 bool first0 = true, first1 = true;
-#define SPLAT_PV(G, H)                                                                                   \
+#define SPLAT_PV(G, H, VS, VP)                                                                           \
     do {                                                                                                 \
-        mbar_wait(&p_full[2 * G + H], pc##G##H & 1);                                                     \
-        ++pc##G##H;                                                                                      \
-        mbar_wait(&v_full[vs##G##H], vp##G##H);                                                          \
+        const int h_ = (H), vs_ = (VS);                                                                  \
+        uint32_t &pcr = h_ ? pc##G##1 : pc##G##0;                                                        \
+        mbar_wait(&p_full[2 * G + h_], pcr & 1);                                                         \
+        TRACE(1, 3 + G);                                                                                 \
+        ++pcr;                                                                                           \
+        mbar_wait(&v_full[vs_], (VP));                                                                   \
         tc_fence_after();                                                                                \
-        const uint32_t vbase = sV + vs##G##H * C::kTileBytes + H * 4 * 2048;                             \
-        const uint32_t ptm = tmem + G * 128 + H * 64;                                                    \
+        const uint32_t vbase = sV + vs_ * C::kTileBytes + h_ * 4 * 2048;                                 \
+        const uint32_t ptm = tmem + G * 128 + h_ * 64;                                                   \
         _Pragma("unroll") for (int kk = 0; kk < 4; ++kk)                                                 \
         {                                                                                                \
             const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);                       \
-            if (!(prm.dbg & 1)) mma_bf16_ts(tmem + 256 + G * D, ptm + kk * 8, b, idO, (first##G && kk == 0) ? 0u : 1u); \
+            if (!(prm.dbg & 1))                                                                          \
+                mma_bf16_ts(tmem + 256 + G * D, ptm + kk * 8, b, idO, (first##G && kk == 0) ? 0u : 1u);  \
         }                                                                                                \
         first##G = false;                                                                                \
         mma_commit(&pv_done[G]);                                                                         \
-        if (--outst[vs##G##H] == 0) mma_commit(&v_empty[vs##G##H]);                                     \
-        pd##G##H = false;                                                                                \
+        if (--outst[vs_] == 0) mma_commit(&v_empty[vs_]);                                                \
     } while (0)
 #define SPLAT_QK(G, H, QB)                                                                               \
     do {                                                                                                 \
@@ -343,31 +359,41 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                             sdesc_sw128(kbase + H * 8192 + off, 16, 1024), idS, kk > 0 ? 1u : 0u);       \
         }                                                                                                \
         mma_commit(&s_full[2 * G + H]);                                                                  \
-        pd##G##H = true;                                                                                 \
-        vs##G##H = ki;                                                                                   \
-        vp##G##H = kph;                                                                                  \
+    } while (0)
+// S of this half-step first, then the PV of the group's previous half-step (whose P the
+// softmax finishes while this S is computed); the slot written by S was freed by the PV
+// issued one half-step earlier.
+#define SPLAT_STEP(G, H, QB)                                                                             \
+    do {                                                                                                 \
+        SPLAT_QK(G, H, QB);                                                                              \
+        if (pd##G) SPLAT_PV(G, ph##G, vs##G, vp##G);                                                     \
+        pd##G = true;                                                                                    \
+        ph##G = H;                                                                                       \
+        vs##G = ki;                                                                                      \
+        vp##G = kph;                                                                                     \
     } while (0)
                 const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
                 for (int e = e0; e < e1; ++e) {
                     const int ent = A.pair_ent[e];
                     const bool u0 = (ent & kUseA) != 0, u1 = hasB && (ent & kUseB) != 0;
-                    // a group that skips this key tile flushes its pending PVs now (frees V stages)
-                    if (!u0) { if (pd00) SPLAT_PV(0, 0); if (pd01) SPLAT_PV(0, 1); }
-                    if (!u1) { if (pd10) SPLAT_PV(1, 0); if (pd11) SPLAT_PV(1, 1); }
+                    // a group that skips this key tile flushes its pending PV now (frees V stages)
+                    if (!u0 && pd0) { SPLAT_PV(0, ph0, vs0, vp0); pd0 = false; }
+                    if (!u1 && pd1) { SPLAT_PV(1, ph1, vs1, vp1); pd1 = false; }
                     outst[ki] = 2 * ((u0 ? 1 : 0) + (u1 ? 1 : 0));
+                    TRACE(1, 1);
                     mbar_wait(&k_full[ki], kph);
+                    TRACE(1, 2);
                     const uint32_t kbase = sK + ki * C::kTileBytes;
-                    if (u0) { if (pd00) SPLAT_PV(0, 0); SPLAT_QK(0, 0, qb0); }
-                    if (u1) { if (pd10) SPLAT_PV(1, 0); SPLAT_QK(1, 0, qb1); }
-                    if (u0) { if (pd01) SPLAT_PV(0, 1); SPLAT_QK(0, 1, qb0); }
-                    if (u1) { if (pd11) SPLAT_PV(1, 1); SPLAT_QK(1, 1, qb1); }
+                    if (u0) SPLAT_STEP(0, 0, qb0);
+                    if (u1) SPLAT_STEP(1, 0, qb1);
+                    if (u0) SPLAT_STEP(0, 1, qb0);
+                    if (u1) SPLAT_STEP(1, 1, qb1);
                     mma_commit(&k_empty[ki]);
                     if (++ki == C::KS) { ki = 0; kph ^= 1; }
                 }
-                if (pd00) SPLAT_PV(0, 0);
-                if (pd10) SPLAT_PV(1, 0);
-                if (pd01) SPLAT_PV(0, 1);
-                if (pd11) SPLAT_PV(1, 1);
+                if (pd0) { SPLAT_PV(0, ph0, vs0, vp0); pd0 = false; }
+                if (pd1) { SPLAT_PV(1, ph1, vs1, vp1); pd1 = false; }
+#undef SPLAT_STEP
 #undef SPLAT_PV
 #undef SPLAT_QK
                 mma_commit(&q_empty[slot0]);
@@ -431,7 +457,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                                (__any_sync(0xffffffffu, mk[1] != 0) ? 2u : 0u);
                     }
                     float sv[64];
+                    if (lane == 0 && quad == 0) TRACE(2 + g, 1);
                     mbar_wait(&s_full[2 * g + h], (j >> 1) & 1);
+                    if (lane == 0 && quad == 0) TRACE(2 + g, 2);
                     tc_fence_after();
                     tmem_ld32(s_tm + 64 * h, sv);
                     tmem_ld32(s_tm + 64 * h + 32, sv + 32);
@@ -495,7 +523,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         unpack2(acc1, c, d);
                         l_run += (a + b) + (c + d);
                     }
+                    if (lane == 0 && quad == 0) TRACE(2 + g, 3);
                     if (j > 0) WAIT_PV(j - 1);
+                    if (lane == 0 && quad == 0) TRACE(2 + g, 4);
                     tmem_wait_st();
                     tc_fence_before();
                     __syncwarp();
@@ -608,6 +638,15 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
 }
 
 }  // namespace
+
+extern "C" int splat_debug_trace(unsigned long long *out, int *counts)
+{
+    cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
+    cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(g_trace_n));
+    int z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_trace_n, z, sizeof(z));
+    return 0;
+}
 
 cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, int d,
                            float scale, void *O, cudaStream_t st, int *n_launch)
