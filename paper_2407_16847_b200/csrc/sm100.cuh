@@ -51,6 +51,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity)
     return ok != 0;
 }
 
+// Non-blocking probe: true iff the phase with the given parity has completed.
+__device__ __forceinline__ bool mbar_test(const uint64_t *bar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     const uint32_t a = smem_u32(bar);

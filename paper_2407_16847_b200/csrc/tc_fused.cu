@@ -74,6 +74,7 @@ struct Params {
 // Profiling aid (SPLAT_TC_DEBUG & 4): clock64 timestamps of pipeline events in CTA 0.
 __device__ unsigned long long g_trace[4][2048];
 __device__ int g_trace_n[4];
+#ifdef SPLAT_TRACE
 #define TRACE(R, TAG)                                                                                    \
     do {                                                                                                 \
         if ((prm.dbg & 4) && blockIdx.x == 0) {                                                          \
@@ -81,6 +82,9 @@ __device__ int g_trace_n[4];
             if (i_ < 2048) g_trace[R][i_] = ((unsigned long long)(TAG) << 48) | (clock64() & 0xffffffffffffull); \
         }                                                                                                \
     } while (0)
+#else
+#define TRACE(R, TAG) do { } while (0)
+#endif
 
 // unit u -> (pair, bh): buckets in order; inside a bucket, head-major.
 __device__ __forceinline__ void unit_at(const DevAcsr &A, int BH, int u, int &pair, int &bh)
@@ -296,11 +300,12 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        // Work of tile group g on key tile e is two half-steps (64 key columns each) using TMEM
+        // Work of tile group g on key tile e is two half-steps (64 key columns each) in TMEM
         // slot (g, h): S = Q_g K_e[64h:64h+64]^T (N = 64), then O_g += P V_e[64h:64h+64] with P
-        // (bf16) written by the softmax over the first 32 columns of the same slot.  Order per
-        // entry: for h, for g: [PV of the slot's previous half-step, S of this half-step], so each
-        // group always has the next S computed while its softmax works on the current one.
+        // (bf16) written by the softmax over the first 32 columns of the same slot.  The issuer
+        // is event driven: it polls the load / P barriers and issues whatever is ready, S
+        // before PV, so neither tile group ever waits behind the other.  Constraints: S of
+        // step j needs PV of step j-2 issued (same slot; tcgen05 executes in issue order).
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(128, 64, false);
             constexpr uint32_t idO = idesc_bf16(128, D, true);
@@ -308,94 +313,100 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const uint32_t sV = smem_u32(smem + C::OFF_V);
             int qi0 = 0, qi1 = 0;
             uint32_t qph0 = 0, qph1 = 0;
-            int ki = 0;
-            uint32_t kph = 0;
-            uint32_t pc00 = 0, pc01 = 0, pc10 = 0, pc11 = 0;   // p_full uses per (group, half)
-            int outst[C::KS];                                  // PVs still to issue per V stage
-#pragma unroll
-            for (int i = 0; i < C::KS; ++i) outst[i] = 0;
+            uint32_t gbase = 0;                                  // entries loaded before this unit
+            uint32_t pc[2][2] = {{0, 0}, {0, 0}};                // p_full uses per (group, slot)
+            int kleft[C::KS], vleft[C::KS];                      // MMAs still to issue per stage
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 int pair, bh;
                 unit_at(A, prm.BH, u, pair, bh);
                 const bool hasB = 2 * pair + 1 < A.n_qt;
+                const int ng = hasB ? 2 : 1;
                 const int slot0 = qi0, slot1 = C::QS + qi1;
                 mbar_wait(&q_full[slot0], qph0);
                 if (hasB) mbar_wait(&q_full[slot1], qph1);
-                const uint32_t qb0 = sQ + slot0 * C::kTileBytes, qb1 = sQ + slot1 * C::kTileBytes;
-                // one pending PV per group: (slot h, V stage, v_full parity)
-                bool pd0 = false, pd1 = false;
-                int ph0 = 0, ph1 = 0, vs0 = 0, vs1 = 0;
-                uint32_t vp0 = 0, vp1 = 0;
-                bool first0 = true, first1 = true;
-#define SPLAT_PV(G, H, VS, VP)                                                                           \
-    do {                                                                                                 \
-        const int h_ = (H), vs_ = (VS);                                                                  \
-        uint32_t &pcr = h_ ? pc##G##1 : pc##G##0;                                                        \
-        mbar_wait(&p_full[2 * G + h_], pcr & 1);                                                         \
-        TRACE(1, 3 + G);                                                                                 \
-        ++pcr;                                                                                           \
-        mbar_wait(&v_full[vs_], (VP));                                                                   \
-        tc_fence_after();                                                                                \
-        const uint32_t vbase = sV + vs_ * C::kTileBytes + h_ * 4 * 2048;                                 \
-        const uint32_t ptm = tmem + G * 128 + h_ * 64;                                                   \
-        _Pragma("unroll") for (int kk = 0; kk < 4; ++kk)                                                 \
-        {                                                                                                \
-            const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);                       \
-            if (!(prm.dbg & 1))                                                                          \
-                mma_bf16_ts(tmem + 256 + G * D, ptm + kk * 8, b, idO, (first##G && kk == 0) ? 0u : 1u);  \
-        }                                                                                                \
-        first##G = false;                                                                                \
-        mma_commit(&pv_done[G]);                                                                         \
-        if (--outst[vs_] == 0) mma_commit(&v_empty[vs_]);                                                \
-    } while (0)
-#define SPLAT_QK(G, H, QB)                                                                               \
-    do {                                                                                                 \
-        tc_fence_after();                                                                                \
-        _Pragma("unroll") for (int kk = 0; kk < D / 16; ++kk)                                            \
-        {                                                                                                \
-            const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;                               \
-            if (!(prm.dbg & 1))                                                                          \
-                mma_bf16_ss(tmem + G * 128 + H * 64, sdesc_sw128(QB + off, 16, 1024),                    \
-                            sdesc_sw128(kbase + H * 8192 + off, 16, 1024), idS, kk > 0 ? 1u : 0u);       \
-        }                                                                                                \
-        mma_commit(&s_full[2 * G + H]);                                                                  \
-    } while (0)
-// S of this half-step first, then the PV of the group's previous half-step (whose P the
-// softmax finishes while this S is computed); the slot written by S was freed by the PV
-// issued one half-step earlier.
-#define SPLAT_STEP(G, H, QB)                                                                             \
-    do {                                                                                                 \
-        SPLAT_QK(G, H, QB);                                                                              \
-        if (pd##G) SPLAT_PV(G, ph##G, vs##G, vp##G);                                                     \
-        pd##G = true;                                                                                    \
-        ph##G = H;                                                                                       \
-        vs##G = ki;                                                                                      \
-        vp##G = kph;                                                                                     \
-    } while (0)
+                const uint32_t qbase[2] = {sQ + slot0 * C::kTileBytes, sQ + slot1 * C::kTileBytes};
                 const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
-                for (int e = e0; e < e1; ++e) {
-                    const int ent = A.pair_ent[e];
-                    const bool u0 = (ent & kUseA) != 0, u1 = hasB && (ent & kUseB) != 0;
-                    // a group that skips this key tile flushes its pending PV now (frees V stages)
-                    if (!u0 && pd0) { SPLAT_PV(0, ph0, vs0, vp0); pd0 = false; }
-                    if (!u1 && pd1) { SPLAT_PV(1, ph1, vs1, vp1); pd1 = false; }
-                    outst[ki] = 2 * ((u0 ? 1 : 0) + (u1 ? 1 : 0));
-                    TRACE(1, 1);
-                    mbar_wait(&k_full[ki], kph);
-                    TRACE(1, 2);
-                    const uint32_t kbase = sK + ki * C::kTileBytes;
-                    if (u0) SPLAT_STEP(0, 0, qb0);
-                    if (u1) SPLAT_STEP(1, 0, qb1);
-                    if (u0) SPLAT_STEP(0, 1, qb0);
-                    if (u1) SPLAT_STEP(1, 1, qb1);
-                    mma_commit(&k_empty[ki]);
-                    if (++ki == C::KS) { ki = 0; kph ^= 1; }
+                const int* ents = A.pair_ent;
+                auto uses = [&](int e, int g) { return (ents[e] & (g == 0 ? kUseA : kUseB)) != 0 && g < ng; };
+                auto next_used = [&](int e, int g) {
+                    while (e < e1 && !uses(e, g)) ++e;
+                    return e;
+                };
+                int qe[2], qh[2] = {0, 0}, pe[2], ph[2] = {0, 0}, pend[2] = {0, 0};
+                bool first[2] = {true, true};
+                qe[0] = pe[0] = next_used(e0, 0);
+                qe[1] = pe[1] = ng > 1 ? next_used(e0, 1) : e1;
+                int loaded = e0, vloaded = e0;
+                while (true) {
+                    bool progress = false;
+                    if (loaded < e1) {
+                        const uint32_t ge = gbase + (loaded - e0);
+                        if (mbar_test(&k_full[ge % C::KS], (ge / C::KS) & 1)) {
+                            const int users = (uses(loaded, 0) ? 1 : 0) + (uses(loaded, 1) ? 1 : 0);
+                            kleft[ge % C::KS] = 2 * users;
+                            vleft[ge % C::KS] = 2 * users;
+                            ++loaded;
+                            progress = true;
+                        }
+                    }
+                    if (vloaded < loaded) {
+                        const uint32_t ge = gbase + (vloaded - e0);
+                        if (mbar_test(&v_full[ge % C::KS], (ge / C::KS) & 1)) {
+                            ++vloaded;
+                            progress = true;
+                        }
+                    }
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        if (g >= ng) continue;
+                        // S = Q K^T for the next half-step (slot qh[g])
+                        if (qe[g] < loaded && pend[g] <= 1) {
+                            const uint32_t ge = gbase + (qe[g] - e0);
+                            const int st = ge % C::KS, h = qh[g];
+                            const uint32_t kbase = sK + st * C::kTileBytes + h * 8192;
+                            tc_fence_after();
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;
+                                if (!(prm.dbg & 1))
+                                    mma_bf16_ss(tmem + g * 128 + h * 64, sdesc_sw128(qbase[g] + off, 16, 1024),
+                                                sdesc_sw128(kbase + off, 16, 1024), idS, kk > 0 ? 1u : 0u);
+                            }
+                            mma_commit(&s_full[2 * g + h]);
+                            if (--kleft[st] == 0) mma_commit(&k_empty[st]);
+                            ++pend[g];
+                            if (h == 0) qh[g] = 1;
+                            else { qh[g] = 0; qe[g] = next_used(qe[g] + 1, g); }
+                            progress = true;
+                        }
+                        // O += P V for the oldest pending half-step
+                        if (pend[g] >= 1 && pe[g] < vloaded && mbar_test(&p_full[2 * g + ph[g]], pc[g][ph[g]] & 1)) {
+                            ++pc[g][ph[g]];
+                            const uint32_t ge = gbase + (pe[g] - e0);
+                            const int st = ge % C::KS, h = ph[g];
+                            const uint32_t vbase = sV + st * C::kTileBytes + h * 4 * 2048;
+                            const uint32_t ptm = tmem + g * 128 + h * 64;
+                            tc_fence_after();
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);
+                                if (!(prm.dbg & 1))
+                                    mma_bf16_ts(tmem + 256 + g * D, ptm + kk * 8, b, idO,
+                                                (first[g] && kk == 0) ? 0u : 1u);
+                            }
+                            first[g] = false;
+                            mma_commit(&pv_done[g]);
+                            if (--vleft[st] == 0) mma_commit(&v_empty[st]);
+                            --pend[g];
+                            if (h == 0) ph[g] = 1;
+                            else { ph[g] = 0; pe[g] = next_used(pe[g] + 1, g); }
+                            progress = true;
+                        }
+                    }
+                    if (qe[0] >= e1 && pend[0] == 0 && (ng < 2 || (qe[1] >= e1 && pend[1] == 0))) break;
+                    if (!progress) __nanosleep(20);
                 }
-                if (pd0) { SPLAT_PV(0, ph0, vs0, vp0); pd0 = false; }
-                if (pd1) { SPLAT_PV(1, ph1, vs1, vp1); pd1 = false; }
-#undef SPLAT_STEP
-#undef SPLAT_PV
-#undef SPLAT_QK
+                gbase += e1 - e0;
                 mma_commit(&q_empty[slot0]);
                 if (++qi0 == C::QS) { qi0 = 0; qph0 ^= 1; }
                 if (hasB) {
