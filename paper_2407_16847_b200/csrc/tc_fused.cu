@@ -342,6 +342,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     if (loaded < e1) {
                         const uint32_t ge = gbase + (loaded - e0);
                         if (mbar_test(&k_full[ge % C::KS], (ge / C::KS) & 1)) {
+                            TRACE(1, 30);
                             const int users = (uses(loaded, 0) ? 1 : 0) + (uses(loaded, 1) ? 1 : 0);
                             kleft[ge % C::KS] = 2 * users;
                             vleft[ge % C::KS] = 2 * users;
@@ -373,6 +374,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                                                 sdesc_sw128(kbase + off, 16, 1024), idS, kk > 0 ? 1u : 0u);
                             }
                             mma_commit(&s_full[2 * g + h]);
+                            TRACE(1, 10 + g);
                             if (--kleft[st] == 0) mma_commit(&k_empty[st]);
                             ++pend[g];
                             if (h == 0) qh[g] = 1;
@@ -396,6 +398,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                             }
                             first[g] = false;
                             mma_commit(&pv_done[g]);
+                            TRACE(1, 20 + g);
                             if (--vleft[st] == 0) mma_commit(&v_empty[st]);
                             --pend[g];
                             if (h == 0) ph[g] = 1;
@@ -475,6 +478,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     tmem_ld32(s_tm + 64 * h, sv);
                     tmem_ld32(s_tm + 64 * h + 32, sv + 32);
                     tmem_wait_ld();
+                    if (lane == 0 && quad == 0) TRACE(2 + g, 5);
                     float mx = -INFINITY;
 #pragma unroll
                     for (int w = 0; w < 2; ++w) {
@@ -515,6 +519,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     const float mref = m_run == -INFINITY ? 0.f : m_run;
                     const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
                     uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
+                    if (lane == 0 && quad == 0) TRACE(2 + g, 6);
                     uint32_t pw[32];
                     if (prm.dbg & 2) live = 0;
 #pragma unroll
@@ -527,6 +532,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         }
                     }
                     // P (bf16 pairs) over the first 32 columns of the slot (S already in registers)
+                    if (lane == 0 && quad == 0) TRACE(2 + g, 7);
                     tmem_st32(s_tm + 64 * h, reinterpret_cast<const float *>(pw));
                     {
                         float a, b, c, d;

@@ -29,4 +29,4 @@ for r in range(4):
     n = min(cnt[r], 2048)
     ev = [(int(x >> 48), int(x & 0xffffffffffff) - t0) for x in arr[r][:n]]
     print(names[r], "events", cnt[r])
-    print("  ", " ".join(f"{tag}@{t}" for tag, t in ev[:160]))
+    print("  ", " ".join(f"{tag}@{t}" for tag, t in ev))
