@@ -75,11 +75,13 @@ struct Params {
 __device__ unsigned long long g_trace[4][2048];
 __device__ int g_trace_n[4];
 #ifdef SPLAT_TRACE
+// per-role event counter lives in a register (tr_n, declared at the top of the kernel)
 #define TRACE(R, TAG)                                                                                    \
     do {                                                                                                 \
         if ((prm.dbg & 4) && blockIdx.x == 0) {                                                          \
-            const int i_ = g_trace_n[R]++;                                                               \
-            if (i_ < 2048) g_trace[R][i_] = ((unsigned long long)(TAG) << 48) | (clock64() & 0xffffffffffffull); \
+            if (tr_n < 2048) g_trace[R][tr_n] = ((unsigned long long)(TAG) << 48) | (clock64() & 0xffffffffffffull); \
+            ++tr_n;                                                                                      \
+            g_trace_n[R] = tr_n;                                                                         \
         }                                                                                                \
     } while (0)
 #else
@@ -233,6 +235,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevAcsr &A = prm.A;
     const int n_units = A.n_pairs * prm.BH;
+#ifdef SPLAT_TRACE
+    int tr_n = 0;
+#endif
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2 * C::QS; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
