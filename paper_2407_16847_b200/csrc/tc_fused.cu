@@ -59,7 +59,7 @@ struct Cfg {
     static constexpr int OFF_K = OFF_Q + 2 * QS * kTileBytes;
     static constexpr int OFF_V = OFF_K + KS * kTileBytes;
     static constexpr int OFF_BAR = OFF_V + KS * kTileBytes;
-    static constexpr int NBAR = 4 * QS + 4 * KS + 10;
+    static constexpr int NBAR = 4 * QS + 4 * KS + 6;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
 };
 
@@ -150,22 +150,22 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         : "memory");
 }
 
-// Column mask of one row for the 64 columns [c0, c0+64): bit x of mk[x/32] set iff column
+// Column mask of one row for the 128 columns [c0, c0+128): bit x of mk[x/32] set iff column
 // c0+x lies in one of the row's runs (fast-index predicate, reading A-7).
-__device__ __forceinline__ void row_mask64(const int4 &sg0, const int4 &sg1, const int4 &sg2, int c0,
-                                           uint32_t (&mk)[2])
+__device__ __forceinline__ void row_mask128(const int4 &sg0, const int4 &sg1, const int4 &sg2, int c0,
+                                            uint32_t (&mk)[4])
 {
-    mk[0] = mk[1] = 0u;
+    mk[0] = mk[1] = mk[2] = mk[3] = 0u;
     const int4 sgs[3] = {sg0, sg1, sg2};
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         const int start = sgs[q].x, step = sgs[q].y, cnt = sgs[q].z;
         if (cnt <= 0) continue;
         const int last = start + step * (cnt - 1);
-        const int lo = max(start, c0), hi = min(last, c0 + 63);
+        const int lo = max(start, c0), hi = min(last, c0 + 127);
         if (lo > hi) continue;
 #pragma unroll
-        for (int w = 0; w < 2; ++w) {
+        for (int w = 0; w < 4; ++w) {
             const int a = max(lo, c0 + 32 * w), b = min(hi, c0 + 32 * w + 31);
             if (a > b) continue;
             if (step == 1) {
@@ -214,6 +214,12 @@ __device__ __forceinline__ void exp32(const float *v, uint64_t cc, uint64_t mm, 
     }
 }
 
+__device__ __forceinline__ void apply_mask(float *v, uint32_t m)
+{
+#pragma unroll
+    for (int x = 0; x < 32; ++x) v[x] = ((m >> x) & 1u) ? v[x] : -INFINITY;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -227,9 +233,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     uint64_t *q_empty = q_full + 2 * C::QS;      // [2][QS]
     uint64_t *k_full = q_empty + 2 * C::QS, *k_empty = k_full + C::KS;
     uint64_t *v_full = k_empty + C::KS, *v_empty = v_full + C::KS;
-    uint64_t *s_full = v_empty + C::KS;          // [2 groups][2 halves]  MMA -> softmax: S slot ready
-    uint64_t *p_full = s_full + 4;               // [2][2]  softmax -> MMA: P written (and O rescaled)
-    uint64_t *pv_done = p_full + 4;              // [2]     MMA -> softmax: PV complete
+    uint64_t *s_full = v_empty + C::KS;          // [2]  MMA -> softmax: S_g ready
+    uint64_t *p_full = s_full + 2;               // [2]  softmax -> MMA: P_g written (O_g rescaled)
+    uint64_t *epi = p_full + 2;                  // [2]  MMA -> softmax: last PV of the tile done
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + C::NBAR);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -245,8 +251,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
             mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
         }
-        for (int i = 0; i < 4; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); }
-        for (int g = 0; g < 2; ++g) mbar_init(&pv_done[g], 1);
+        for (int g = 0; g < 2; ++g) { mbar_init(&s_full[g], 1); mbar_init(&p_full[g], 4); mbar_init(&epi[g], 1); }
         fence_mbar_init();
         tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
     }
@@ -257,37 +262,38 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ------------------------------------------------------------ TMA producer
-        if (lane == 0) {
-            int qi[2] = {0, 0}, qc[2] = {0, 0};
-            uint32_t qph[2] = {0, 0};
-            int ki = 0, kc = 0;
-            uint32_t kph = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                int pair, bh;
-                unit_at(A, prm.BH, u, pair, bh);
+        // ------------------------------------------------------------ TMA producer (warp-uniform loop)
+        int qi[2] = {0, 0}, qc[2] = {0, 0};
+        uint32_t qph[2] = {0, 0};
+        int ki = 0, kc = 0;
+        uint32_t kph = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            int pair, bh;
+            unit_at(A, prm.BH, u, pair, bh);
 #pragma unroll
-                for (int g = 0; g < 2; ++g) {
-                    const int t = 2 * pair + g;
-                    if (t >= A.n_qt) continue;
-                    const int slot = g * C::QS + qi[g];
-                    if (qc[g] >= C::QS) mbar_wait(&q_empty[slot], qph[g] ^ 1);
+            for (int g = 0; g < 2; ++g) {
+                const int t = 2 * pair + g;
+                if (t >= A.n_qt) continue;
+                const int slot = g * C::QS + qi[g];
+                if (qc[g] >= C::QS) mbar_wait(&q_empty[slot], qph[g] ^ 1);
+                if (lane == 0) {
                     mbar_expect_tx(&q_full[slot], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
                         tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ, &q_full[slot],
                                     64 * c, t * 128, bh);
-                    ++qc[g];
-                    if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
                 }
-                const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
-                for (int e = e0; e < e1; ++e) {
-                    const int kv = A.pair_ent[e] & kKvMask;
-                    if (kc >= C::KS) {
-                        mbar_wait(&k_empty[ki], kph ^ 1);
-                        mbar_wait(&v_empty[ki], kph ^ 1);
-                    }
-                    TRACE(0, 1);
+                ++qc[g];
+                if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
+            }
+            const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
+            for (int e = e0; e < e1; ++e) {
+                const int kv = A.pair_ent[e] & kKvMask;
+                if (kc >= C::KS) {
+                    mbar_wait(&k_empty[ki], kph ^ 1);
+                    mbar_wait(&v_empty[ki], kph ^ 1);
+                }
+                if (lane == 0) {
                     mbar_expect_tx(&k_full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
@@ -298,129 +304,126 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     for (int c = 0; c < C::kChunks; ++c)
                         tma_load_3d(smem + C::OFF_V + ki * C::kTileBytes + c * kTileBytes64, &tmV, &v_full[ki],
                                     64 * c, kv * 128, bh);
-                    ++kc;
-                    if (++ki == C::KS) { ki = 0; kph ^= 1; }
                 }
+                ++kc;
+                if (++ki == C::KS) { ki = 0; kph ^= 1; }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        // Work of tile group g on key tile e is two half-steps (64 key columns each) in TMEM
-        // slot (g, h): S = Q_g K_e[64h:64h+64]^T (N = 64), then O_g += P V_e[64h:64h+64] with P
-        // (bf16) written by the softmax over the first 32 columns of the same slot.  The issuer
-        // is event driven: it polls the load / P barriers and issues whatever is ready, S
-        // before PV, so neither tile group ever waits behind the other.  Constraints: S of
-        // step j needs PV of step j-2 issued (same slot; tcgen05 executes in issue order).
-        if (lane == 0) {
-            constexpr uint32_t idS = idesc_bf16(128, 64, false);
-            constexpr uint32_t idO = idesc_bf16(128, D, true);
-            const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
-            const uint32_t sV = smem_u32(smem + C::OFF_V);
-            int qi0 = 0, qi1 = 0;
-            uint32_t qph0 = 0, qph1 = 0;
-            uint32_t gbase = 0;                                  // entries loaded before this unit
-            uint32_t pc[2][2] = {{0, 0}, {0, 0}};                // p_full uses per (group, slot)
-            int kleft[C::KS], vleft[C::KS];                      // MMAs still to issue per stage
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                int pair, bh;
-                unit_at(A, prm.BH, u, pair, bh);
-                const bool hasB = 2 * pair + 1 < A.n_qt;
-                const int ng = hasB ? 2 : 1;
-                const int slot0 = qi0, slot1 = C::QS + qi1;
-                mbar_wait(&q_full[slot0], qph0);
-                if (hasB) mbar_wait(&q_full[slot1], qph1);
-                const uint32_t qbase[2] = {sQ + slot0 * C::kTileBytes, sQ + slot1 * C::kTileBytes};
-                const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
-                const int* ents = A.pair_ent;
-                auto uses = [&](int e, int g) { return (ents[e] & (g == 0 ? kUseA : kUseB)) != 0 && g < ng; };
-                auto next_used = [&](int e, int g) {
-                    while (e < e1 && !uses(e, g)) ++e;
-                    return e;
-                };
-                int qe[2], qh[2] = {0, 0}, pe[2], ph[2] = {0, 0}, pend[2] = {0, 0};
-                bool first[2] = {true, true};
-                qe[0] = pe[0] = next_used(e0, 0);
-                qe[1] = pe[1] = ng > 1 ? next_used(e0, 1) : e1;
-                int loaded = e0, vloaded = e0;
-                while (true) {
-                    bool progress = false;
-                    if (loaded < e1) {
-                        const uint32_t ge = gbase + (loaded - e0);
-                        if (mbar_test(&k_full[ge % C::KS], (ge / C::KS) & 1)) {
-                            TRACE(1, 30);
-                            const int users = (uses(loaded, 0) ? 1 : 0) + (uses(loaded, 1) ? 1 : 0);
-                            kleft[ge % C::KS] = 2 * users;
-                            vleft[ge % C::KS] = 2 * users;
-                            ++loaded;
-                            progress = true;
-                        }
+        // ------------------------------------------------------------ MMA issuer (warp-uniform)
+        // The whole warp runs the (uniform) issue loop so descriptors live in uniform registers;
+        // lane 0 issues every tcgen05.mma / commit.  Per tile group g the sequence is strictly
+        // S_g(j) = Q_g K_j^T, [P_g(j) ready] O_g += P_g(j) V_j, S_g(j+1) ... (P aliases S in TMEM).
+        // The issuer polls the load and P barriers and serves whichever group is ready, so the
+        // two groups ping-pong: one group's exponentials overlap the other group's MMAs.
+        constexpr uint32_t idS = idesc_bf16(128, 128, false);
+        constexpr uint32_t idO = idesc_bf16(128, D, true);
+        const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
+        const uint32_t sV = smem_u32(smem + C::OFF_V);
+        const bool leader = lane == 0;
+        int qi0 = 0, qi1 = 0;
+        uint32_t qph0 = 0, qph1 = 0;
+        uint32_t gbase = 0;                                  // entries loaded before this unit
+        uint32_t pc0 = 0, pc1 = 0;                           // p_full phases consumed per group
+        int kleft[C::KS], vleft[C::KS];                      // MMAs still to issue per stage
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            int pair, bh;
+            unit_at(A, prm.BH, u, pair, bh);
+            const bool hasB = 2 * pair + 1 < A.n_qt;
+            const int slot0 = qi0, slot1 = C::QS + qi1;
+            mbar_wait(&q_full[slot0], qph0);
+            if (hasB) mbar_wait(&q_full[slot1], qph1);
+            const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
+            const int *ents = A.pair_ent;
+            const int use0 = kUseA, use1 = hasB ? kUseB : 0;
+            auto next_used = [&](int e, int bit) {
+                while (e < e1 && !(ents[e] & bit)) ++e;
+                return e;
+            };
+            int qe0 = next_used(e0, use0), qe1 = use1 ? next_used(e0, use1) : e1;
+            int pe0 = qe0, pe1 = qe1;
+            bool pend0 = false, pend1 = false, first0 = true, first1 = true;
+            int loaded = e0, vloaded = e0;
+            while (true) {
+                bool progress = false;
+                if (loaded < e1) {
+                    const uint32_t ge = gbase + (loaded - e0);
+                    if (mbar_test(&k_full[ge % C::KS], (ge / C::KS) & 1)) {
+                        const int ent = ents[loaded];
+                        const int users = ((ent & use0) ? 1 : 0) + ((use1 && (ent & use1)) ? 1 : 0);
+                        kleft[ge % C::KS] = users;
+                        vleft[ge % C::KS] = users;
+                        ++loaded;
+                        progress = true;
                     }
-                    if (vloaded < loaded) {
-                        const uint32_t ge = gbase + (vloaded - e0);
-                        if (mbar_test(&v_full[ge % C::KS], (ge / C::KS) & 1)) {
-                            ++vloaded;
-                            progress = true;
-                        }
-                    }
-#pragma unroll
-                    for (int g = 0; g < 2; ++g) {
-                        if (g >= ng) continue;
-                        // S = Q K^T for the next half-step (slot qh[g])
-                        if (qe[g] < loaded && pend[g] <= 1) {
-                            const uint32_t ge = gbase + (qe[g] - e0);
-                            const int st = ge % C::KS, h = qh[g];
-                            const uint32_t kbase = sK + st * C::kTileBytes + h * 8192;
-                            tc_fence_after();
-#pragma unroll
-                            for (int kk = 0; kk < D / 16; ++kk) {
-                                const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;
-                                if (!(prm.dbg & 1))
-                                    mma_bf16_ss(tmem + g * 128 + h * 64, sdesc_sw128(qbase[g] + off, 16, 1024),
-                                                sdesc_sw128(kbase + off, 16, 1024), idS, kk > 0 ? 1u : 0u);
-                            }
-                            mma_commit(&s_full[2 * g + h]);
-                            TRACE(1, 10 + g);
-                            if (--kleft[st] == 0) mma_commit(&k_empty[st]);
-                            ++pend[g];
-                            if (h == 0) qh[g] = 1;
-                            else { qh[g] = 0; qe[g] = next_used(qe[g] + 1, g); }
-                            progress = true;
-                        }
-                        // O += P V for the oldest pending half-step
-                        if (pend[g] >= 1 && pe[g] < vloaded && mbar_test(&p_full[2 * g + ph[g]], pc[g][ph[g]] & 1)) {
-                            ++pc[g][ph[g]];
-                            const uint32_t ge = gbase + (pe[g] - e0);
-                            const int st = ge % C::KS, h = ph[g];
-                            const uint32_t vbase = sV + st * C::kTileBytes + h * 4 * 2048;
-                            const uint32_t ptm = tmem + g * 128 + h * 64;
-                            tc_fence_after();
-#pragma unroll
-                            for (int kk = 0; kk < 4; ++kk) {
-                                const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);
-                                if (!(prm.dbg & 1))
-                                    mma_bf16_ts(tmem + 256 + g * D, ptm + kk * 8, b, idO,
-                                                (first[g] && kk == 0) ? 0u : 1u);
-                            }
-                            first[g] = false;
-                            mma_commit(&pv_done[g]);
-                            TRACE(1, 20 + g);
-                            if (--vleft[st] == 0) mma_commit(&v_empty[st]);
-                            --pend[g];
-                            if (h == 0) ph[g] = 1;
-                            else { ph[g] = 0; pe[g] = next_used(pe[g] + 1, g); }
-                            progress = true;
-                        }
-                    }
-                    if (qe[0] >= e1 && pend[0] == 0 && (ng < 2 || (qe[1] >= e1 && pend[1] == 0))) break;
-                    if (!progress) __nanosleep(20);
                 }
-                gbase += e1 - e0;
-                mma_commit(&q_empty[slot0]);
-                if (++qi0 == C::QS) { qi0 = 0; qph0 ^= 1; }
-                if (hasB) {
-                    mma_commit(&q_empty[slot1]);
-                    if (++qi1 == C::QS) { qi1 = 0; qph1 ^= 1; }
+                if (vloaded < loaded) {
+                    const uint32_t ge = gbase + (vloaded - e0);
+                    if (mbar_test(&v_full[ge % C::KS], (ge / C::KS) & 1)) {
+                        ++vloaded;
+                        progress = true;
+                    }
                 }
+#define SPLAT_GROUP(G)                                                                                   \
+    do {                                                                                                 \
+        if (!pend##G && qe##G < loaded) {                                                                \
+            /* S_G = Q_G K^T into TMEM columns [128 G, 128 G + 128) */                                   \
+            const uint32_t ge = gbase + (qe##G - e0);                                                    \
+            const int st = ge % C::KS;                                                                   \
+            const uint32_t kbase = sK + st * C::kTileBytes, qb = sQ + slot##G * C::kTileBytes;           \
+            tc_fence_after();                                                                            \
+            if (leader) {                                                                                \
+                _Pragma("unroll") for (int kk = 0; kk < D / 16; ++kk)                                    \
+                {                                                                                        \
+                    const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;                       \
+                    if (!(prm.dbg & 1))                                                                  \
+                        mma_bf16_ss(tmem + G * 128, sdesc_sw128(qb + off, 16, 1024),                     \
+                                    sdesc_sw128(kbase + off, 16, 1024), idS, kk > 0 ? 1u : 0u);          \
+                }                                                                                        \
+                mma_commit(&s_full[G]);                                                                  \
+                if (--kleft[st] == 0) mma_commit(&k_empty[st]);                                          \
+            }                                                                                            \
+            TRACE(1, 10 + G);                                                                            \
+            pend##G = true;                                                                              \
+            progress = true;                                                                             \
+        }                                                                                                \
+        if (pend##G && pe##G < vloaded && mbar_test(&p_full[G], pc##G & 1)) {                            \
+            /* O_G += P_G V, P_G packed bf16 in TMEM columns [128 G, 128 G + 64) */                     \
+            ++pc##G;                                                                                     \
+            const uint32_t ge = gbase + (pe##G - e0);                                                    \
+            const int st = ge % C::KS;                                                                   \
+            const uint32_t vbase = sV + st * C::kTileBytes;                                              \
+            tc_fence_after();                                                                            \
+            if (leader) {                                                                                \
+                _Pragma("unroll") for (int kk = 0; kk < 8; ++kk)                                         \
+                {                                                                                        \
+                    const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);               \
+                    if (!(prm.dbg & 1))                                                                  \
+                        mma_bf16_ts(tmem + 256 + G * D, tmem + G * 128 + kk * 8, b, idO,                 \
+                                    (first##G && kk == 0) ? 0u : 1u);                                    \
+                }                                                                                        \
+                if (--vleft[st] == 0) mma_commit(&v_empty[st]);                                          \
+            }                                                                                            \
+            TRACE(1, 20 + G);                                                                            \
+            first##G = false;                                                                            \
+            pend##G = false;                                                                             \
+            pe##G = qe##G = next_used(qe##G + 1, use##G);                                                \
+            if (qe##G >= e1 && leader) mma_commit(&epi[G]);                                              \
+            progress = true;                                                                             \
+        }                                                                                                \
+    } while (0)
+                SPLAT_GROUP(0);
+                if (hasB) SPLAT_GROUP(1);
+#undef SPLAT_GROUP
+                if (qe0 >= e1 && !pend0 && (!hasB || (qe1 >= e1 && !pend1))) break;
+                if (!progress) __nanosleep(16);
+            }
+            gbase += e1 - e0;
+            if (leader) mma_commit(&q_empty[slot0]);
+            if (++qi0 == C::QS) { qi0 = 0; qph0 ^= 1; }
+            if (hasB) {
+                if (leader) mma_commit(&q_empty[slot1]);
+                if (++qi1 == C::QS) { qi1 = 0; qph1 ^= 1; }
             }
         }
     } else if (warp >= 4) {
@@ -433,18 +436,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const uint32_t o_tm = tmem + lane_off + 256 + g * D;
         const int use_bit = g == 0 ? kUseA : kUseB, part_bit = g == 0 ? kPartA : kPartB;
         const float c2 = prm.scale_log2;
-        uint32_t j = 0;                          // half-steps done by this group (global)
-        // pv_done phases are consumed strictly in order (a parity wait is only unambiguous while
-        // the barrier is at most one phase ahead): PV k is consumed before P of step k+2 is
-        // handed over, which bounds the lead, and at the end of each tile.
-        uint32_t pv_seen = 0;
-#define WAIT_PV(k)                                                                                       \
-    do {                                                                                                 \
-        if (pv_seen <= (uint32_t)(k)) {                                                                  \
-            mbar_wait(&pv_done[g], (k) & 1);                                                             \
-            pv_seen = (k) + 1;                                                                           \
-        }                                                                                                \
-    } while (0)
+        uint32_t s_cnt = 0, e_cnt = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int pair, bh;
             unit_at(A, prm.BH, u, pair, bh);
@@ -459,103 +451,110 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (ns > 2) sg2 = A.seg[(size_t)row * 4 + 2];
             }
             float m_run = -INFINITY, l_run = 0.f;
-            const uint32_t j_first = j;
+            bool first = true;
             const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
+            int ent_next = e0 < e1 ? A.pair_ent[e0] : 0;
             for (int e = e0; e < e1; ++e) {
-                const int ent = A.pair_ent[e];
+                const int ent = ent_next;
+                if (e + 1 < e1) ent_next = A.pair_ent[e + 1];      // prefetch the next entry
                 if (!(ent & use_bit)) continue;
                 const bool partial = (ent & part_bit) != 0;
+                uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
+                uint32_t live = 0xF;     // 32-column chunks with any valid entry in this warp
+                if (partial) {
+                    row_mask128(sg0, sg1, sg2, (ent & kKvMask) * 128, mk);
+                    live = 0;
 #pragma unroll
-                for (int h = 0; h < 2; ++h, ++j) {
-                    const int c0 = (ent & kKvMask) * 128 + 64 * h;
-                    uint32_t mk[2] = {~0u, ~0u};
-                    uint32_t live = 3;       // 32-column chunks with any valid entry in this warp
-                    if (partial) {
-                        row_mask64(sg0, sg1, sg2, c0, mk);
-                        live = (__any_sync(0xffffffffu, mk[0] != 0) ? 1u : 0u) |
-                               (__any_sync(0xffffffffu, mk[1] != 0) ? 2u : 0u);
-                    }
-                    float sv[64];
-                    if (lane == 0 && quad == 0) TRACE(2 + g, 1);
-                    mbar_wait(&s_full[2 * g + h], (j >> 1) & 1);
-                    if (lane == 0 && quad == 0) TRACE(2 + g, 2);
-                    tc_fence_after();
-                    tmem_ld32(s_tm + 64 * h, sv);
-                    tmem_ld32(s_tm + 64 * h + 32, sv + 32);
+                    for (int w = 0; w < 4; ++w)
+                        if (__any_sync(0xffffffffu, mk[w] != 0)) live |= 1u << w;
+                }
+                if (lane == 0 && quad == 0) TRACE(2 + g, 1);
+                mbar_wait(&s_full[g], s_cnt & 1);
+                ++s_cnt;
+                tc_fence_after();
+                if (lane == 0 && quad == 0) TRACE(2 + g, 2);
+                // pass 1: row max over the live chunks
+                float mx = -INFINITY;
+#pragma unroll
+                for (int w2 = 0; w2 < 2; ++w2) {
+                    float v[2][32];
+                    tmem_ld32(s_tm + 64 * w2, v[0]);
+                    tmem_ld32(s_tm + 64 * w2 + 32, v[1]);
                     tmem_wait_ld();
-                    if (lane == 0 && quad == 0) TRACE(2 + g, 5);
-                    float mx = -INFINITY;
 #pragma unroll
-                    for (int w = 0; w < 2; ++w) {
+                    for (int q = 0; q < 2; ++q) {
+                        const int w = 2 * w2 + q;
                         if (live & (1u << w)) {
-                            if (partial) {
-#pragma unroll
-                                for (int x = 0; x < 32; ++x)
-                                    sv[32 * w + x] = ((mk[w] >> x) & 1u) ? sv[32 * w + x] : -INFINITY;
-                            }
-                            mx = fmax3(mx, max32(sv + 32 * w), -INFINITY);
+                            if (partial) apply_mask(v[q], mk[w]);
+                            mx = fmax3(mx, max32(v[q]), -INFINITY);
                         }
                     }
-                    mx *= c2;
-                    float alpha = 1.f;
-                    bool resc = false;
-                    if (mx > m_run + kRescaleThresh) {
-                        if (m_run != -INFINITY) {
-                            alpha = ex2(m_run - mx);
-                            resc = true;
-                        }
-                        m_run = mx;
-                        l_run *= alpha;
+                }
+                mx *= c2;
+                float alpha = 1.f;
+                bool resc = false;
+                if (mx > m_run + kRescaleThresh) {
+                    if (m_run != -INFINITY) {
+                        alpha = ex2(m_run - mx);
+                        resc = true;
                     }
-                    if (j > j_first && __any_sync(0xffffffffu, resc)) {
-                        // every earlier PV of this tile must have landed in O before rescaling it
-                        WAIT_PV(j - 1);
-                        tc_fence_after();
+                    m_run = mx;
+                    l_run *= alpha;
+                }
+                if (!first && __any_sync(0xffffffffu, resc)) {
+                    // O holds every earlier PV of this tile: S_g(j) was computed after PV_g(j-1)
 #pragma unroll
-                        for (int c = 0; c < D / 32; ++c) {
-                            float o[32];
-                            tmem_ld32(o_tm + c * 32, o);
-                            tmem_wait_ld();
+                    for (int c = 0; c < D / 32; ++c) {
+                        float o[32];
+                        tmem_ld32(o_tm + c * 32, o);
+                        tmem_wait_ld();
 #pragma unroll
-                            for (int x = 0; x < 32; ++x) o[x] *= alpha;
-                            tmem_st32(o_tm + c * 32, o);
-                        }
+                        for (int x = 0; x < 32; ++x) o[x] *= alpha;
+                        tmem_st32(o_tm + c * 32, o);
                     }
-                    const float mref = m_run == -INFINITY ? 0.f : m_run;
-                    const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
-                    uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
-                    if (lane == 0 && quad == 0) TRACE(2 + g, 6);
+                }
+                if (lane == 0 && quad == 0) TRACE(2 + g, 3);
+                const float mref = m_run == -INFINITY ? 0.f : m_run;
+                const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
+                uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
+                if (prm.dbg & 2) live = 0;
+                // pass 2: chunks 2h, 2h+1 are read before P columns [32h, 32h+32) overwrite them
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
                     uint32_t pw[32];
-                    if (prm.dbg & 2) live = 0;
+                    float v[2][32];
+                    tmem_ld32(s_tm + 64 * h, v[0]);
+                    tmem_ld32(s_tm + 64 * h + 32, v[1]);
+                    tmem_wait_ld();
 #pragma unroll
-                    for (int w = 0; w < 2; ++w) {
+                    for (int q = 0; q < 2; ++q) {
+                        const int w = 2 * h + q;
                         if (live & (1u << w)) {
-                            exp32(sv + 32 * w, cc, mm, acc0, acc1, pw + 16 * w);
+                            if (partial) apply_mask(v[q], mk[w]);
+                            exp32(v[q], cc, mm, acc0, acc1, pw + 16 * q);
                         } else {
 #pragma unroll
-                            for (int x = 0; x < 16; ++x) pw[16 * w + x] = 0u;
+                            for (int x = 0; x < 16; ++x) pw[16 * q + x] = 0u;
                         }
                     }
-                    // P (bf16 pairs) over the first 32 columns of the slot (S already in registers)
-                    if (lane == 0 && quad == 0) TRACE(2 + g, 7);
-                    tmem_st32(s_tm + 64 * h, reinterpret_cast<const float *>(pw));
-                    {
-                        float a, b, c, d;
-                        unpack2(acc0, a, b);
-                        unpack2(acc1, c, d);
-                        l_run += (a + b) + (c + d);
-                    }
-                    if (lane == 0 && quad == 0) TRACE(2 + g, 3);
-                    if (j > 0) WAIT_PV(j - 1);
-                    if (lane == 0 && quad == 0) TRACE(2 + g, 4);
-                    tmem_wait_st();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&p_full[2 * g + h]);
+                    tmem_st32(s_tm + 32 * h, reinterpret_cast<const float *>(pw));
                 }
+                {
+                    float a, b, c, d;
+                    unpack2(acc0, a, b);
+                    unpack2(acc1, c, d);
+                    l_run += (a + b) + (c + d);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[g]);
+                if (lane == 0 && quad == 0) TRACE(2 + g, 4);
+                first = false;
             }
-            // epilogue: wait for the last PV of this tile, then O / l -> bf16 -> HBM
-            WAIT_PV(j - 1);
+            // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
+            mbar_wait(&epi[g], e_cnt & 1);
+            ++e_cnt;
             tc_fence_after();
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
             __nv_bfloat16 *orow = prm.O + ((size_t)bh * prm.N + row) * D;
@@ -578,7 +577,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             }
             tc_fence_before();
         }
-#undef WAIT_PV
     }
     __syncthreads();
     if (warp == 1) {

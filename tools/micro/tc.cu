@@ -22,7 +22,35 @@ __global__ void __launch_bounds__(128, 1) k_mma(unsigned long long *out, int n_m
     for (int i = threadIdx.x; i < 65536 / 4; i += 128) reinterpret_cast<uint32_t *>(smem)[i] = 0x3c003c00u;
     fence_proxy_async_smem();
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0 && n_mma < 0) {
+        // whole warp runs the loop (uniform control flow); one elected lane issues the MMA
+        const int nm = -n_mma;
+        const uint32_t s = smem_u32(smem);
+        const uint32_t id = idesc_bf16(128, N, false);
+        const uint64_t da = sdesc_sw128(s, 16, 1024), db = sdesc_sw128(s + 32768, 16, 1024);
+        unsigned long long t0 = clock64();
+        for (int i = 0; i < nm; ++i) {
+            uint32_t pred;
+            asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+            if (pred) mma_bf16_ss(tm, da + (uint64_t)((i & 3) * 2), db + (uint64_t)((i & 3) * 2), id, 1);
+            __syncwarp();
+        }
+        unsigned long long t1 = clock64();
+        if (threadIdx.x == 0) {
+            mma_commit(&bar);
+            mbar_wait(&bar, 0);
+        }
+        __syncwarp();
+        unsigned long long t2 = clock64();
+        if (threadIdx.x == 0) {
+            mma_commit(&bar);
+            mbar_wait(&bar, 1);
+            unsigned long long t3 = clock64();
+            out[blockIdx.x * 4 + 0] = t1 - t0;
+            out[blockIdx.x * 4 + 1] = t2 - t0;
+            out[blockIdx.x * 4 + 2] = t3 - t2;
+        }
+    } else if (threadIdx.x == 0 && n_mma > 0) {
         const uint32_t s = smem_u32(smem);
         const uint32_t id = idesc_bf16(128, N, false);
         unsigned long long t0 = clock64();
@@ -79,7 +107,7 @@ int main()
     cudaMalloc(&d, 1 << 20);
     cudaFuncSetAttribute(k_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024 + 1024);
     for (int N : {64, 128, 256}) {
-        for (int n : {1, 4, 16, 64}) {
+        for (int n : {1, 4, 16, 64, -1, -4, -16, -64}) {
             k_mma<<<148, 128, 66 * 1024 + 1024>>>(d, n, N);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
@@ -87,7 +115,7 @@ int main()
             cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
             printf("M=128 N=%3d K=16 x%2d: issue %6llu cyc, issue+complete %6llu cyc (ideal %d), empty commit rt %llu; "
                    "ld.x32+wait %.1f cyc, st.x32+wait %.1f cyc, 8 ld pipelined %llu cyc\n",
-                   N, n, h[0], h[1], n * N / 2, h[2], (h[3] >> 32) / 64.0, (h[3] & 0xffffffff) / 64.0, h[4 * 148]);
+                   N, n, h[0], h[1], (n < 0 ? -n : n) * N / 2, h[2], (h[3] >> 32) / 64.0, (h[3] & 0xffffffff) / 64.0, h[4 * 148]);
         }
     }
     return 0;
