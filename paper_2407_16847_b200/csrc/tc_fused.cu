@@ -473,6 +473,14 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 ++s_cnt;
                 tc_fence_after();
                 if (lane == 0 && quad == 0) TRACE(2 + g, 2);
+                if (prm.dbg & 8) {     // profiling aid: no TMEM traffic from the softmax at all
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&p_full[g]);
+                    if (lane == 0 && quad == 0) TRACE(2 + g, 4);
+                    first = false;
+                    continue;
+                }
                 // pass 1: row max over the live chunks
                 float mx = -INFINITY;
 #pragma unroll
