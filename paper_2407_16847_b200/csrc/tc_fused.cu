@@ -105,6 +105,48 @@ __device__ __forceinline__ void unit_at(const DevAcsr &A, int BH, int u, int &pa
     bh = 0;
 }
 
+// Per-unit metadata, fetched one unit ahead so the dependent global loads never sit on the
+// critical path of a role.
+struct UnitInfo {
+    int pair, bh, e0, e1;
+};
+
+__device__ __forceinline__ UnitInfo fetch_unit(const DevAcsr &A, int BH, int u)
+{
+    UnitInfo x;
+    unit_at(A, BH, u, x.pair, x.bh);
+    x.e0 = A.pair_ptr[x.pair];
+    x.e1 = A.pair_ptr[x.pair + 1];
+    return x;
+}
+
+// The unit's plan entries cached in the registers of a (uniformly executing) warp: lane l
+// holds entries e0 + l + 32k, k < 4; ent_at() broadcasts with a shuffle (beyond 128 entries it
+// falls back to a global load).
+struct EntRegs {
+    int r[4];
+};
+
+__device__ __forceinline__ void load_ents(const DevAcsr &A, const UnitInfo &un, int lane, EntRegs &er)
+{
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int idx = un.e0 + lane + 32 * k;
+        er.r[k] = idx < un.e1 ? A.pair_ent[idx] : 0;
+    }
+}
+
+__device__ __forceinline__ int ent_at(const DevAcsr &A, const UnitInfo &un, const EntRegs &er, int e)
+{
+    const int i = e - un.e0;
+    if (i < 128) {
+        const int k = i >> 5;
+        const int v = k == 0 ? er.r[0] : (k == 1 ? er.r[1] : (k == 2 ? er.r[2] : er.r[3]));
+        return __shfl_sync(0xffffffffu, v, i & 31);
+    }
+    return A.pair_ent[e];
+}
+
 __device__ __forceinline__ float fmax3(float a, float b, float c)
 {
     float d;
@@ -267,9 +309,14 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         uint32_t qph[2] = {0, 0};
         int ki = 0, kc = 0;
         uint32_t kph = 0;
+        UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
+        EntRegs ner;
+        load_ents(A, nx, lane, ner);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            int pair, bh;
-            unit_at(A, prm.BH, u, pair, bh);
+            const UnitInfo un = nx;
+            const EntRegs er = ner;
+            if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
+            const int pair = un.pair, bh = un.bh;
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
                 const int t = 2 * pair + g;
@@ -286,9 +333,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 ++qc[g];
                 if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
             }
-            const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
+            const int e0 = un.e0, e1 = un.e1;
             for (int e = e0; e < e1; ++e) {
-                const int kv = A.pair_ent[e] & kKvMask;
+                const int kv = ent_at(A, un, er, e) & kKvMask;
+                if (e == e0 + 1) load_ents(A, nx, lane, ner);     // next unit's entries, in the shadow
                 if (kc >= C::KS) {
                     mbar_wait(&k_empty[ki], kph ^ 1);
                     mbar_wait(&v_empty[ki], kph ^ 1);
@@ -308,6 +356,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
             }
+            if (e1 - e0 <= 1) load_ents(A, nx, lane, ner);
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer (warp-uniform)
@@ -326,18 +375,23 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         uint32_t gbase = 0;                                  // entries loaded before this unit
         uint32_t pc0 = 0, pc1 = 0;                           // p_full phases consumed per group
         int kleft[C::KS], vleft[C::KS];                      // MMAs still to issue per stage
+        UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
+        EntRegs ner;
+        load_ents(A, nx, lane, ner);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            int pair, bh;
-            unit_at(A, prm.BH, u, pair, bh);
+            const UnitInfo un = nx;
+            const EntRegs er = ner;
+            if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
+            const int pair = un.pair;
+            bool ents_next_loaded = false;
             const bool hasB = 2 * pair + 1 < A.n_qt;
             const int slot0 = qi0, slot1 = C::QS + qi1;
             mbar_wait(&q_full[slot0], qph0);
             if (hasB) mbar_wait(&q_full[slot1], qph1);
-            const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
-            const int *ents = A.pair_ent;
+            const int e0 = un.e0, e1 = un.e1;
             const int use0 = kUseA, use1 = hasB ? kUseB : 0;
             auto next_used = [&](int e, int bit) {
-                while (e < e1 && !(ents[e] & bit)) ++e;
+                while (e < e1 && !(ent_at(A, un, er, e) & bit)) ++e;
                 return e;
             };
             int qe0 = next_used(e0, use0), qe1 = use1 ? next_used(e0, use1) : e1;
@@ -349,7 +403,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (loaded < e1) {
                     const uint32_t ge = gbase + (loaded - e0);
                     if (mbar_test(&k_full[ge % C::KS], (ge / C::KS) & 1)) {
-                        const int ent = ents[loaded];
+                        const int ent = ent_at(A, un, er, loaded);
                         const int users = ((ent & use0) ? 1 : 0) + ((use1 && (ent & use1)) ? 1 : 0);
                         kleft[ge % C::KS] = users;
                         vleft[ge % C::KS] = users;
@@ -416,9 +470,17 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (hasB) SPLAT_GROUP(1);
 #undef SPLAT_GROUP
                 if (qe0 >= e1 && !pend0 && (!hasB || (qe1 >= e1 && !pend1))) break;
-                if (!progress) __nanosleep(16);
+                if (!progress) {
+                    if (!ents_next_loaded) {           // idle: fetch the next unit's entries now
+                        load_ents(A, nx, lane, ner);
+                        ents_next_loaded = true;
+                    } else {
+                        __nanosleep(16);
+                    }
+                }
             }
             gbase += e1 - e0;
+            if (!ents_next_loaded) load_ents(A, nx, lane, ner);
             if (leader) mma_commit(&q_empty[slot0]);
             if (++qi0 == C::QS) { qi0 = 0; qph0 ^= 1; }
             if (hasB) {
@@ -437,26 +499,39 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const int use_bit = g == 0 ? kUseA : kUseB, part_bit = g == 0 ? kPartA : kPartB;
         const float c2 = prm.scale_log2;
         uint32_t s_cnt = 0, e_cnt = 0;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            int pair, bh;
-            unit_at(A, prm.BH, u, pair, bh);
-            const int t = 2 * pair + g;
-            if (t >= A.n_qt) continue;
-            const int row = t * 128 + r;
-            int4 sg0 = make_int4(0, 1, 0, 0), sg1 = sg0, sg2 = sg0;
-            if (row < A.n) {
-                const int ns = A.nseg[row];
-                if (ns > 0) sg0 = A.seg[(size_t)row * 4 + 0];
-                if (ns > 1) sg1 = A.seg[(size_t)row * 4 + 1];
-                if (ns > 2) sg2 = A.seg[(size_t)row * 4 + 2];
+        // the row's runs (segments) for a unit; nseg is encoded by count = 0 of unused runs
+        auto load_segs = [&](const UnitInfo &x, int4 &a0, int4 &a1, int4 &a2) {
+            const int rw = (2 * x.pair + g) * 128 + r;
+            a0 = a1 = a2 = make_int4(0, 1, 0, 0);
+            if (2 * x.pair + g < A.n_qt && rw < A.n) {
+                a0 = A.seg[(size_t)rw * 4 + 0];
+                a1 = A.seg[(size_t)rw * 4 + 1];
+                a2 = A.seg[(size_t)rw * 4 + 2];
             }
+        };
+        UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
+        EntRegs ner;
+        load_ents(A, nx, lane, ner);
+        int4 nsg0, nsg1, nsg2;
+        load_segs(nx, nsg0, nsg1, nsg2);
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const UnitInfo un = nx;
+            const EntRegs er = ner;
+            const int4 sg0 = nsg0, sg1 = nsg1, sg2 = nsg2;
+            if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
+            const int pair = un.pair, bh = un.bh;
+            const int t = 2 * pair + g;
+            if (t >= A.n_qt) {
+                load_ents(A, nx, lane, ner);
+                load_segs(nx, nsg0, nsg1, nsg2);
+                continue;
+            }
+            const int row = t * 128 + r;
             float m_run = -INFINITY, l_run = 0.f;
             bool first = true;
-            const int e0 = A.pair_ptr[pair], e1 = A.pair_ptr[pair + 1];
-            int ent_next = e0 < e1 ? A.pair_ent[e0] : 0;
+            const int e0 = un.e0, e1 = un.e1;
             for (int e = e0; e < e1; ++e) {
-                const int ent = ent_next;
-                if (e + 1 < e1) ent_next = A.pair_ent[e + 1];      // prefetch the next entry
+                const int ent = ent_at(A, un, er, e);
                 if (!(ent & use_bit)) continue;
                 const bool partial = (ent & part_bit) != 0;
                 uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
@@ -560,6 +635,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (lane == 0 && quad == 0) TRACE(2 + g, 4);
                 first = false;
             }
+            // next unit's metadata, in the shadow of the epilogue
+            load_ents(A, nx, lane, ner);
+            load_segs(nx, nsg0, nsg1, nsg2);
             // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
             mbar_wait(&epi[g], e_cnt & 1);
             ++e_cnt;
