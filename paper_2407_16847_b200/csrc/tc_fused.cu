@@ -533,6 +533,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             for (int e = e0; e < e1; ++e) {
                 const int ent = ent_at(A, un, er, e);
                 if (!(ent & use_bit)) continue;
+                if (lane == 0 && quad == 0) TRACE(2 + g, 5);
                 const bool partial = (ent & part_bit) != 0;
                 uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
                 uint32_t live = 0xF;     // 32-column chunks with any valid entry in this warp
@@ -638,10 +639,12 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             // next unit's metadata, in the shadow of the epilogue
             load_ents(A, nx, lane, ner);
             load_segs(nx, nsg0, nsg1, nsg2);
+            if (lane == 0 && quad == 0) TRACE(2 + g, 7);
             // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
             mbar_wait(&epi[g], e_cnt & 1);
             ++e_cnt;
             tc_fence_after();
+            if (lane == 0 && quad == 0) TRACE(2 + g, 8);
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
             __nv_bfloat16 *orow = prm.O + ((size_t)bh * prm.N + row) * D;
 #pragma unroll
@@ -662,6 +665,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 }
             }
             tc_fence_before();
+            if (lane == 0 && quad == 0) TRACE(2 + g, 9);
         }
     }
     __syncthreads();
