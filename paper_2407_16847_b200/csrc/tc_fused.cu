@@ -290,8 +290,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2 * C::QS; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
         for (int i = 0; i < C::KS; ++i) {
-            mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
-            mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
+            mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 2);
+            mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 2);
         }
         for (int g = 0; g < 2; ++g) { mbar_init(&s_full[g], 1); mbar_init(&p_full[g], 4); mbar_init(&epi[g], 1); }
         fence_mbar_init();
@@ -358,23 +358,26 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             }
             if (e1 - e0 <= 1) load_ents(A, nx, lane, ner);
         }
-    } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer (warp-uniform)
-        // The whole warp runs the (uniform) issue loop so descriptors live in uniform registers;
-        // lane 0 issues every tcgen05.mma / commit.  Per tile group g the sequence is strictly
-        // S_g(j) = Q_g K_j^T, [P_g(j) ready] O_g += P_g(j) V_j, S_g(j+1) ... (P aliases S in TMEM).
-        // The issuer polls the load and P barriers and serves whichever group is ready, so the
-        // two groups ping-pong: one group's exponentials overlap the other group's MMAs.
+    } else if (warp == 1 || warp == 2) {
+        // ------------------------------------------------------------ MMA issuers (warp-uniform)
+        // Warp 1 serves tile group A, warp 2 tile group B, so the two groups never wait for each
+        // other's turnaround.  Per group the sequence is S(e) = Q K_e^T, [P(e) ready]
+        // O += P(e) V_e, S(e') ... with P aliased into S's TMEM columns, hence PV(e) is issued
+        // before S(e') (tcgen05 executes in issue order).  The whole warp runs the loop so the
+        // descriptors live in uniform registers; lane 0 issues.  K/V stages are released when
+        // both groups are done with them (empty barriers count two arrivals; a group that skips
+        // an entry arrives once the entry is resident).
+        const int g = warp - 1;
         constexpr uint32_t idS = idesc_bf16(128, 128, false);
         constexpr uint32_t idO = idesc_bf16(128, D, true);
         const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
         const uint32_t sV = smem_u32(smem + C::OFF_V);
         const bool leader = lane == 0;
-        int qi0 = 0, qi1 = 0;
-        uint32_t qph0 = 0, qph1 = 0;
-        uint32_t gbase = 0;                                  // entries loaded before this unit
-        uint32_t pc0 = 0, pc1 = 0;                           // p_full phases consumed per group
-        int kleft[C::KS], vleft[C::KS];                      // MMAs still to issue per stage
+        const int use_bit = g == 0 ? kUseA : kUseB;
+        const uint32_t s_tm = tmem + g * 128, o_tm = tmem + 256 + g * D;
+        int qi = 0;
+        uint32_t qph = 0, pcnt = 0;
+        uint32_t gent = 0;                                   // global entry counter (ring position)
         UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
         EntRegs ner;
         load_ents(A, nx, lane, ner);
@@ -382,110 +385,85 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const UnitInfo un = nx;
             const EntRegs er = ner;
             if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
-            const int pair = un.pair;
-            bool ents_next_loaded = false;
-            const bool hasB = 2 * pair + 1 < A.n_qt;
-            const int slot0 = qi0, slot1 = C::QS + qi1;
-            mbar_wait(&q_full[slot0], qph0);
-            if (hasB) mbar_wait(&q_full[slot1], qph1);
-            const int e0 = un.e0, e1 = un.e1;
-            const int use0 = kUseA, use1 = hasB ? kUseB : 0;
-            auto next_used = [&](int e, int bit) {
-                while (e < e1 && !(ent_at(A, un, er, e) & bit)) ++e;
-                return e;
-            };
-            int qe0 = next_used(e0, use0), qe1 = use1 ? next_used(e0, use1) : e1;
-            int pe0 = qe0, pe1 = qe1;
-            bool pend0 = false, pend1 = false, first0 = true, first1 = true;
-            int loaded = e0, vloaded = e0;
-            while (true) {
-                bool progress = false;
-                if (loaded < e1) {
-                    const uint32_t ge = gbase + (loaded - e0);
-                    if (mbar_test(&k_full[ge % C::KS], (ge / C::KS) & 1)) {
-                        const int ent = ent_at(A, un, er, loaded);
-                        const int users = ((ent & use0) ? 1 : 0) + ((use1 && (ent & use1)) ? 1 : 0);
-                        kleft[ge % C::KS] = users;
-                        vleft[ge % C::KS] = users;
-                        ++loaded;
-                        progress = true;
-                    }
+            const bool active = 2 * un.pair + g < A.n_qt;
+            const int slot = g * C::QS + qi;
+            if (active) mbar_wait(&q_full[slot], qph);
+            const uint32_t qb = sQ + slot * C::kTileBytes;
+            bool pend = false, first = true;
+            int pst = 0;
+            uint32_t pph = 0;
+            for (int e = un.e0; e < un.e1; ++e) {
+                const int ent = ent_at(A, un, er, e);
+                const int st = gent % C::KS;
+                const uint32_t ph = (gent / C::KS) & 1;
+                ++gent;
+                if (e == un.e0 + 1) load_ents(A, nx, lane, ner);
+                if (!active || !(ent & use_bit)) {
+                    // not ours: release the stage (once it really holds this entry)
+                    mbar_wait(&k_full[st], ph);
+                    mbar_wait(&v_full[st], ph);
+                    if (leader) { mbar_arrive(&k_empty[st]); mbar_arrive(&v_empty[st]); }
+                    continue;
                 }
-                if (vloaded < loaded) {
-                    const uint32_t ge = gbase + (vloaded - e0);
-                    if (mbar_test(&v_full[ge % C::KS], (ge / C::KS) & 1)) {
-                        ++vloaded;
-                        progress = true;
+                mbar_wait(&k_full[st], ph);
+                if (pend) {
+                    // O += P V of the previous entry (P written by the softmax over S's columns)
+                    mbar_wait(&p_full[g], pcnt & 1);
+                    ++pcnt;
+                    mbar_wait(&v_full[pst], pph);
+                    tc_fence_after();
+                    const uint32_t vbase = sV + pst * C::kTileBytes;
+                    if (leader) {
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)
+                            if (!(prm.dbg & 1))
+                                mma_bf16_ts(o_tm, s_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024),
+                                            idO, (first && kk == 0) ? 0u : 1u);
+                        mma_commit(&v_empty[pst]);
                     }
+                    first = false;
                 }
-#define SPLAT_GROUP(G)                                                                                   \
-    do {                                                                                                 \
-        if (!pend##G && qe##G < loaded) {                                                                \
-            /* S_G = Q_G K^T into TMEM columns [128 G, 128 G + 128) */                                   \
-            const uint32_t ge = gbase + (qe##G - e0);                                                    \
-            const int st = ge % C::KS;                                                                   \
-            const uint32_t kbase = sK + st * C::kTileBytes, qb = sQ + slot##G * C::kTileBytes;           \
-            tc_fence_after();                                                                            \
-            if (leader) {                                                                                \
-                _Pragma("unroll") for (int kk = 0; kk < D / 16; ++kk)                                    \
-                {                                                                                        \
-                    const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;                       \
-                    if (!(prm.dbg & 1))                                                                  \
-                        mma_bf16_ss(tmem + G * 128, sdesc_sw128(qb + off, 16, 1024),                     \
-                                    sdesc_sw128(kbase + off, 16, 1024), idS, kk > 0 ? 1u : 0u);          \
-                }                                                                                        \
-                mma_commit(&s_full[G]);                                                                  \
-                if (--kleft[st] == 0) mma_commit(&k_empty[st]);                                          \
-            }                                                                                            \
-            TRACE(1, 10 + G);                                                                            \
-            pend##G = true;                                                                              \
-            progress = true;                                                                             \
-        }                                                                                                \
-        if (pend##G && pe##G < vloaded && mbar_test(&p_full[G], pc##G & 1)) {                            \
-            /* O_G += P_G V, P_G packed bf16 in TMEM columns [128 G, 128 G + 64) */                     \
-            ++pc##G;                                                                                     \
-            const uint32_t ge = gbase + (pe##G - e0);                                                    \
-            const int st = ge % C::KS;                                                                   \
-            const uint32_t vbase = sV + st * C::kTileBytes;                                              \
-            tc_fence_after();                                                                            \
-            if (leader) {                                                                                \
-                _Pragma("unroll") for (int kk = 0; kk < 8; ++kk)                                         \
-                {                                                                                        \
-                    const uint64_t b = sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024);               \
-                    if (!(prm.dbg & 1))                                                                  \
-                        mma_bf16_ts(tmem + 256 + G * D, tmem + G * 128 + kk * 8, b, idO,                 \
-                                    (first##G && kk == 0) ? 0u : 1u);                                    \
-                }                                                                                        \
-                if (--vleft[st] == 0) mma_commit(&v_empty[st]);                                          \
-            }                                                                                            \
-            TRACE(1, 20 + G);                                                                            \
-            first##G = false;                                                                            \
-            pend##G = false;                                                                             \
-            pe##G = qe##G = next_used(qe##G + 1, use##G);                                                \
-            if (qe##G >= e1 && leader) mma_commit(&epi[G]);                                              \
-            progress = true;                                                                             \
-        }                                                                                                \
-    } while (0)
-                SPLAT_GROUP(0);
-                if (hasB) SPLAT_GROUP(1);
-#undef SPLAT_GROUP
-                if (qe0 >= e1 && !pend0 && (!hasB || (qe1 >= e1 && !pend1))) break;
-                if (!progress) {
-                    if (!ents_next_loaded) {           // idle: fetch the next unit's entries now
-                        load_ents(A, nx, lane, ner);
-                        ents_next_loaded = true;
-                    } else {
-                        __nanosleep(16);
+                tc_fence_after();
+                const uint32_t kbase = sK + st * C::kTileBytes;
+                if (leader) {
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;
+                        if (!(prm.dbg & 1))
+                            mma_bf16_ss(s_tm, sdesc_sw128(qb + off, 16, 1024), sdesc_sw128(kbase + off, 16, 1024),
+                                        idS, kk > 0 ? 1u : 0u);
                     }
+                    mma_commit(&s_full[g]);
+                    mma_commit(&k_empty[st]);
                 }
+                TRACE(1, 10 + g);
+                pend = true;
+                pst = st;
+                pph = ph;
             }
-            gbase += e1 - e0;
-            if (!ents_next_loaded) load_ents(A, nx, lane, ner);
-            if (leader) mma_commit(&q_empty[slot0]);
-            if (++qi0 == C::QS) { qi0 = 0; qph0 ^= 1; }
-            if (hasB) {
-                if (leader) mma_commit(&q_empty[slot1]);
-                if (++qi1 == C::QS) { qi1 = 0; qph1 ^= 1; }
+            if (pend) {
+                mbar_wait(&p_full[g], pcnt & 1);
+                ++pcnt;
+                mbar_wait(&v_full[pst], pph);
+                tc_fence_after();
+                const uint32_t vbase = sV + pst * C::kTileBytes;
+                if (leader) {
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        if (!(prm.dbg & 1))
+                            mma_bf16_ts(o_tm, s_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024),
+                                        idO, (first && kk == 0) ? 0u : 1u);
+                    mma_commit(&v_empty[pst]);
+                }
+                TRACE(1, 20 + g);
+            }
+            if (un.e1 - un.e0 <= 1) load_ents(A, nx, lane, ner);
+            if (active) {
+                if (leader) {
+                    mma_commit(&epi[g]);
+                    mma_commit(&q_empty[slot]);
+                }
+                if (++qi == C::QS) { qi = 0; qph ^= 1; }
             }
         }
     } else if (warp >= 4) {
