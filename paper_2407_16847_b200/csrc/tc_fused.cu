@@ -392,12 +392,34 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             bool pend = false, first = true;
             int pst = 0;
             uint32_t pph = 0;
+            // O += P V of the pending entry (P written by the softmax over S's columns).  Issued
+            // before anything waits on a later K/V stage: that stage may only be refilled after
+            // this PV releases its V.
+#define SPLAT_PV_PENDING()                                                                               \
+    do {                                                                                                 \
+        mbar_wait(&p_full[g], pcnt & 1);                                                                 \
+        ++pcnt;                                                                                          \
+        mbar_wait(&v_full[pst], pph);                                                                    \
+        tc_fence_after();                                                                                \
+        const uint32_t vbase = sV + pst * C::kTileBytes;                                                 \
+        if (leader) {                                                                                    \
+            _Pragma("unroll") for (int kk = 0; kk < 8; ++kk)                                             \
+                if (!(prm.dbg & 1))                                                                      \
+                    mma_bf16_ts(o_tm, s_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024), \
+                                idO, (first && kk == 0) ? 0u : 1u);                                      \
+            mma_commit(&v_empty[pst]);                                                                   \
+        }                                                                                                \
+        TRACE(1, 20 + g);                                                                                \
+        first = false;                                                                                   \
+        pend = false;                                                                                    \
+    } while (0)
             for (int e = un.e0; e < un.e1; ++e) {
                 const int ent = ent_at(A, un, er, e);
                 const int st = gent % C::KS;
                 const uint32_t ph = (gent / C::KS) & 1;
                 ++gent;
                 if (e == un.e0 + 1) load_ents(A, nx, lane, ner);
+                if (pend) SPLAT_PV_PENDING();
                 if (!active || !(ent & use_bit)) {
                     // not ours: release the stage (once it really holds this entry)
                     mbar_wait(&k_full[st], ph);
@@ -406,23 +428,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     continue;
                 }
                 mbar_wait(&k_full[st], ph);
-                if (pend) {
-                    // O += P V of the previous entry (P written by the softmax over S's columns)
-                    mbar_wait(&p_full[g], pcnt & 1);
-                    ++pcnt;
-                    mbar_wait(&v_full[pst], pph);
-                    tc_fence_after();
-                    const uint32_t vbase = sV + pst * C::kTileBytes;
-                    if (leader) {
-#pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)
-                            if (!(prm.dbg & 1))
-                                mma_bf16_ts(o_tm, s_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024),
-                                            idO, (first && kk == 0) ? 0u : 1u);
-                        mma_commit(&v_empty[pst]);
-                    }
-                    first = false;
-                }
                 tc_fence_after();
                 const uint32_t kbase = sK + st * C::kTileBytes;
                 if (leader) {
@@ -441,22 +446,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 pst = st;
                 pph = ph;
             }
-            if (pend) {
-                mbar_wait(&p_full[g], pcnt & 1);
-                ++pcnt;
-                mbar_wait(&v_full[pst], pph);
-                tc_fence_after();
-                const uint32_t vbase = sV + pst * C::kTileBytes;
-                if (leader) {
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk)
-                        if (!(prm.dbg & 1))
-                            mma_bf16_ts(o_tm, s_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024),
-                                        idO, (first && kk == 0) ? 0u : 1u);
-                    mma_commit(&v_empty[pst]);
-                }
-                TRACE(1, 20 + g);
-            }
+            if (pend) SPLAT_PV_PENDING();
+#undef SPLAT_PV_PENDING
             if (un.e1 - un.e0 <= 1) load_ents(A, nx, lane, ner);
             if (active) {
                 if (leader) {
