@@ -113,6 +113,10 @@ void free_device(splat_acsr_s *a)
     cudaFree(a->plan.d_pair_ptr);
     cudaFree(a->plan.d_pair_ent);
     cudaFree(a->plan.d_pair_order);
+    cudaFree(a->plan.d_pair_info);
+    cudaFree(a->plan.d_pair_mask);
+    cudaFree(a->plan.d_pair_live);
+    cudaFree(a->plan.d_masks);
 }
 
 void finish_host_meta(splat_acsr_s *a)
@@ -138,6 +142,10 @@ DevAcsr dev_view(const splat_acsr_s *a)
     A.pair_ptr = a->plan.d_pair_ptr;
     A.pair_ent = a->plan.d_pair_ent;
     A.pair_order = a->plan.d_pair_order;
+    A.pair_info = reinterpret_cast<const int4 *>(a->plan.d_pair_info);
+    A.pair_mask = reinterpret_cast<const int2 *>(a->plan.d_pair_mask);
+    A.pair_live = a->plan.d_pair_live;
+    A.masks = reinterpret_cast<const uint4 *>(a->plan.d_masks);
     A.n_pairs = a->plan.n_pairs;
     A.n_buckets = a->plan.n_buckets;
     for (int b = 0; b <= a->plan.n_buckets && b <= kMaxBuckets; ++b) A.bucket_start[b] = a->plan.bucket_start[b];
@@ -251,7 +259,11 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
         (e = cudaMalloc(&P.d_order, sizeof(int32_t) * P.n_qt)) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_ptr, sizeof(int32_t) * (P.n_pairs + 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_ent, sizeof(int32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_pair_order, sizeof(int32_t) * P.n_pairs)) != cudaSuccess) {
+        (e = cudaMalloc(&P.d_pair_order, sizeof(int32_t) * P.n_pairs)) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_pair_info, sizeof(int32_t) * 4 * P.n_pairs)) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_pair_mask, sizeof(int32_t) * 2 * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_pair_live, sizeof(uint32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess) {
         free_device(a);
         delete a;
         return cuda_fail(e, "plan allocation");
@@ -267,6 +279,16 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
         e = cudaMemcpyAsync(P.d_pair_ent, P.pair_ent.data(), sizeof(int32_t) * P.n_pair_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_pair_order, P.pair_order.data(), sizeof(int32_t) * P.n_pairs, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(P.d_pair_info, P.pair_info.data(), sizeof(int32_t) * 4 * P.n_pairs, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && P.n_pair_entries > 0)
+        e = cudaMemcpyAsync(P.d_pair_mask, P.pair_mask.data(), sizeof(int32_t) * 2 * P.n_pair_entries,
+                            cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && P.n_pair_entries > 0)
+        e = cudaMemcpyAsync(P.d_pair_live, P.pair_live.data(), sizeof(uint32_t) * P.n_pair_entries,
+                            cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && !P.masks.empty())
+        e = cudaMemcpyAsync(P.d_masks, P.masks.data(), sizeof(uint32_t) * P.masks.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) {
         free_device(a);

@@ -23,6 +23,10 @@ struct DevAcsr {
     const int32_t *pair_ptr;    // [n_pairs+1]
     const int32_t *pair_ent;    // kv | kUseA | kUseB | kPartA | kPartB
     const int32_t *pair_order;  // [n_pairs], bucketed longest first
+    const int4 *pair_info;      // [n_pairs]: (pair, e0, e1, 0) in pair_order order
+    const int2 *pair_mask;      // [n_pair_entries]: mask id for tile A / B (-1: none)
+    const uint32_t *pair_live;  // [n_pair_entries]: chunk liveness per (group, warp quad)
+    const uint4 *masks;         // [n_masks][128]: row column masks
     int n_pairs, n_buckets;
     int bucket_start[kMaxBuckets + 1];
 };

@@ -107,6 +107,53 @@ void build_plan(splat_acsr_s &a)
         if (i == 0 || bucket(P.pair_order[i]) != bucket(P.pair_order[i - 1])) P.bucket_start.push_back(i);
     P.bucket_start.push_back(P.n_pairs);
     P.n_buckets = (int)P.bucket_start.size() - 1;
+    P.pair_info.assign((size_t)P.n_pairs * 4, 0);
+    for (int k = 0; k < P.n_pairs; ++k) {
+        const int p = P.pair_order[k];
+        P.pair_info[4 * k + 0] = p;
+        P.pair_info[4 * k + 1] = P.pair_ptr[p];
+        P.pair_info[4 * k + 2] = P.pair_ptr[p + 1];
+    }
+
+    // ---- per-row column masks of the PARTIAL (tile, key tile) entries (fast-index predicate
+    // of reading A-7 evaluated once per pattern, shared by every (b, h)), and per-warp chunk
+    // liveness of every entry.
+    P.pair_mask.assign((size_t)P.n_pair_entries * 2, -1);
+    P.pair_live.assign(P.n_pair_entries, 0u);
+    P.masks.clear();
+    for (int p = 0; p < P.n_pairs; ++p) {
+        for (int e = P.pair_ptr[p]; e < P.pair_ptr[p + 1]; ++e) {
+            const int ent = P.pair_ent[e], c0 = (ent & kKvMask) * bn;
+            for (int g = 0; g < 2; ++g) {
+                const int t = 2 * p + g;
+                if (!(ent & (g == 0 ? kUseA : kUseB))) continue;
+                if (!(ent & (g == 0 ? kPartA : kPartB))) {
+                    P.pair_live[e] |= 0xFFFFu << (16 * g);
+                    continue;
+                }
+                const size_t base = P.masks.size();
+                P.masks.resize(base + 128 * 4, 0u);
+                uint32_t *m = &P.masks[base];
+                for (int r = 0; r < 128; ++r) {
+                    const int i = t * bm + r;
+                    if (i >= N) continue;
+                    const int32_t *sg = &a.seg_h[(size_t)i * 16];
+                    for (int s = 0; s < a.nseg_h[i]; ++s) {
+                        const int start = sg[4 * s], step = sg[4 * s + 1], count = sg[4 * s + 2];
+                        const int last = start + step * (count - 1);
+                        const int lo = std::max(start, c0), hi = std::min(last, c0 + bn - 1);
+                        if (lo > hi) continue;
+                        const int first = start + ((lo - start + step - 1) / step) * step;
+                        for (int c = first; c <= hi; c += step) m[4 * r + ((c - c0) >> 5)] |= 1u << ((c - c0) & 31);
+                    }
+                    for (int w = 0; w < 4; ++w)
+                        if (m[4 * r + w]) P.pair_live[e] |= 1u << (16 * g + 4 * (r >> 5) + w);
+                }
+                P.pair_mask[(size_t)e * 2 + g] = (int32_t)(base / (128 * 4));
+            }
+        }
+    }
+    P.n_masks = (int)(P.masks.size() / (128 * 4));
 }
 
 }  // namespace splat

@@ -138,10 +138,16 @@ struct Plan {
     int bm = kBM, bn = kBN, n_qt = 0, n_entries = 0, n_kt = 0;
     std::vector<int32_t> qt_ptr, kv, order;          // per query tile (ABI: splat_plan_copy)
     // query-tile pairs
-    int n_pairs = 0, n_pair_entries = 0, n_buckets = 0;
+    int n_pairs = 0, n_pair_entries = 0, n_buckets = 0, n_masks = 0;
     std::vector<int32_t> pair_ptr, pair_ent, pair_order, bucket_start;
+    std::vector<int32_t> pair_info;   // [n_pairs][4]: pair, e0, e1, 0 -- in pair_order order
+    std::vector<int32_t> pair_mask;   // [n_pair_entries][2]: mask id of tile A / B (-1: FULL or unused)
+    std::vector<uint32_t> pair_live;  // [n_pair_entries]: bit 16g + 4 quad + w = chunk w live for warp quad
+    std::vector<uint32_t> masks;      // [n_masks][128 rows][4 words]: column mask of each row
     int32_t *d_qt_ptr = nullptr, *d_kv = nullptr, *d_order = nullptr;
     int32_t *d_pair_ptr = nullptr, *d_pair_ent = nullptr, *d_pair_order = nullptr;
+    int32_t *d_pair_info = nullptr, *d_pair_mask = nullptr;
+    uint32_t *d_pair_live = nullptr, *d_masks = nullptr;
 };
 
 }  // namespace splat

@@ -88,23 +88,6 @@ __device__ int g_trace_n[4];
 #define TRACE(R, TAG) do { } while (0)
 #endif
 
-// unit u -> (pair, bh): buckets in order; inside a bucket, head-major.
-__device__ __forceinline__ void unit_at(const DevAcsr &A, int BH, int u, int &pair, int &bh)
-{
-    for (int b = 0; b < A.n_buckets; ++b) {
-        const int nb = A.bucket_start[b + 1] - A.bucket_start[b];
-        const int ub = nb * BH;
-        if (u < ub) {
-            bh = u / nb;
-            pair = A.pair_order[A.bucket_start[b] + u % nb];
-            return;
-        }
-        u -= ub;
-    }
-    pair = 0;
-    bh = 0;
-}
-
 // Per-unit metadata, fetched one unit ahead so the dependent global loads never sit on the
 // critical path of a role.
 struct UnitInfo {
@@ -113,10 +96,24 @@ struct UnitInfo {
 
 __device__ __forceinline__ UnitInfo fetch_unit(const DevAcsr &A, int BH, int u)
 {
+    // bucket arithmetic on kernel parameters, then a single (independent) load
+    int k = 0, bh = 0;
+    for (int b = 0; b < A.n_buckets; ++b) {
+        const int nb = A.bucket_start[b + 1] - A.bucket_start[b];
+        const int ub = nb * BH;
+        if (u < ub) {
+            bh = u / nb;
+            k = A.bucket_start[b] + u % nb;
+            break;
+        }
+        u -= ub;
+    }
+    const int4 info = A.pair_info[k];
     UnitInfo x;
-    unit_at(A, BH, u, x.pair, x.bh);
-    x.e0 = A.pair_ptr[x.pair];
-    x.e1 = A.pair_ptr[x.pair + 1];
+    x.pair = info.x;
+    x.bh = bh;
+    x.e0 = info.y;
+    x.e1 = info.z;
     return x;
 }
 
@@ -125,6 +122,7 @@ __device__ __forceinline__ UnitInfo fetch_unit(const DevAcsr &A, int BH, int u)
 // falls back to a global load).
 struct EntRegs {
     int r[4];
+    uint32_t l[4];   // pair_live words of the same entries
 };
 
 __device__ __forceinline__ void load_ents(const DevAcsr &A, const UnitInfo &un, int lane, EntRegs &er)
@@ -133,7 +131,19 @@ __device__ __forceinline__ void load_ents(const DevAcsr &A, const UnitInfo &un, 
     for (int k = 0; k < 4; ++k) {
         const int idx = un.e0 + lane + 32 * k;
         er.r[k] = idx < un.e1 ? A.pair_ent[idx] : 0;
+        er.l[k] = idx < un.e1 ? A.pair_live[idx] : 0u;
     }
+}
+
+__device__ __forceinline__ uint32_t live_at(const DevAcsr &A, const UnitInfo &un, const EntRegs &er, int e)
+{
+    const int i = e - un.e0;
+    if (i < 128) {
+        const int k = i >> 5;
+        const uint32_t v = k == 0 ? er.l[0] : (k == 1 ? er.l[1] : (k == 2 ? er.l[2] : er.l[3]));
+        return __shfl_sync(0xffffffffu, v, i & 31);
+    }
+    return A.pair_live[e];
 }
 
 __device__ __forceinline__ int ent_at(const DevAcsr &A, const UnitInfo &un, const EntRegs &er, int e)
@@ -190,37 +200,6 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
-}
-
-// Column mask of one row for the 128 columns [c0, c0+128): bit x of mk[x/32] set iff column
-// c0+x lies in one of the row's runs (fast-index predicate, reading A-7).
-__device__ __forceinline__ void row_mask128(const int4 &sg0, const int4 &sg1, const int4 &sg2, int c0,
-                                            uint32_t (&mk)[4])
-{
-    mk[0] = mk[1] = mk[2] = mk[3] = 0u;
-    const int4 sgs[3] = {sg0, sg1, sg2};
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const int start = sgs[q].x, step = sgs[q].y, cnt = sgs[q].z;
-        if (cnt <= 0) continue;
-        const int last = start + step * (cnt - 1);
-        const int lo = max(start, c0), hi = min(last, c0 + 127);
-        if (lo > hi) continue;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const int a = max(lo, c0 + 32 * w), b = min(hi, c0 + 32 * w + 31);
-            if (a > b) continue;
-            if (step == 1) {
-                const int n = b - a + 1;
-                mk[w] |= (n == 32 ? 0xffffffffu : ((1u << n) - 1u)) << (a - c0 - 32 * w);
-            } else {
-                const int f = start + ((a - start + step - 1) / step) * step;
-                uint32_t bits = 0;
-                for (int c = f; c <= b; c += step) bits |= 1u << (c - c0 - 32 * w);
-                mk[w] |= bits;
-            }
-        }
-    }
 }
 
 __device__ __forceinline__ float max32(const float *v)
@@ -335,7 +314,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             }
             const int e0 = un.e0, e1 = un.e1;
             for (int e = e0; e < e1; ++e) {
-                const int kv = ent_at(A, un, er, e) & kKvMask;
+                const int ent_at_lane0 = ent_at(A, un, er, e);
+                const int kv = ent_at_lane0 & kKvMask;
                 if (e == e0 + 1) load_ents(A, nx, lane, ner);     // next unit's entries, in the shadow
                 if (kc >= C::KS) {
                     mbar_wait(&k_empty[ki], kph ^ 1);
@@ -352,6 +332,14 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     for (int c = 0; c < C::kChunks; ++c)
                         tma_load_3d(smem + C::OFF_V + ki * C::kTileBytes + c * kTileBytes64, &tmV, &v_full[ki],
                                     64 * c, kv * 128, bh);
+                    // the stage is released by two arrivals (one per tile group); arrive now on
+                    // behalf of a group that does not use this key tile
+                    const int ent = ent_at_lane0;
+                    const bool both = (ent & kUseA) && (ent & kUseB) && 2 * pair + 1 < A.n_qt;
+                    if (!both) {
+                        mbar_arrive(&k_empty[ki]);
+                        mbar_arrive(&v_empty[ki]);
+                    }
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -420,13 +408,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 ++gent;
                 if (e == un.e0 + 1) load_ents(A, nx, lane, ner);
                 if (pend) SPLAT_PV_PENDING();
-                if (!active || !(ent & use_bit)) {
-                    // not ours: release the stage (once it really holds this entry)
-                    mbar_wait(&k_full[st], ph);
-                    mbar_wait(&v_full[st], ph);
-                    if (leader) { mbar_arrive(&k_empty[st]); mbar_arrive(&v_empty[st]); }
-                    continue;
-                }
+                if (!active || !(ent & use_bit)) continue;   // not ours (the producer arrived for us)
                 mbar_wait(&k_full[st], ph);
                 tc_fence_after();
                 const uint32_t kbase = sK + st * C::kTileBytes;
@@ -468,31 +450,17 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const int use_bit = g == 0 ? kUseA : kUseB, part_bit = g == 0 ? kPartA : kPartB;
         const float c2 = prm.scale_log2;
         uint32_t s_cnt = 0, e_cnt = 0;
-        // the row's runs (segments) for a unit; nseg is encoded by count = 0 of unused runs
-        auto load_segs = [&](const UnitInfo &x, int4 &a0, int4 &a1, int4 &a2) {
-            const int rw = (2 * x.pair + g) * 128 + r;
-            a0 = a1 = a2 = make_int4(0, 1, 0, 0);
-            if (2 * x.pair + g < A.n_qt && rw < A.n) {
-                a0 = A.seg[(size_t)rw * 4 + 0];
-                a1 = A.seg[(size_t)rw * 4 + 1];
-                a2 = A.seg[(size_t)rw * 4 + 2];
-            }
-        };
         UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
         EntRegs ner;
         load_ents(A, nx, lane, ner);
-        int4 nsg0, nsg1, nsg2;
-        load_segs(nx, nsg0, nsg1, nsg2);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const UnitInfo un = nx;
             const EntRegs er = ner;
-            const int4 sg0 = nsg0, sg1 = nsg1, sg2 = nsg2;
             if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
             const int pair = un.pair, bh = un.bh;
             const int t = 2 * pair + g;
             if (t >= A.n_qt) {
                 load_ents(A, nx, lane, ner);
-                load_segs(nx, nsg0, nsg1, nsg2);
                 continue;
             }
             const int row = t * 128 + r;
@@ -504,14 +472,13 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (!(ent & use_bit)) continue;
                 if (lane == 0 && quad == 0) TRACE(2 + g, 5);
                 const bool partial = (ent & part_bit) != 0;
+                // 32-column chunks of this warp with any valid entry (precomputed per pattern)
+                uint32_t live = (live_at(A, un, er, e) >> (16 * g + 4 * quad)) & 0xFu;
                 uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
-                uint32_t live = 0xF;     // 32-column chunks with any valid entry in this warp
                 if (partial) {
-                    row_mask128(sg0, sg1, sg2, (ent & kKvMask) * 128, mk);
-                    live = 0;
-#pragma unroll
-                    for (int w = 0; w < 4; ++w)
-                        if (__any_sync(0xffffffffu, mk[w] != 0)) live |= 1u << w;
+                    const int2 mid = A.pair_mask[e];
+                    const uint4 m4 = A.masks[(size_t)(g == 0 ? mid.x : mid.y) * 128 + r];
+                    mk[0] = m4.x; mk[1] = m4.y; mk[2] = m4.z; mk[3] = m4.w;
                 }
                 if (lane == 0 && quad == 0) TRACE(2 + g, 1);
                 mbar_wait(&s_full[g], s_cnt & 1);
@@ -607,7 +574,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             }
             // next unit's metadata, in the shadow of the epilogue
             load_ents(A, nx, lane, ner);
-            load_segs(nx, nsg0, nsg1, nsg2);
             if (lane == 0 && quad == 0) TRACE(2 + g, 7);
             // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
             mbar_wait(&epi[g], e_cnt & 1);
