@@ -65,12 +65,33 @@ __device__ __forceinline__ bool mbar_test(const uint64_t *bar, uint32_t parity)
     return ok != 0;
 }
 
+#ifdef SPLAT_HANG_DEBUG
+// Debug build: a wait that spins too long records (smem offset, parity, warp, lane, block) of the
+// first stuck barrier and gives up, so the kernel terminates and the host can read the record.
+__device__ unsigned long long g_hang[4];
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    const uint32_t a = smem_u32(bar);
+    long long n = 0;
+    while (!mbar_try_wait(a, parity)) {
+        if (++n == (1ll << 22)) {
+            if (atomicCAS(&g_hang[0], 0ull, 1ull) == 0ull) {
+                g_hang[1] = a;
+                g_hang[2] = parity;
+                g_hang[3] = ((unsigned long long)blockIdx.x << 32) | (threadIdx.x);
+            }
+            return;
+        }
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     const uint32_t a = smem_u32(bar);
     while (!mbar_try_wait(a, parity)) {
     }
 }
+#endif
 
 // --------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap *m)

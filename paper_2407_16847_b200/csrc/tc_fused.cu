@@ -684,6 +684,17 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
 
 }  // namespace
 
+extern "C" int splat_debug_hang(unsigned long long *out)
+{
+#ifdef SPLAT_HANG_DEBUG
+    cudaMemcpyFromSymbol(out, sm100::g_hang, sizeof(sm100::g_hang));
+    return 1;
+#else
+    (void)out;
+    return 0;
+#endif
+}
+
 extern "C" int splat_debug_trace(unsigned long long *out, int *counts)
 {
     cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
