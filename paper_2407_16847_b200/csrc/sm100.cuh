@@ -66,21 +66,23 @@ __device__ __forceinline__ bool mbar_test(const uint64_t *bar, uint32_t parity)
 }
 
 #ifdef SPLAT_HANG_DEBUG
-// Debug build: a wait that spins too long records (smem offset, parity, warp, lane, block) of the
-// first stuck barrier and gives up, so the kernel terminates and the host can read the record.
-__device__ unsigned long long g_hang[4];
+// Debug build: a wait that spins too long records, per (block, warp), the first stuck barrier
+// (smem address, parity) and gives up; once anything is stuck every later wait returns, so the
+// kernel terminates and the host can read the records.
+__device__ unsigned long long g_hang[1 + 148 * 16];
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     const uint32_t a = smem_u32(bar);
     long long n = 0;
     while (!mbar_try_wait(a, parity)) {
-        if (++n == (1ll << 22)) {
-            if (atomicCAS(&g_hang[0], 0ull, 1ull) == 0ull) {
-                g_hang[1] = a;
-                g_hang[2] = parity;
-                g_hang[3] = ((unsigned long long)blockIdx.x << 32) | (threadIdx.x);
-            }
-            return;
+        if ((++n & 1023) == 0 && *(volatile unsigned long long *)&g_hang[0] > 20000ull) return;
+        if (n == (1ll << 22)) {
+            atomicAdd(&g_hang[0], 1ull);
+            const int w = threadIdx.x >> 5;
+            if (blockIdx.x < 148 && w < 16 && (threadIdx.x & 31) == 0)
+                g_hang[1 + blockIdx.x * 16 + w] = (1ull << 63) | ((unsigned long long)parity << 32) | a;
+            n = 0;
+            if (*(volatile unsigned long long *)&g_hang[0] > 64ull) g_hang[0] = 100000ull;
         }
     }
 }
