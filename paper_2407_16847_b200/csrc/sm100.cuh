@@ -79,8 +79,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         if (n == (1ll << 22)) {
             atomicAdd(&g_hang[0], 1ull);
             const int w = threadIdx.x >> 5;
-            if (blockIdx.x < 148 && w < 16 && (threadIdx.x & 31) == 0)
-                g_hang[1 + blockIdx.x * 16 + w] = (1ull << 63) | ((unsigned long long)parity << 32) | a;
+            if (blockIdx.x < 148 && w < 16 && (threadIdx.x & 31) == 0 && g_hang[1 + blockIdx.x * 16 + w] == 0ull)
+                g_hang[1 + blockIdx.x * 16 + w] = (1ull << 63) | ((unsigned long long)(clock64() & 0x7fffff) << 40) |
+                                                  ((unsigned long long)parity << 32) | a;
             n = 0;
             if (*(volatile unsigned long long *)&g_hang[0] > 64ull) g_hang[0] = 100000ull;
         }
