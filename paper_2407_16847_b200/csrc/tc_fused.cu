@@ -314,8 +314,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             }
             const int e0 = un.e0, e1 = un.e1;
             for (int e = e0; e < e1; ++e) {
-                const int ent_at_lane0 = ent_at(A, un, er, e);
-                const int kv = ent_at_lane0 & kKvMask;
+                const int kv = ent_at(A, un, er, e) & kKvMask;
                 if (e == e0 + 1) load_ents(A, nx, lane, ner);     // next unit's entries, in the shadow
                 if (kc >= C::KS) {
                     mbar_wait(&k_empty[ki], kph ^ 1);
@@ -332,14 +331,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     for (int c = 0; c < C::kChunks; ++c)
                         tma_load_3d(smem + C::OFF_V + ki * C::kTileBytes + c * kTileBytes64, &tmV, &v_full[ki],
                                     64 * c, kv * 128, bh);
-                    // the stage is released by two arrivals (one per tile group); arrive now on
-                    // behalf of a group that does not use this key tile
-                    const int ent = ent_at_lane0;
-                    const bool both = (ent & kUseA) && (ent & kUseB) && 2 * pair + 1 < A.n_qt;
-                    if (!both) {
-                        mbar_arrive(&k_empty[ki]);
-                        mbar_arrive(&v_empty[ki]);
-                    }
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -408,7 +399,15 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 ++gent;
                 if (e == un.e0 + 1) load_ents(A, nx, lane, ner);
                 if (pend) SPLAT_PV_PENDING();
-                if (!active || !(ent & use_bit)) continue;   // not ours (the producer arrived for us)
+                if (!active || !(ent & use_bit)) {
+                    // Not ours: release the stage, but only once it holds this entry.  Every group
+                    // observes every phase of every stage in order -- parity waits are ambiguous
+                    // as soon as a waiter could lag two phases behind a barrier.
+                    mbar_wait(&k_full[st], ph);
+                    mbar_wait(&v_full[st], ph);
+                    if (leader) { mbar_arrive(&k_empty[st]); mbar_arrive(&v_empty[st]); }
+                    continue;
+                }
                 mbar_wait(&k_full[st], ph);
                 tc_fence_after();
                 const uint32_t kbase = sK + st * C::kTileBytes;
