@@ -59,7 +59,11 @@ struct Cfg {
     static constexpr int OFF_K = OFF_Q + 2 * QS * kTileBytes;
     static constexpr int OFF_V = OFF_K + KS * kTileBytes;
     static constexpr int OFF_BAR = OFF_V + KS * kTileBytes;
-    static constexpr int NBAR = 4 * QS + 4 * KS + 6;
+    static constexpr int NBAR = 4 * QS + 4 * KS + 10;
+    // SEP (d = 64): P gets its own TMEM columns (S 2x128 + O 2x64 + P 2x64 = 512), so S is released
+    // as soon as the softmax has loaded it and the next S = Q K^T overlaps the exponentials.
+    // d = 128 (S 2x128 + O 2x128 = 512): P overwrites S and the next S waits for the PV.
+    static constexpr bool SEP = D == 64;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
 };
 
@@ -257,7 +261,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     uint64_t *s_full = v_empty + C::KS;          // [2]  MMA -> softmax: S_g ready
     uint64_t *p_full = s_full + 2;               // [2]  softmax -> MMA: P_g written (O_g rescaled)
     uint64_t *epi = p_full + 2;                  // [2]  MMA -> softmax: last PV of the tile done
+    uint64_t *s_empty = epi + 2;                 // [2]  softmax -> MMA: S_g loaded (SEP)
+    uint64_t *pv_done = s_empty + 2;             // [2]  MMA -> softmax: PV_g complete (SEP)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + C::NBAR);
+    constexpr bool SEP = C::SEP;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevAcsr &A = prm.A;
@@ -272,7 +279,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 2);
             mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 2);
         }
-        for (int g = 0; g < 2; ++g) { mbar_init(&s_full[g], 1); mbar_init(&p_full[g], 4); mbar_init(&epi[g], 1); }
+        for (int g = 0; g < 2; ++g) {
+            mbar_init(&s_full[g], 1); mbar_init(&p_full[g], 4); mbar_init(&epi[g], 1);
+            mbar_init(&s_empty[g], 4); mbar_init(&pv_done[g], 1);
+        }
         fence_mbar_init();
         tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
     }
@@ -282,8 +292,13 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // Register budget (SEP): each SM sub-partition holds 16K registers and runs warps w, w+4, w+8;
+    // warpgroup 0 (TMA, 2 MMA issuers, 1 idle) hands registers to the two softmax warpgroups,
+    // which keep a whole 128-column S row in registers: 128*(168-56) == 256*(224-168).  The
+    // setmaxnreg of each role sits inside the role's branch so ptxas can allocate per region.
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer (warp-uniform loop)
+        if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
         int qi[2] = {0, 0}, qc[2] = {0, 0};
         uint32_t qph[2] = {0, 0};
         int ki = 0, kc = 0;
@@ -346,6 +361,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         // descriptors live in uniform registers; lane 0 issues.  K/V stages are released when
         // both groups are done with them (empty barriers count two arrivals; a group that skips
         // an entry arrives once the entry is resident).
+        if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
         const int g = warp - 1;
         constexpr uint32_t idS = idesc_bf16(128, 128, false);
         constexpr uint32_t idO = idesc_bf16(128, D, true);
@@ -354,8 +370,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const bool leader = lane == 0;
         const int use_bit = g == 0 ? kUseA : kUseB;
         const uint32_t s_tm = tmem + g * 128, o_tm = tmem + 256 + g * D;
+        const uint32_t p_tm = SEP ? tmem + 384 + g * 64 : s_tm;
         int qi = 0;
-        uint32_t qph = 0, pcnt = 0;
+        uint32_t qph = 0, pcnt = 0, scnt = 0;
         uint32_t gent = 0;                                   // global entry counter (ring position)
         UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
         EntRegs ner;
@@ -384,9 +401,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         if (leader) {                                                                                    \
             _Pragma("unroll") for (int kk = 0; kk < 8; ++kk)                                             \
                 if (!(prm.dbg & 1))                                                                      \
-                    mma_bf16_ts(o_tm, s_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024), \
+                    mma_bf16_ts(o_tm, p_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024), \
                                 idO, (first && kk == 0) ? 0u : 1u);                                      \
             mma_commit(&v_empty[pst]);                                                                   \
+            if (SEP) mma_commit(&pv_done[g]);                                                            \
         }                                                                                                \
         TRACE(1, 20 + g);                                                                                \
         first = false;                                                                                   \
@@ -398,8 +416,12 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const uint32_t ph = (gent / C::KS) & 1;
                 ++gent;
                 if (e == un.e0 + 1) load_ents(A, nx, lane, ner);
-                if (pend) SPLAT_PV_PENDING();
-                if (!active || !(ent & use_bit)) {
+                const bool ours = active && (ent & use_bit);
+                // non-SEP: P lives in S's columns, so the PV must precede the next S.  SEP: the next S
+                // goes first (the PV waits for the softmax); a pending PV is still flushed before
+                // waiting on a stage this group does not use (that stage may need its release).
+                if (pend && (!SEP || !ours)) SPLAT_PV_PENDING();
+                if (!ours) {
                     // Not ours: release the stage, but only once it holds this entry.  Every group
                     // observes every phase of every stage in order -- parity waits are ambiguous
                     // as soon as a waiter could lag two phases behind a barrier.
@@ -409,6 +431,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     continue;
                 }
                 mbar_wait(&k_full[st], ph);
+                if (SEP && scnt > 0) mbar_wait(&s_empty[g], (scnt - 1) & 1);   // previous S loaded
+                ++scnt;
                 tc_fence_after();
                 const uint32_t kbase = sK + st * C::kTileBytes;
                 if (leader) {
@@ -423,6 +447,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     mma_commit(&k_empty[st]);
                 }
                 TRACE(1, 10 + g);
+                if (SEP && pend) SPLAT_PV_PENDING();
                 pend = true;
                 pst = st;
                 pph = ph;
@@ -438,14 +463,18 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (++qi == C::QS) { qi = 0; qph ^= 1; }
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp == 3) {
+        if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    } else {
         // ------------------------------------------------------------ softmax warps (4..7: A, 8..11: B)
+        if constexpr (SEP) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
         const int g = (warp - 4) >> 2;          // tile group: 0 = A, 1 = B
         const int quad = warp & 3;              // TMEM lane quadrant of this warp
         const int r = quad * 32 + lane;         // row within the query tile
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t s_tm = tmem + lane_off + g * 128;
         const uint32_t o_tm = tmem + lane_off + 256 + g * D;
+        const uint32_t p_tm = SEP ? tmem + lane_off + 384 + g * 64 : s_tm;
         const int use_bit = g == 0 ? kUseA : kUseB, part_bit = g == 0 ? kPartA : kPartB;
         const float c2 = prm.scale_log2;
         uint32_t s_cnt = 0, e_cnt = 0;
@@ -492,20 +521,38 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     first = false;
                     continue;
                 }
-                // pass 1: row max over the live chunks
                 float mx = -INFINITY;
+                float sv[SEP ? 128 : 1];
+                if constexpr (SEP) {
+                    // one pass: the whole S row -> registers, then S goes back to the MMA warp
 #pragma unroll
-                for (int w2 = 0; w2 < 2; ++w2) {
-                    float v[2][32];
-                    tmem_ld32(s_tm + 64 * w2, v[0]);
-                    tmem_ld32(s_tm + 64 * w2 + 32, v[1]);
+                    for (int w = 0; w < 4; ++w) tmem_ld32(s_tm + 32 * w, sv + 32 * w);
                     tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s_empty[g]);
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int w = 2 * w2 + q;
+                    for (int w = 0; w < 4; ++w) {
                         if (live & (1u << w)) {
-                            if (partial) apply_mask(v[q], mk[w]);
-                            mx = fmax3(mx, max32(v[q]), -INFINITY);
+                            if (partial) apply_mask(sv + 32 * w, mk[w]);
+                            mx = fmax3(mx, max32(sv + 32 * w), -INFINITY);
+                        }
+                    }
+                } else {
+                    // pass 1 of 2 (d = 128 keeps no S row in registers): row max over the live chunks
+#pragma unroll
+                    for (int w2 = 0; w2 < 2; ++w2) {
+                        float v[2][32];
+                        tmem_ld32(s_tm + 64 * w2, v[0]);
+                        tmem_ld32(s_tm + 64 * w2 + 32, v[1]);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const int w = 2 * w2 + q;
+                            if (live & (1u << w)) {
+                                if (partial) apply_mask(v[q], mk[w]);
+                                mx = fmax3(mx, max32(v[q]), -INFINITY);
+                            }
                         }
                     }
                 }
@@ -520,8 +567,13 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     m_run = mx;
                     l_run *= alpha;
                 }
+                if (SEP && s_cnt > 1) {
+                    // PV of this group's previous tile: complete before O is rescaled or P rewritten
+                    mbar_wait(&pv_done[g], (s_cnt - 2) & 1);
+                    tc_fence_after();
+                }
                 if (!first && __any_sync(0xffffffffu, resc)) {
-                    // O holds every earlier PV of this tile: S_g(j) was computed after PV_g(j-1)
+                    // O holds every earlier PV of this tile (non-SEP: S_g(j) was computed after PV_g(j-1))
 #pragma unroll
                     for (int c = 0; c < D / 32; ++c) {
                         float o[32];
@@ -537,26 +589,40 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
                 uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
                 if (prm.dbg & 2) live = 0;
-                // pass 2: chunks 2h, 2h+1 are read before P columns [32h, 32h+32) overwrite them
+                if constexpr (SEP) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t pw[32];
-                    float v[2][32];
-                    tmem_ld32(s_tm + 64 * h, v[0]);
-                    tmem_ld32(s_tm + 64 * h + 32, v[1]);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int w = 2 * h + q;
+                    for (int w = 0; w < 4; ++w) {
+                        uint32_t pw[16];
                         if (live & (1u << w)) {
-                            if (partial) apply_mask(v[q], mk[w]);
-                            exp32(v[q], cc, mm, acc0, acc1, pw + 16 * q);
+                            exp32(sv + 32 * w, cc, mm, acc0, acc1, pw);
                         } else {
 #pragma unroll
-                            for (int x = 0; x < 16; ++x) pw[16 * q + x] = 0u;
+                            for (int x = 0; x < 16; ++x) pw[x] = 0u;
                         }
+                        tmem_st16(p_tm + 16 * w, pw);
                     }
-                    tmem_st32(s_tm + 32 * h, reinterpret_cast<const float *>(pw));
+                } else {
+                    // pass 2: chunks 2h, 2h+1 are read before P columns [32h, 32h+32) overwrite them
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        uint32_t pw[32];
+                        float v[2][32];
+                        tmem_ld32(s_tm + 64 * h, v[0]);
+                        tmem_ld32(s_tm + 64 * h + 32, v[1]);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            const int w = 2 * h + q;
+                            if (live & (1u << w)) {
+                                if (partial) apply_mask(v[q], mk[w]);
+                                exp32(v[q], cc, mm, acc0, acc1, pw + 16 * q);
+                            } else {
+#pragma unroll
+                                for (int x = 0; x < 16; ++x) pw[16 * q + x] = 0u;
+                            }
+                        }
+                        tmem_st32(p_tm + 32 * h, reinterpret_cast<const float *>(pw));
+                    }
                 }
                 {
                     float a, b, c, d;
