@@ -220,6 +220,40 @@ __device__ __forceinline__ float max32(const float *v)
     return fmax3(fmax3(a0, a1, a2), a3, -INFINITY);
 }
 
+// Number of the 32 exponentials of a chunk evaluated on the FMA pipe instead of MUFU (the MUFU
+// does 16 ex2/clk/SM against 8192 bf16 FLOP/clk on the tensor pipe: at d = 64 it is the
+// co-bottleneck).  Multiple of 4.
+#ifndef SPLAT_NEMU
+#define SPLAT_NEMU 12
+#endif
+
+__device__ __forceinline__ uint64_t fmax2_clamp(uint64_t z)
+{
+    float a, b;
+    unpack2(z, a, b);
+    return pack2(fmaxf(a, -127.f), fmaxf(b, -127.f));
+}
+
+// 2^x for a packed pair on the FMA pipe: x = j + f with j = rint(x) (1.5*2^23 magic-number
+// rounding), f in [-1/2, 1/2]; 2^f by a degree-3 polynomial (max relative error 7.5e-5, far
+// below bf16's 2^-9); the exponent j is added to the bits of 2^f.  x is clamped at -127 so
+// masked (-inf) scores give 0.
+__device__ __forceinline__ void exp2_emu2(uint64_t z, float &ra, float &rb)
+{
+    const uint64_t zc = fmax2_clamp(z);
+    const uint64_t t = fadd2(zc, pack2(12582912.f, 12582912.f));
+    const uint64_t jf = fadd2(t, pack2(-12582912.f, -12582912.f));
+    const uint64_t f = ffma2(jf, pack2(-1.f, -1.f), zc);
+    uint64_t p = ffma2(pack2(0.0551716648f, 0.0551716648f), f, pack2(0.2426111251f, 0.2426111251f));
+    p = ffma2(p, f, pack2(0.6932609677f, 0.6932609677f));
+    p = ffma2(p, f, pack2(0.9999280572f, 0.9999280572f));
+    float pa, pb, ta, tb;
+    unpack2(p, pa, pb);
+    unpack2(t, ta, tb);
+    ra = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23));
+    rb = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
+}
+
 // p = exp2(s*c - m) for 32 scores -> 16 packed bf16 pairs; row-sum partials in acc0/acc1.
 __device__ __forceinline__ void exp32(const float *v, uint64_t cc, uint64_t mm, uint64_t &acc0, uint64_t &acc1,
                                       uint32_t *pw)
@@ -229,9 +263,14 @@ __device__ __forceinline__ void exp32(const float *v, uint64_t cc, uint64_t mm, 
         const uint64_t z0 = ffma2(pack2(v[x], v[x + 1]), cc, mm);
         const uint64_t z1 = ffma2(pack2(v[x + 2], v[x + 3]), cc, mm);
         float a, b, c, d;
-        unpack2(z0, a, b);
-        unpack2(z1, c, d);
-        a = ex2(a); b = ex2(b); c = ex2(c); d = ex2(d);
+        if (x < SPLAT_NEMU) {
+            exp2_emu2(z0, a, b);
+            exp2_emu2(z1, c, d);
+        } else {
+            unpack2(z0, a, b);
+            unpack2(z1, c, d);
+            a = ex2(a); b = ex2(b); c = ex2(c); d = ex2(d);
+        }
         acc0 = fadd2(acc0, pack2(a, b));
         acc1 = fadd2(acc1, pack2(c, d));
         pw[x / 2] = pack_bf16(a, b);
