@@ -127,16 +127,29 @@ __device__ __forceinline__ UnitInfo fetch_unit(const DevAcsr &A, int BH, int u)
 struct EntRegs {
     int r[4];
     uint32_t l[4];   // pair_live words of the same entries
+    int m[4];        // mask id of tile group g (softmax warps only)
 };
 
-__device__ __forceinline__ void load_ents(const DevAcsr &A, const UnitInfo &un, int lane, EntRegs &er)
+__device__ __forceinline__ void load_ents(const DevAcsr &A, const UnitInfo &un, int lane, EntRegs &er, int g = -1)
 {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int idx = un.e0 + lane + 32 * k;
         er.r[k] = idx < un.e1 ? A.pair_ent[idx] : 0;
         er.l[k] = idx < un.e1 ? A.pair_live[idx] : 0u;
+        er.m[k] = (g >= 0 && idx < un.e1) ? (g == 0 ? A.pair_mask[idx].x : A.pair_mask[idx].y) : 0;
     }
+}
+
+__device__ __forceinline__ int mask_at(const DevAcsr &A, const UnitInfo &un, const EntRegs &er, int e, int g)
+{
+    const int i = e - un.e0;
+    if (i < 128) {
+        const int k = i >> 5;
+        const int v = k == 0 ? er.m[0] : (k == 1 ? er.m[1] : (k == 2 ? er.m[2] : er.m[3]));
+        return __shfl_sync(0xffffffffu, v, i & 31);
+    }
+    return g == 0 ? A.pair_mask[e].x : A.pair_mask[e].y;
 }
 
 __device__ __forceinline__ uint32_t live_at(const DevAcsr &A, const UnitInfo &un, const EntRegs &er, int e)
@@ -224,20 +237,21 @@ __device__ __forceinline__ float max32(const float *v)
 // does 16 ex2/clk/SM against 8192 bf16 FLOP/clk on the tensor pipe: at d = 64 it is the
 // co-bottleneck).  Multiple of 4.
 #ifndef SPLAT_NEMU
-#define SPLAT_NEMU 12
+#define SPLAT_NEMU 8
 #endif
 
 __device__ __forceinline__ uint64_t fmax2_clamp(uint64_t z)
 {
     float a, b;
     unpack2(z, a, b);
-    return pack2(fmaxf(a, -127.f), fmaxf(b, -127.f));
+    return pack2(fmaxf(a, -126.f), fmaxf(b, -126.f));
 }
 
 // 2^x for a packed pair on the FMA pipe: x = j + f with j = rint(x) (1.5*2^23 magic-number
 // rounding), f in [-1/2, 1/2]; 2^f by a degree-3 polynomial (max relative error 7.5e-5, far
-// below bf16's 2^-9); the exponent j is added to the bits of 2^f.  x is clamped at -127 so
-// masked (-inf) scores give 0.
+// below bf16's 2^-9); the exponent j is added to the bits of 2^f.  x is clamped at -126 so
+// masked (-inf) scores give 2^-126 (below any bf16 P that matters; -127 would wrap the
+// exponent field of a p just under 1).
 __device__ __forceinline__ void exp2_emu2(uint64_t z, float &ra, float &rb)
 {
     const uint64_t zc = fmax2_clamp(z);
@@ -519,7 +533,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         uint32_t s_cnt = 0, e_cnt = 0;
         UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
         EntRegs ner;
-        load_ents(A, nx, lane, ner);
+        load_ents(A, nx, lane, ner, g);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const UnitInfo un = nx;
             const EntRegs er = ner;
@@ -527,7 +541,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const int pair = un.pair, bh = un.bh;
             const int t = 2 * pair + g;
             if (t >= A.n_qt) {
-                load_ents(A, nx, lane, ner);
+                load_ents(A, nx, lane, ner, g);
                 continue;
             }
             const int row = t * 128 + r;
@@ -543,8 +557,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 uint32_t live = (live_at(A, un, er, e) >> (16 * g + 4 * quad)) & 0xFu;
                 uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
                 if (partial) {
-                    const int2 mid = A.pair_mask[e];
-                    const uint4 m4 = A.masks[(size_t)(g == 0 ? mid.x : mid.y) * 128 + r];
+                    const uint4 m4 = A.masks[(size_t)mask_at(A, un, er, e, g) * 128 + r];
                     mk[0] = m4.x; mk[1] = m4.y; mk[2] = m4.z; mk[3] = m4.w;
                 }
                 if (lane == 0 && quad == 0) TRACE(2 + g, 1);
@@ -606,41 +619,54 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     m_run = mx;
                     l_run *= alpha;
                 }
-                if (SEP && s_cnt > 1) {
-                    // PV of this group's previous tile: complete before O is rescaled or P rewritten
-                    mbar_wait(&pv_done[g], (s_cnt - 2) & 1);
-                    tc_fence_after();
-                }
-                if (!first && __any_sync(0xffffffffu, resc)) {
-                    // O holds every earlier PV of this tile (non-SEP: S_g(j) was computed after PV_g(j-1))
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
-                        float o[32];
-                        tmem_ld32(o_tm + c * 32, o);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int x = 0; x < 32; ++x) o[x] *= alpha;
-                        tmem_st32(o_tm + c * 32, o);
-                    }
-                }
-                if (lane == 0 && quad == 0) TRACE(2 + g, 3);
                 const float mref = m_run == -INFINITY ? 0.f : m_run;
                 const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
                 uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
                 if (prm.dbg & 2) live = 0;
                 if constexpr (SEP) {
+                    // exponentials first (registers), so the previous PV has long finished when
+                    // O is rescaled and P rewritten
+                    uint32_t pw[64];
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
-                        uint32_t pw[16];
                         if (live & (1u << w)) {
-                            exp32(sv + 32 * w, cc, mm, acc0, acc1, pw);
+                            exp32(sv + 32 * w, cc, mm, acc0, acc1, pw + 16 * w);
                         } else {
 #pragma unroll
-                            for (int x = 0; x < 16; ++x) pw[x] = 0u;
+                            for (int x = 0; x < 16; ++x) pw[16 * w + x] = 0u;
                         }
-                        tmem_st16(p_tm + 16 * w, pw);
                     }
+                    if (s_cnt > 1) {
+                        // PV of this group's previous tile: complete before O is rescaled or P rewritten
+                        mbar_wait(&pv_done[g], (s_cnt - 2) & 1);
+                        tc_fence_after();
+                    }
+                    if (!first && __any_sync(0xffffffffu, resc)) {
+#pragma unroll
+                        for (int c = 0; c < D / 32; ++c) {
+                            float o[32];
+                            tmem_ld32(o_tm + c * 32, o);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int x = 0; x < 32; ++x) o[x] *= alpha;
+                            tmem_st32(o_tm + c * 32, o);
+                        }
+                    }
+                    tmem_st32(p_tm, reinterpret_cast<const float *>(pw));
+                    tmem_st32(p_tm + 32, reinterpret_cast<const float *>(pw + 32));
                 } else {
+                    if (!first && __any_sync(0xffffffffu, resc)) {
+                        // O holds every earlier PV of this tile: S_g(j) was computed after PV_g(j-1)
+#pragma unroll
+                        for (int c = 0; c < D / 32; ++c) {
+                            float o[32];
+                            tmem_ld32(o_tm + c * 32, o);
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int x = 0; x < 32; ++x) o[x] *= alpha;
+                            tmem_st32(o_tm + c * 32, o);
+                        }
+                    }
                     // pass 2: chunks 2h, 2h+1 are read before P columns [32h, 32h+32) overwrite them
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
@@ -663,6 +689,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         tmem_st32(p_tm + 32 * h, reinterpret_cast<const float *>(pw));
                     }
                 }
+                if (lane == 0 && quad == 0) TRACE(2 + g, 3);
                 {
                     float a, b, c, d;
                     unpack2(acc0, a, b);
@@ -677,7 +704,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 first = false;
             }
             // next unit's metadata, in the shadow of the epilogue
-            load_ents(A, nx, lane, ner);
+            load_ents(A, nx, lane, ner, g);
             if (lane == 0 && quad == 0) TRACE(2 + g, 7);
             // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
             mbar_wait(&epi[g], e_cnt & 1);
