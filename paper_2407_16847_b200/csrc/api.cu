@@ -117,6 +117,7 @@ void free_device(splat_acsr_s *a)
     cudaFree(a->plan.d_pair_mask);
     cudaFree(a->plan.d_pair_live);
     cudaFree(a->plan.d_masks);
+    cudaFree(a->plan.d_kv_mask);
 }
 
 void finish_host_meta(splat_acsr_s *a)
@@ -146,6 +147,7 @@ DevAcsr dev_view(const splat_acsr_s *a)
     A.pair_mask = reinterpret_cast<const int2 *>(a->plan.d_pair_mask);
     A.pair_live = a->plan.d_pair_live;
     A.masks = reinterpret_cast<const uint4 *>(a->plan.d_masks);
+    A.kv_mask = a->plan.d_kv_mask;
     A.n_pairs = a->plan.n_pairs;
     A.n_buckets = a->plan.n_buckets;
     for (int b = 0; b <= a->plan.n_buckets && b <= kMaxBuckets; ++b) A.bucket_start[b] = a->plan.bucket_start[b];
@@ -263,7 +265,8 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
         (e = cudaMalloc(&P.d_pair_info, sizeof(int32_t) * 4 * P.n_pairs)) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_mask, sizeof(int32_t) * 2 * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_live, sizeof(uint32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess) {
+        (e = cudaMalloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess) {
         free_device(a);
         delete a;
         return cuda_fail(e, "plan allocation");
@@ -289,6 +292,8 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
                             cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && !P.masks.empty())
         e = cudaMemcpyAsync(P.d_masks, P.masks.data(), sizeof(uint32_t) * P.masks.size(), cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && P.n_entries > 0)
+        e = cudaMemcpyAsync(P.d_kv_mask, P.kv_mask.data(), sizeof(int32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) {
         free_device(a);
@@ -363,7 +368,9 @@ splat_status splat_rsddmm(splat_acsr a, const void *Q, const void *K, splat_dtyp
     if (!Q || !K || !S) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
     if (!aligned16(Q) || !aligned16(K) || !aligned16(S)) return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
     DeviceGuard g(a->device);
-    cudaError_t e = launch_rsddmm_simt(dev_view(a), Q, K, dt == SPLAT_BF16, B * H, d, scale, S, (cudaStream_t)stream);
+    cudaError_t e = dt == SPLAT_BF16
+                        ? launch_rsddmm_tc(dev_view(a), Q, K, B * H, d, scale, S, (cudaStream_t)stream)
+                        : launch_rsddmm_simt(dev_view(a), Q, K, false, B * H, d, scale, S, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "splat_rsddmm launch");
     note_launches(1);
     return SPLAT_OK;
@@ -393,7 +400,8 @@ splat_status splat_rspmm(splat_acsr a, const void *P, const void *V, splat_dtype
     if (!P || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
     if (!aligned16(P) || !aligned16(V) || !aligned16(O)) return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
     DeviceGuard g(a->device);
-    cudaError_t e = launch_rspmm_simt(dev_view(a), P, V, dt == SPLAT_BF16, B * H, d, O, (cudaStream_t)stream);
+    cudaError_t e = dt == SPLAT_BF16 ? launch_rspmm_tc(dev_view(a), P, V, B * H, d, O, (cudaStream_t)stream)
+                                     : launch_rspmm_simt(dev_view(a), P, V, false, B * H, d, O, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "splat_rspmm launch");
     note_launches(1);
     return SPLAT_OK;

@@ -27,6 +27,7 @@ struct DevAcsr {
     const int2 *pair_mask;      // [n_pair_entries]: mask id for tile A / B (-1: none)
     const uint32_t *pair_live;  // [n_pair_entries]: chunk liveness per (group, warp quad)
     const uint4 *masks;         // [n_masks][128]: row column masks
+    const int32_t *kv_mask;     // [n_entries]: mask id per (query tile, key tile) entry, -1 = FULL
     int n_pairs, n_buckets;
     int bucket_start[kMaxBuckets + 1];
 };
@@ -48,5 +49,9 @@ cudaError_t launch_mhsa_simt(const DevAcsr &A, const void *Q, const void *K, con
 // when the configuration is outside what they implement.
 cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, int d,
                            float scale, void *O, cudaStream_t st, int *n_launch);
+cudaError_t launch_rsddmm_tc(const DevAcsr &A, const void *Q, const void *K, int BH, int d, float scale, float *S,
+                             cudaStream_t st);
+cudaError_t launch_rspmm_tc(const DevAcsr &A, const void *P, const void *V, int BH, int d, void *O,
+                            cudaStream_t st);
 
 }  // namespace splat

@@ -75,6 +75,9 @@ void build_plan(splat_acsr_s &a)
     P.n_pairs = (P.n_qt + 1) / 2;
     P.pair_ptr.assign(P.n_pairs + 1, 0);
     P.pair_ent.clear();
+    std::vector<int32_t> qent_of_pair_ent[2];   // pair entry -> query-tile entry index of tile A / B
+    qent_of_pair_ent[0].clear();
+    qent_of_pair_ent[1].clear();
     for (int p = 0; p < P.n_pairs; ++p) {
         const int ta = 2 * p, tb = 2 * p + 1;
         int ia = P.qt_ptr[ta], ea = P.qt_ptr[ta + 1];
@@ -84,9 +87,12 @@ void build_plan(splat_acsr_s &a)
             const int kb = ib < eb ? (P.kv[ib] & kKvMask) : 0x7fffffff;
             const int k = std::min(ka, kb);
             int ent = k;
-            if (ka == k) { ent |= kUseA | ((P.kv[ia] & kPartialBit) ? kPartA : 0); ++ia; }
-            if (kb == k) { ent |= kUseB | ((P.kv[ib] & kPartialBit) ? kPartB : 0); ++ib; }
+            int qa = -1, qb = -1;
+            if (ka == k) { ent |= kUseA | ((P.kv[ia] & kPartialBit) ? kPartA : 0); qa = ia; ++ia; }
+            if (kb == k) { ent |= kUseB | ((P.kv[ib] & kPartialBit) ? kPartB : 0); qb = ib; ++ib; }
             P.pair_ent.push_back(ent);
+            qent_of_pair_ent[0].push_back(qa);
+            qent_of_pair_ent[1].push_back(qb);
         }
         P.pair_ptr[p + 1] = (int32_t)P.pair_ent.size();
     }
@@ -154,6 +160,10 @@ void build_plan(splat_acsr_s &a)
         }
     }
     P.n_masks = (int)(P.masks.size() / (128 * 4));
+    P.kv_mask.assign(P.n_entries, -1);
+    for (int e = 0; e < P.n_pair_entries; ++e)
+        for (int g = 0; g < 2; ++g)
+            if (qent_of_pair_ent[g][e] >= 0) P.kv_mask[qent_of_pair_ent[g][e]] = P.pair_mask[(size_t)e * 2 + g];
 }
 
 }  // namespace splat

@@ -144,10 +144,12 @@ struct Plan {
     std::vector<int32_t> pair_mask;   // [n_pair_entries][2]: mask id of tile A / B (-1: FULL or unused)
     std::vector<uint32_t> pair_live;  // [n_pair_entries]: bit 16g + 4 quad + w = chunk w live for warp quad
     std::vector<uint32_t> masks;      // [n_masks][128 rows][4 words]: column mask of each row
+    std::vector<int32_t> kv_mask;     // [n_entries]: mask id of each (query tile, key tile) entry (-1: FULL)
     int32_t *d_qt_ptr = nullptr, *d_kv = nullptr, *d_order = nullptr;
     int32_t *d_pair_ptr = nullptr, *d_pair_ent = nullptr, *d_pair_order = nullptr;
     int32_t *d_pair_info = nullptr, *d_pair_mask = nullptr;
     uint32_t *d_pair_live = nullptr, *d_masks = nullptr;
+    int32_t *d_kv_mask = nullptr;
 };
 
 }  // namespace splat
