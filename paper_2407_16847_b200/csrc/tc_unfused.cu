@@ -2,19 +2,23 @@
 //
 // The paper's primitives (Listing 1 P:412-431 and the R-SpMM listing P:553-568) run one SIMT
 // thread per output point.  Here the dense 128x128 sub-tiles of the contractions named by the
-// tile plan (span specialisation) go through tcgen05:
+// tile plan (span specialisation) go through tcgen05, and the sparse side (the ACSR
+// value arrays S and P, laid out row by row) is moved with coalesced accesses:
 //
-//   R-SDDMM : S_tile = Q_t K_j^T (TMA -> 128B-swizzled SMEM -> tcgen05.mma -> TMEM, double
-//             buffered) and 4 epilogue warps scatter scale * S of the tile's non-zeros to their
-//             ACSR positions (thread = row; position = row_ptr[i] + rank of the column in its
-//             row, the rank of the first column of the tile from the row's runs, the rest by
-//             popcount of the pattern's row mask).
-//   R-SpMM  : the 4 gather warps expand the row's ACSR values of key tile j into a dense bf16
-//             P tile in TMEM (zeros off the mask), then O += P V_j as a TS-MMA (A from TMEM,
-//             V an MN-major SMEM operand), O accumulated in TMEM over the tile's key tiles and
-//             written once as bf16.
+//   R-SDDMM : S_tile^T = K_j Q_t^T (TMA -> 128B-swizzled SMEM -> tcgen05.mma -> TMEM).  In the
+//             transposed accumulator a TMEM lane is a key column and a TMEM column a query row,
+//             so after tcgen05.ld a warp holds 32 consecutive key columns of each query row and
+//             writes scale * S of the row's non-zeros with one coalesced store per row.  The
+//             position of (row i, column c) is row_ptr[i] + (runs of row i left of the tile,
+//             closed form) + (popcount of the pattern's row mask left of c).
+//   R-SpMM  : a warp reads each query row's ACSR segment of key tile j with lanes over columns
+//             (coalesced) and expands it into a dense bf16 P tile in 128B-swizzled SMEM (zeros
+//             off the mask); O += P V_j is an SS-MMA (V an MN-major operand), O accumulated in
+//             TMEM over the tile's key tiles and written once as bf16.
 //
-// Work units: (b*H+h, 128-row query tile), head-major, tiles in LPT order; persistent CTAs.
+// Both kernels run 4 epilogue / gather warpgroups that take the S / P tiles round robin, so
+// four tiles are in flight per SM.  Work units: (b*H+h, 128-row query tile), head-major,
+// query tiles in LPT order; persistent CTAs, one per SM.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -27,21 +31,16 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kThreadsU = 192;           // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue / gather
-constexpr int kSub = 128 * 128;          // [128 rows x 64 bf16] swizzle-128B sub-tile (16 KB)
-
-template <int D>
-struct CfgU {
-    static constexpr int kChunks = D / 64;
-    static constexpr int kTileBytes = kChunks * kSub;
-    static constexpr int QS = 2;
-    static constexpr int KS = D == 64 ? 4 : 3;
-    static constexpr int OFF_Q = 0;                       // SDDMM only
-    static constexpr int OFF_K = OFF_Q + QS * kTileBytes;  // K ring (SDDMM) / V ring (SpMM)
-    static constexpr int OFF_BAR = OFF_K + KS * kTileBytes;
-    static constexpr int NBAR = 2 * QS + 2 * KS + 6;
-    static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
-};
+#ifndef SPLAT_UNF_NWG
+#define SPLAT_UNF_NWG 4
+#endif
+constexpr int kNWG = SPLAT_UNF_NWG;               // epilogue / gather warpgroups
+constexpr int kThreadsU = 64 + 128 * kNWG;        // warp 0 TMA, warp 1 MMA, then the warpgroups
+constexpr int kNWGP = 3;                          // SpMM gather warpgroups (+ 1 epilogue warpgroup)
+constexpr int kThreadsP = 64 + 128 + 128 * kNWGP;
+constexpr int kSub = 128 * 128;                   // [128 rows x 64 bf16] swizzle-128B sub-tile (16 KB)
+constexpr int kRB = 4;                            // SpMM gather, PARTIAL tiles: rows per load batch
+constexpr int kRF = 8;                            // SpMM gather, FULL tiles: rows per load batch
 
 struct ParamsU {
     DevAcsr A;
@@ -58,7 +57,12 @@ __device__ __forceinline__ void unit_tile(const DevAcsr &A, int u, int &bh, int 
     t = A.order[u % A.n_qt];
 }
 
-// number of columns of the row's runs that lie left of column c0
+__device__ __forceinline__ void wg_sync(int id)
+{
+    asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
+// number of columns of run g that lie left of column c0
 __device__ __forceinline__ int run_rank(const int4 &g, int c0)
 {
     if (g.z <= 0 || c0 <= g.x) return 0;
@@ -91,16 +95,33 @@ __device__ __forceinline__ void row_info(const DevAcsr &A, int row, long long &b
 
 // ============================================================================ R-SDDMM
 template <int D>
+struct CfgS {
+    static constexpr int kChunks = D / 64;
+    static constexpr int kTileBytes = kChunks * kSub;
+    static constexpr int QS = 2;
+    static constexpr int KS = D == 64 ? 4 : 3;
+    static constexpr int OFF_Q = 0;
+    static constexpr int OFF_K = OFF_Q + QS * kTileBytes;
+    static constexpr int OFF_TOFF = OFF_K + KS * kTileBytes;                 // [kNWG][2][128] int64
+    static constexpr int OFF_TMASK = OFF_TOFF + kNWG * 2 * 128 * 8;         // [kNWG][2][128] uint4
+    static constexpr int OFF_BAR = OFF_TMASK + kNWG * 2 * 128 * 16;
+    static constexpr int NBAR = 2 * QS + 2 * KS + 2 * kNWG;
+    static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
+    static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+template <int D>
 __global__ void __launch_bounds__(kThreadsU, 1)
 rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK, const ParamsU prm)
 {
-    using C = CfgU<D>;
+    using C = CfgS<D>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // pointer arithmetic on the __shared__ array keeps the state space known (LDS/STS, not generic)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
     uint64_t *q_full = bars, *q_empty = bars + C::QS;
     uint64_t *k_full = q_empty + C::QS, *k_empty = k_full + C::KS;
-    uint64_t *s_full = k_empty + C::KS, *s_empty = s_full + 2;
+    uint64_t *s_full = k_empty + C::KS, *s_empty = s_full + kNWG;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + C::NBAR);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevAcsr &A = prm.A;
@@ -109,11 +130,11 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::QS; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
         for (int i = 0; i < C::KS; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4); }
+        for (int i = 0; i < kNWG; ++i) { mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4); }
         fence_mbar_init();
         tma_prefetch(&tmQ); tma_prefetch(&tmK);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 256);
+    if (warp == 1) tmem_alloc(tmem_slot, 128 * kNWG);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -149,110 +170,144 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             }
         }
     } else if (warp == 1) {
+        // S^T = K Q^T: A = K tile (M = 128 key rows), B = Q tile (N = 128 query rows), both K-major
         constexpr uint32_t idS = idesc_bf16(128, 128, false);
         const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
-        int qi = 0, ki = 0, sb = 0;
-        uint32_t qph = 0, kph = 0, scnt[2] = {0, 0};
+        int qi = 0, ki = 0;
+        uint32_t qph = 0, kph = 0, ns = 0;   // ns: S tiles issued so far (buffer ns % kNWG)
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
             unit_tile(A, u, bh, t);
             mbar_wait(&q_full[qi], qph);
             const uint32_t qb = sQ + qi * C::kTileBytes;
             for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
+                const int sb = ns % kNWG;
                 mbar_wait(&k_full[ki], kph);
-                if (scnt[sb] > 0) mbar_wait(&s_empty[sb], (scnt[sb] - 1) & 1);
+                if (ns >= kNWG) mbar_wait(&s_empty[sb], ((ns / kNWG) - 1) & 1);
                 tc_fence_after();
                 const uint32_t kb = sK + ki * C::kTileBytes;
                 if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t off = (kk >> 2) * kSub + (kk & 3) * 32;
-                        mma_bf16_ss(tmem + sb * 128, sdesc_sw128(qb + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
+                        mma_bf16_ss(tmem + sb * 128, sdesc_sw128(kb + off, 16, 1024), sdesc_sw128(qb + off, 16, 1024),
                                     idS, kk > 0 ? 1u : 0u);
                     }
                     mma_commit(&s_full[sb]);
                     mma_commit(&k_empty[ki]);
                 }
-                ++scnt[sb];
-                sb ^= 1;
+                __syncwarp();
+                ++ns;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
             }
             if (lane == 0) mma_commit(&q_empty[qi]);
+            __syncwarp();
             if (++qi == C::QS) { qi = 0; qph ^= 1; }
         }
     } else {
-        // epilogue: thread = row of the query tile (TMEM lane)
-        const int quad = warp & 3, r = quad * 32 + lane;
+        // epilogue warpgroup eg takes S tiles i = eg, eg + kNWG, ...  Thread r of the group first
+        // publishes its query row's ACSR offset and column mask for the tile; then warp quad
+        // (TMEM lanes = key columns 32 quad .. 32 quad + 31) stores every query row's values.
+        const int eg = (warp - 2) >> 2, quad = warp & 3, r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        int sb = 0;
-        uint32_t scnt[2] = {0, 0};
+        long long *toff = reinterpret_cast<long long *>(smem + C::OFF_TOFF) + eg * 256;
+        uint4 *tmask = reinterpret_cast<uint4 *>(smem + C::OFF_TMASK) + eg * 256;
+        const uint32_t below = (1u << lane) - 1u;
+        const int col = 32 * quad + lane;
+        float *const Sg = prm.S;
+        const float scale = prm.scale;
+        uint32_t i = 0, k = 0;   // i: CTA tile counter, k: this group's tile counter
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
             unit_tile(A, u, bh, t);
+            const int e0 = A.qt_ptr[t], e1 = A.qt_ptr[t + 1];
+            // first tile of this unit owned by eg
+            int e = e0 + (int)((eg - (int)(i % kNWG) + kNWG) % kNWG);
+            i += (uint32_t)(e1 - e0);
+            if (e >= e1) continue;
             const int row = t * 128 + r;
             long long base;
             RowRuns R;
             row_info(A, row, base, R);
-            float *srow = prm.S + (size_t)bh * A.nnz + base;
-            for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
+            const long long rowoff = (long long)bh * A.nnz + base;
+            for (; e < e1; e += kNWG) {
                 const int ent = A.kv[e];
                 const int c0 = (ent & kKvMask) * 128;
-                uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
-                if (ent & kPartialBit) {
-                    const uint4 m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
-                    mk[0] = m4.x; mk[1] = m4.y; mk[2] = m4.z; mk[3] = m4.w;
-                }
-                if (row >= A.n) mk[0] = mk[1] = mk[2] = mk[3] = 0u;
-                const int rk = rank_before(R, c0);
-                float v[128];
-                mbar_wait(&s_full[sb], scnt[sb] & 1);
+                const bool partial = (ent & kPartialBit) != 0;
+                const int tb = (k & 1) * 128;
+                uint4 m4 = make_uint4(~0u, ~0u, ~0u, ~0u);
+                if (partial) m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
+                toff[tb + r] = row < A.n ? rowoff + rank_before(R, c0) : -1ll;
+                tmask[tb + r] = m4;
+                wg_sync(1 + eg);
+                mbar_wait(&s_full[eg], k & 1);
                 tc_fence_after();
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    float v[32];
+                    tmem_ld32(tmem + lane_off + eg * 128 + 32 * c, v);
+                    tmem_wait_ld();
+                    if (c == 3) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&s_empty[eg]);
+                    }
+                    if (!partial) {
 #pragma unroll
-                for (int w = 0; w < 4; ++w) tmem_ld32(tmem + lane_off + sb * 128 + 32 * w, v + 32 * w);
-                tmem_wait_ld();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&s_empty[sb]);
-                ++scnt[sb];
-                sb ^= 1;
-                float *out = srow + rk;
+                        for (int j = 0; j < 32; ++j) {
+                            const long long o = toff[tb + 32 * c + j];
+                            if (o >= 0) Sg[o + col] = scale * v[j];
+                        }
+                    } else {
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    const uint32_t m = mk[w];
-                    if (m == 0xffffffffu) {
-#pragma unroll
-                        for (int x = 0; x < 32; ++x) out[x] = prm.scale * v[32 * w + x];
-                        out += 32;
-                    } else if (m) {
-                        int k = 0;
-#pragma unroll
-                        for (int x = 0; x < 32; ++x)
-                            if ((m >> x) & 1u) out[k++] = prm.scale * v[32 * w + x];
-                        out += k;
+                        for (int j = 0; j < 32; ++j) {
+                            const long long o = toff[tb + 32 * c + j];
+                            const uint4 mm = tmask[tb + 32 * c + j];
+                            const uint32_t mw = quad == 0 ? mm.x : quad == 1 ? mm.y : quad == 2 ? mm.z : mm.w;
+                            const int pre = (quad > 0 ? __popc(mm.x) : 0) + (quad > 1 ? __popc(mm.y) : 0) +
+                                            (quad > 2 ? __popc(mm.z) : 0);
+                            if (o >= 0 && ((mw >> lane) & 1u)) Sg[o + pre + __popc(mw & below)] = scale * v[j];
+                        }
                     }
                 }
+                ++k;
             }
         }
     }
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 128 * kNWG);
     }
 }
 
 // ============================================================================ R-SpMM
 template <int D>
-__global__ void __launch_bounds__(kThreadsU, 1)
+struct CfgP {
+    static constexpr int kChunks = D / 64;
+    static constexpr int kTileBytes = kChunks * kSub;                 // V tile
+    static constexpr int KS = D == 64 ? 4 : 2;
+    static constexpr int OFF_V = 0;
+    static constexpr int OFF_P = OFF_V + KS * kTileBytes;             // [kNWGP] P tiles, 32 KB each
+    static constexpr int OFF_BAR = OFF_P + kNWGP * 2 * kSub;
+    static constexpr int NBAR = 2 * KS + 2 * kNWGP + 4;
+    static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
+    static constexpr int TMEM_COLS = 2 * D;                           // O double buffer
+    static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreadsP, 1)
 rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
 {
-    using C = CfgU<D>;
+    using C = CfgP<D>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // pointer arithmetic on the __shared__ array keeps the state space known (LDS/STS, not generic)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
     uint64_t *v_full = bars, *v_empty = bars + C::KS;
-    uint64_t *p_full = v_empty + C::KS, *p_empty = p_full + 2;
-    uint64_t *o_full = p_empty + 2;
+    uint64_t *p_full = v_empty + C::KS, *p_empty = p_full + kNWGP;
+    uint64_t *o_full = p_empty + kNWGP, *o_empty = o_full + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + C::NBAR);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevAcsr &A = prm.A;
@@ -260,16 +315,16 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::KS; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1); }
-        mbar_init(o_full, 1);
+        for (int i = 0; i < kNWGP; ++i) { mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&o_full[i], 1); mbar_init(&o_empty[i], 4); }
         fence_mbar_init();
         tma_prefetch(&tmV);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 256);
+    if (warp == 1) tmem_alloc(tmem_slot, C::TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;     // P buffers at columns [0,64), [64,128); O at [128, 128+D)
+    const uint32_t tmem = *tmem_slot;     // O buffers at columns [0, D), [D, 2D)
 
     if (warp == 0) {
         int ki = 0, kc = 0;
@@ -284,7 +339,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     mbar_expect_tx(&v_full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
-                        tma_load_3d(smem + C::OFF_K + ki * C::kTileBytes + c * kSub, &tmV, &v_full[ki], 64 * c,
+                        tma_load_3d(smem + C::OFF_V + ki * C::kTileBytes + c * kSub, &tmV, &v_full[ki], 64 * c,
                                     kv * 128, bh);
                 }
                 ++kc;
@@ -293,126 +348,196 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
         }
     } else if (warp == 1) {
         constexpr uint32_t idO = idesc_bf16(128, D, true);
-        const uint32_t sV = smem_u32(smem + C::OFF_K);
-        int ki = 0, pb = 0;
-        uint32_t kph = 0, pcnt[2] = {0, 0};
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const uint32_t sV = smem_u32(smem + C::OFF_V), sP = smem_u32(smem + C::OFF_P);
+        int ki = 0;
+        uint32_t kph = 0, np = 0, uo = 0;   // np: P tiles consumed; uo: units started
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++uo) {
             int bh, t;
             unit_tile(A, u, bh, t);
+            const int ob = uo & 1;
+            if (uo >= 2) mbar_wait(&o_empty[ob], ((uo >> 1) - 1) & 1);
             bool first = true;
             for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
+                const int pb = np % kNWGP;
                 mbar_wait(&v_full[ki], kph);
-                mbar_wait(&p_full[pb], pcnt[pb] & 1);
-                ++pcnt[pb];
+                mbar_wait(&p_full[pb], (np / kNWGP) & 1);
+                ++np;
                 tc_fence_after();
-                const uint32_t vb = sV + ki * C::kTileBytes;
+                const uint32_t vb = sV + ki * C::kTileBytes, pa = sP + pb * 2 * kSub;
                 if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk)
-                        mma_bf16_ts(tmem + 128, tmem + pb * 64 + kk * 8, sdesc_sw128(vb + kk * 2048, kSub, 1024), idO,
-                                    (first && kk == 0) ? 0u : 1u);
+                        mma_bf16_ss(tmem + ob * D, sdesc_sw128(pa + (kk >> 2) * kSub + (kk & 3) * 32, 16, 1024),
+                                    sdesc_sw128(vb + kk * 2048, kSub, 1024), idO, (first && kk == 0) ? 0u : 1u);
                     mma_commit(&v_empty[ki]);
                     mma_commit(&p_empty[pb]);
                 }
+                __syncwarp();
                 first = false;
-                pb ^= 1;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
             }
-            if (lane == 0) mma_commit(o_full);
+            if (lane == 0) mma_commit(&o_full[ob]);
+            __syncwarp();
         }
-    } else {
-        // gather + epilogue: thread = row of the query tile (TMEM lane)
-        const int quad = warp & 3, r = quad * 32 + lane;
-        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        int pb = 0;
-        uint32_t puse[2] = {0, 0}, ocnt = 0;
+    } else if (warp >= 6) {
+        // gather warpgroup eg takes P tiles i = eg, eg + kNWGP, ...; warp quad fills query rows
+        // 32 quad .. 32 quad + 31 of the tile.
+        const int eg = (warp - 6) >> 2, quad = warp & 3, r = quad * 32 + lane;
+        uint8_t *ptile = smem + C::OFF_P + eg * 2 * kSub;
+        const uint32_t below = (1u << lane) - 1u;
+        const unsigned short *Pg = reinterpret_cast<const unsigned short *>(prm.P);
+        const long long total = (long long)prm.BH * A.nnz;   // elements of P
+        uint32_t i = 0, k = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
             unit_tile(A, u, bh, t);
+            const int e0 = A.qt_ptr[t], e1 = A.qt_ptr[t + 1];
+            int e = e0 + (int)((eg - (int)(i % kNWGP) + kNWGP) % kNWGP);
+            i += (uint32_t)(e1 - e0);
             const int row = t * 128 + r;
-            long long base;
-            RowRuns R;
-            row_info(A, row, base, R);
-            const unsigned short *prow =
-                reinterpret_cast<const unsigned short *>(prm.P) + (size_t)bh * A.nnz + base;
-            for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
-                const int ent = A.kv[e];
-                const int c0 = (ent & kKvMask) * 128;
-                uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
-                if (ent & kPartialBit) {
-                    const uint4 m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
-                    mk[0] = m4.x; mk[1] = m4.y; mk[2] = m4.z; mk[3] = m4.w;
-                }
-                if (row >= A.n) mk[0] = mk[1] = mk[2] = mk[3] = 0u;
-                const unsigned short *src = prow + rank_before(R, c0);
-                uint32_t pw[64];
+            if (e < e1) {
+                const int nrows = min(32, A.n - (t * 128 + quad * 32));
+                long long base;
+                RowRuns R;
+                row_info(A, row, base, R);
+                const long long rowoff = (long long)bh * A.nnz + base;
+                for (; e < e1; e += kNWGP) {
+                    const int ent = A.kv[e];
+                    const int c0 = (ent & kKvMask) * 128;
+                    const bool partial = (ent & kPartialBit) != 0;
+                    uint4 m4 = make_uint4(~0u, ~0u, ~0u, ~0u);
+                    if (partial) m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
+                    const long long off = rowoff + rank_before(R, c0);
+                    if (!partial) {
+                        // FULL tile: each row's segment is 128 consecutive values.  Lane l loads the
+                        // 8-byte aligned words l (and l+1 when the segment is not 8-byte aligned) and
+                        // funnel-shifts columns 4l .. 4l+3 out of them: 8 bytes per lane per row.
+                        for (int r0 = 0; r0 < 32; r0 += kRF) {
+                            uint2 c[kRF], x[kRF];
+                            int sh[kRF];
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                    const uint32_t m = mk[w];
-                    uint32_t h[32];
-                    if (m == 0xffffffffu) {
+                            for (int j = 0; j < kRF; ++j) {
+                                const int rr = r0 + j;
+                                const long long o = __shfl_sync(0xffffffffu, off, rr);
+                                const long long a = o & ~3ll;
+                                sh[j] = (int)(o - a);
+                                const uint2 *src = reinterpret_cast<const uint2 *>(Pg + a) + lane;
+                                c[j] = x[j] = make_uint2(0u, 0u);
+                                if (rr < nrows) {
+                                    c[j] = __ldg(src);
+                                    if (sh[j] && a + 4 * lane + 8 <= total) x[j] = __ldg(src + 1);
+                                }
+                            }
+                            if (r0 == 0 && k >= 1) mbar_wait(&p_empty[eg], (k - 1) & 1);
 #pragma unroll
-                        for (int x = 0; x < 32; ++x) h[x] = __ldg(src + x);
-                        src += 32;
-                    } else {
-                        int k = 0;
-#pragma unroll
-                        for (int x = 0; x < 32; ++x) {
-                            h[x] = 0u;
-                            if ((m >> x) & 1u) h[x] = __ldg(src + k++);
+                            for (int j = 0; j < kRF; ++j) {
+                                const int rr = quad * 32 + r0 + j;
+                                uint2 v = c[j];
+                                if (sh[j] == 1) v = make_uint2(__funnelshift_r(c[j].x, c[j].y, 16), __funnelshift_r(c[j].y, x[j].x, 16));
+                                else if (sh[j] == 2) v = make_uint2(c[j].y, x[j].x);
+                                else if (sh[j] == 3) v = make_uint2(__funnelshift_r(c[j].y, x[j].x, 16), __funnelshift_r(x[j].x, x[j].y, 16));
+                                // columns 4 lane .. 4 lane + 3 -> sub-tile lane / 16, swizzled 16-byte chunk
+                                const int byte = rr * 128 + (((((lane & 15) >> 1) ^ (rr & 7))) << 4) + (lane & 1) * 8;
+                                *reinterpret_cast<uint2 *>(ptile + (lane >> 4) * kSub + byte) = v;
+                            }
                         }
-                        src += k;
-                    }
+                    } else {
+                    if (k >= 1) mbar_wait(&p_empty[eg], (k - 1) & 1);
+                    // kRB rows per batch: 4 kRB independent loads in flight per lane
+                    for (int r0 = 0; r0 < 32; r0 += kRB) {
+                        unsigned short h[kRB][4];
 #pragma unroll
-                    for (int x = 0; x < 16; ++x) pw[16 * w + x] = h[2 * x] | (h[2 * x + 1] << 16);
+                        for (int j = 0; j < kRB; ++j) {
+                            const int rr = r0 + j;
+                            const long long o = __shfl_sync(0xffffffffu, off, rr);
+                            const uint32_t mw[4] = {__shfl_sync(0xffffffffu, m4.x, rr), __shfl_sync(0xffffffffu, m4.y, rr),
+                                                    __shfl_sync(0xffffffffu, m4.z, rr), __shfl_sync(0xffffffffu, m4.w, rr)};
+                            const unsigned short *src = Pg + o;
+                            int pre = 0;
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                h[j][w] = 0;
+                                if (rr < nrows && ((mw[w] >> lane) & 1u)) h[j][w] = __ldg(src + pre + __popc(mw[w] & below));
+                                pre += __popc(mw[w]);
+                            }
+                        }
+#pragma unroll
+                        for (int j = 0; j < kRB; ++j) {
+                            const int rr = quad * 32 + r0 + j;     // row within the tile
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                // column 32 w + lane -> sub-tile w/2, 16-byte chunk (col & 63) / 8, swizzled by row
+                                const int cc = (32 * (w & 1) + lane);
+                                const int byte = rr * 128 + ((((cc >> 3) ^ (rr & 7))) << 4) + (cc & 7) * 2;
+                                *reinterpret_cast<unsigned short *>(ptile + (w >> 1) * kSub + byte) = h[j][w];
+                            }
+                        }
+                    }
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&p_full[eg]);
+                    ++k;
                 }
-                // this P buffer is free once the PV that read it two tiles ago has completed
-                if (puse[pb] > 0) mbar_wait(&p_empty[pb], (puse[pb] - 1) & 1);
+            }
+        }
+    } else {
+        // epilogue warpgroup (warps 2..5): O of unit uo (the plain sum P V) -> bf16 -> HBM;
+        // thread = query row.  O is double buffered in TMEM so the MMA runs one unit ahead.
+        const int quad = warp & 3, r = quad * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        uint32_t uo = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++uo) {
+            int bh, t;
+            unit_tile(A, u, bh, t);
+            const int row = t * 128 + r;
+            const int e0 = A.qt_ptr[t], e1 = A.qt_ptr[t + 1];
+            {
+                const int ob = uo & 1;
+                mbar_wait(&o_full[ob], (uo >> 1) & 1);
                 tc_fence_after();
-                tmem_st32(tmem + lane_off + pb * 64, reinterpret_cast<const float *>(pw));
-                tmem_st32(tmem + lane_off + pb * 64 + 32, reinterpret_cast<const float *>(pw + 32));
-                tmem_wait_st();
+                const bool empty = e0 == e1;   // no key tile: O = 0
+                __nv_bfloat16 *orow = prm.O + ((size_t)bh * A.n + row) * D;
+#pragma unroll
+                for (int c = 0; c < D / 32; ++c) {
+                    float o[32];
+                    tmem_ld32(tmem + lane_off + ob * D + c * 32, o);
+                    tmem_wait_ld();
+                    if (empty) {
+#pragma unroll
+                        for (int x = 0; x < 32; ++x) o[x] = 0.f;
+                    }
+                    if (row < A.n) {
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            uint4 w4;
+                            w4.x = pack_bf16(o[8 * v + 0], o[8 * v + 1]);
+                            w4.y = pack_bf16(o[8 * v + 2], o[8 * v + 3]);
+                            w4.z = pack_bf16(o[8 * v + 4], o[8 * v + 5]);
+                            w4.w = pack_bf16(o[8 * v + 6], o[8 * v + 7]);
+                            *reinterpret_cast<uint4 *>(orow + c * 32 + 8 * v) = w4;
+                        }
+                    }
+                }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&p_full[pb]);
-                ++puse[pb];
-                pb ^= 1;
+                if (lane == 0) mbar_arrive(&o_empty[ob]);
             }
-            // epilogue: O (the plain sum P V) -> bf16 -> HBM
-            mbar_wait(o_full, ocnt & 1);
-            ++ocnt;
-            tc_fence_after();
-            const bool empty = A.qt_ptr[t] == A.qt_ptr[t + 1];   // no key tile: O = 0
-            __nv_bfloat16 *orow = prm.O + ((size_t)bh * A.n + row) * D;
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                float o[32];
-                tmem_ld32(tmem + lane_off + 128 + c * 32, o);
-                tmem_wait_ld();
-                if (empty) {
-#pragma unroll
-                    for (int x = 0; x < 32; ++x) o[x] = 0.f;
-                }
-                if (row < A.n) {
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        uint4 w4;
-                        w4.x = pack_bf16(o[8 * v + 0], o[8 * v + 1]);
-                        w4.y = pack_bf16(o[8 * v + 2], o[8 * v + 3]);
-                        w4.z = pack_bf16(o[8 * v + 4], o[8 * v + 5]);
-                        w4.w = pack_bf16(o[8 * v + 6], o[8 * v + 7]);
-                        *reinterpret_cast<uint4 *>(orow + c * 32 + 8 * v) = w4;
-                    }
-                }
-            }
-            tc_fence_before();
         }
     }
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, C::TMEM_COLS);
     }
+}
+
+int grid_for(long long units)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int sms = num_sms(dev);
+    return (int)(units < sms ? units : sms);
 }
 
 template <int D>
@@ -421,18 +546,14 @@ cudaError_t launch_sddmm_d(const DevAcsr &A, const void *Q, const void *K, int B
 {
     CUtensorMap mq, mk;
     if (!make_map(&mq, Q, BH, A.n, D) || !make_map(&mk, K, BH, A.n, D)) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(rsddmm_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgU<D>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(rsddmm_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgS<D>::SMEM);
     if (e != cudaSuccess) return e;
     ParamsU p{};
     p.A = A;
     p.BH = BH;
     p.scale = scale;
     p.S = S;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const long long units = (long long)A.n_qt * BH;
-    const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
-    rsddmm_tc_kernel<D><<<grid, kThreadsU, CfgU<D>::SMEM, st>>>(mq, mk, p);
+    rsddmm_tc_kernel<D><<<grid_for((long long)A.n_qt * BH), kThreadsP, CfgS<D>::SMEM, st>>>(mq, mk, p);
     return cudaGetLastError();
 }
 
@@ -441,18 +562,14 @@ cudaError_t launch_spmm_d(const DevAcsr &A, const void *P, const void *V, int BH
 {
     CUtensorMap mv;
     if (!make_map(&mv, V, BH, A.n, D)) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(rspmm_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgU<D>::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(rspmm_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgP<D>::SMEM);
     if (e != cudaSuccess) return e;
     ParamsU p{};
     p.A = A;
     p.BH = BH;
     p.P = reinterpret_cast<const __nv_bfloat16 *>(P);
     p.O = reinterpret_cast<__nv_bfloat16 *>(O);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const long long units = (long long)A.n_qt * BH;
-    const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
-    rspmm_tc_kernel<D><<<grid, kThreadsU, CfgU<D>::SMEM, st>>>(mv, p);
+    rspmm_tc_kernel<D><<<grid_for((long long)A.n_qt * BH), kThreadsP, CfgP<D>::SMEM, st>>>(mv, p);
     return cudaGetLastError();
 }
 
