@@ -27,8 +27,11 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--max-bh", type=int, default=0, help="cap heads (memory); 0 = all")
     args = ap.parse_args()
-    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-        peaks = json.load(f)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        peaks = {"hbm_gbs": 6650.0}     # B200_PROFILING.md fallback
     hbm = None
     for k, v in peaks.items():
         if "hbm" in k.lower() and isinstance(v, (int, float)):
