@@ -118,6 +118,7 @@ void free_device(splat_acsr_s *a)
     cudaFree(a->plan.d_pair_live);
     cudaFree(a->plan.d_masks);
     cudaFree(a->plan.d_kv_mask);
+    cudaFree(a->plan.d_qt_bits);
 }
 
 void finish_host_meta(splat_acsr_s *a)
@@ -148,6 +149,7 @@ DevAcsr dev_view(const splat_acsr_s *a)
     A.pair_live = a->plan.d_pair_live;
     A.masks = reinterpret_cast<const uint4 *>(a->plan.d_masks);
     A.kv_mask = a->plan.d_kv_mask;
+    A.qt_bits = a->plan.d_qt_bits;
     A.n_pairs = a->plan.n_pairs;
     A.n_buckets = a->plan.n_buckets;
     for (int b = 0; b <= a->plan.n_buckets && b <= kMaxBuckets; ++b) A.bucket_start[b] = a->plan.bucket_start[b];
@@ -262,11 +264,12 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
         (e = cudaMalloc(&P.d_pair_ptr, sizeof(int32_t) * (P.n_pairs + 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_ent, sizeof(int32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_order, sizeof(int32_t) * P.n_pairs)) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_pair_info, sizeof(int32_t) * 4 * P.n_pairs)) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_pair_info, sizeof(int32_t) * 8 * P.n_pairs)) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_mask, sizeof(int32_t) * 2 * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_live, sizeof(uint32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess) {
+        (e = cudaMalloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_qt_bits, sizeof(uint32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess) {
         free_device(a);
         delete a;
         return cuda_fail(e, "plan allocation");
@@ -283,7 +286,7 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_pair_order, P.pair_order.data(), sizeof(int32_t) * P.n_pairs, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(P.d_pair_info, P.pair_info.data(), sizeof(int32_t) * 4 * P.n_pairs, cudaMemcpyHostToDevice, cs);
+        e = cudaMemcpyAsync(P.d_pair_info, P.pair_info.data(), sizeof(int32_t) * 8 * P.n_pairs, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && P.n_pair_entries > 0)
         e = cudaMemcpyAsync(P.d_pair_mask, P.pair_mask.data(), sizeof(int32_t) * 2 * P.n_pair_entries,
                             cudaMemcpyHostToDevice, cs);
@@ -294,6 +297,8 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
         e = cudaMemcpyAsync(P.d_masks, P.masks.data(), sizeof(uint32_t) * P.masks.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && P.n_entries > 0)
         e = cudaMemcpyAsync(P.d_kv_mask, P.kv_mask.data(), sizeof(int32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && P.n_entries > 0)
+        e = cudaMemcpyAsync(P.d_qt_bits, P.qt_bits.data(), sizeof(uint32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) {
         free_device(a);

@@ -113,12 +113,18 @@ void build_plan(splat_acsr_s &a)
         if (i == 0 || bucket(P.pair_order[i]) != bucket(P.pair_order[i - 1])) P.bucket_start.push_back(i);
     P.bucket_start.push_back(P.n_pairs);
     P.n_buckets = (int)P.bucket_start.size() - 1;
-    P.pair_info.assign((size_t)P.n_pairs * 4, 0);
+    // pair_info: (pair, e0, e1, jA0), (jA1, jB1, 0, 0) -- the union range and the two query
+    // tiles' own entry ranges [jA0, jA1) and [jA1, jB1) (adjacent tiles: jB0 == jA1).
+    P.pair_info.assign((size_t)P.n_pairs * 8, 0);
     for (int k = 0; k < P.n_pairs; ++k) {
         const int p = P.pair_order[k];
-        P.pair_info[4 * k + 0] = p;
-        P.pair_info[4 * k + 1] = P.pair_ptr[p];
-        P.pair_info[4 * k + 2] = P.pair_ptr[p + 1];
+        const int ta = 2 * p, tb = std::min(2 * p + 1, P.n_qt);
+        P.pair_info[8 * k + 0] = p;
+        P.pair_info[8 * k + 1] = P.pair_ptr[p];
+        P.pair_info[8 * k + 2] = P.pair_ptr[p + 1];
+        P.pair_info[8 * k + 3] = P.qt_ptr[ta];
+        P.pair_info[8 * k + 4] = P.qt_ptr[ta + 1];
+        P.pair_info[8 * k + 5] = P.qt_ptr[std::min(tb + 1, P.n_qt)];
     }
 
     // ---- per-row column masks of the PARTIAL (tile, key tile) entries (fast-index predicate
@@ -126,6 +132,10 @@ void build_plan(splat_acsr_s &a)
     // liveness of every entry.
     P.pair_mask.assign((size_t)P.n_pair_entries * 2, -1);
     P.pair_live.assign(P.n_pair_entries, 0u);
+    // qt_bits per query-tile entry: bit 4 quad + w = chunk w (32 key columns) has a valid entry
+    // in some row of warp quad; bit 16 + 4 quad + w = every row of the warp has all 32 columns
+    // (the softmax skips the fast-index mask there).
+    P.qt_bits.assign(P.n_entries, 0xFFFFFFFFu);
     P.masks.clear();
     for (int p = 0; p < P.n_pairs; ++p) {
         for (int e = P.pair_ptr[p]; e < P.pair_ptr[p + 1]; ++e) {
@@ -156,6 +166,18 @@ void build_plan(splat_acsr_s &a)
                         if (m[4 * r + w]) P.pair_live[e] |= 1u << (16 * g + 4 * (r >> 5) + w);
                 }
                 P.pair_mask[(size_t)e * 2 + g] = (int32_t)(base / (128 * 4));
+                uint32_t bits = 0;
+                for (int q = 0; q < 4; ++q)
+                    for (int w = 0; w < 4; ++w) {
+                        bool any = false, all = true;
+                        for (int r = 32 * q; r < 32 * q + 32; ++r) {
+                            any |= m[4 * r + w] != 0u;
+                            all &= m[4 * r + w] == ~0u;
+                        }
+                        if (any) bits |= 1u << (4 * q + w);
+                        if (all) bits |= 1u << (16 + 4 * q + w);
+                    }
+                P.qt_bits[qent_of_pair_ent[g][e]] = bits;
             }
         }
     }

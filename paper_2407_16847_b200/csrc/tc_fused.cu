@@ -58,7 +58,8 @@ struct Cfg {
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + 2 * QS * kTileBytes;
     static constexpr int OFF_V = OFF_K + KS * kTileBytes;
-    static constexpr int OFF_BAR = OFF_V + KS * kTileBytes;
+    static constexpr int OFF_O = OFF_V + KS * kTileBytes;          // O staging: one 64-column sub-tile per group
+    static constexpr int OFF_BAR = OFF_O + 2 * kTileBytes64;
     static constexpr int NBAR = 4 * QS + 4 * KS + 10;
     // SEP (d = 64): P gets its own TMEM columns (S 2x128 + O 2x64 + P 2x64 = 512), so S is released
     // as soon as the softmax has loaded it and the next S = Q K^T overlaps the exponentials.
@@ -76,8 +77,8 @@ struct Params {
 };
 
 // Profiling aid (SPLAT_TC_DEBUG & 4): clock64 timestamps of pipeline events in CTA 0.
-__device__ unsigned long long g_trace[4][2048];
-__device__ int g_trace_n[4];
+__device__ unsigned long long g_trace[6][2048];
+__device__ int g_trace_n[6];
 #ifdef SPLAT_TRACE
 // per-role event counter lives in a register (tr_n, declared at the top of the kernel)
 #define TRACE(R, TAG)                                                                                    \
@@ -96,6 +97,7 @@ __device__ int g_trace_n[4];
 // critical path of a role.
 struct UnitInfo {
     int pair, bh, e0, e1;
+    int j0[3];      // the two query tiles' own entry ranges: tile g owns [j0[g], j0[g+1])
 };
 
 __device__ __forceinline__ UnitInfo fetch_unit(const DevAcsr &A, int BH, int u)
@@ -112,13 +114,57 @@ __device__ __forceinline__ UnitInfo fetch_unit(const DevAcsr &A, int BH, int u)
         }
         u -= ub;
     }
-    const int4 info = A.pair_info[k];
+    const int4 info = A.pair_info[2 * k], info2 = A.pair_info[2 * k + 1];
     UnitInfo x;
     x.pair = info.x;
     x.bh = bh;
     x.e0 = info.y;
     x.e1 = info.z;
+    x.j0[0] = info.w;
+    x.j0[1] = info2.x;
+    x.j0[2] = info2.y;
     return x;
+}
+
+// A query tile's own plan entries (softmax warps): lane l caches mask id and chunk bits of
+// entries j0 + l + 32k, k < 2 (beyond 64 entries: global loads).
+struct TileRegs {
+    int m[2];
+    uint32_t b[2];
+};
+
+__device__ __forceinline__ void load_tile(const DevAcsr &A, int j0, int j1, int lane, TileRegs &tr)
+{
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int j = j0 + lane + 32 * k;
+        tr.m[k] = j < j1 ? A.kv_mask[j] : -1;
+        tr.b[k] = j < j1 ? A.qt_bits[j] : 0u;
+    }
+}
+
+__device__ __forceinline__ void tile_at(const DevAcsr &A, const TileRegs &tr, int j0, int j, int &mid, uint32_t &bits)
+{
+    const int i = j - j0;
+    if (i < 64) {
+        mid = __shfl_sync(0xffffffffu, i < 32 ? tr.m[0] : tr.m[1], i & 31);
+        bits = __shfl_sync(0xffffffffu, i < 32 ? tr.b[0] : tr.b[1], i & 31);
+    } else {
+        mid = A.kv_mask[j];
+        bits = A.qt_bits[j];
+    }
+}
+
+// Column mask of row r for entry j (all ones where the warp's chunks need no masking).
+__device__ __forceinline__ uint4 fetch_mask(const DevAcsr &A, const TileRegs &tr, int j0, int j, int quad, int r)
+{
+    int mid;
+    uint32_t bits;
+    tile_at(A, tr, j0, j, mid, bits);
+    const uint32_t need = (bits >> (4 * quad)) & ~(bits >> (16 + 4 * quad)) & 0xFu;
+    uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);
+    if (need && mid >= 0) m = A.masks[(size_t)mid * 128 + r];
+    return m;
 }
 
 // The unit's plan entries cached in the registers of a (uniformly executing) warp: lane l
@@ -289,7 +335,7 @@ __device__ __forceinline__ void apply_mask(float *v, uint32_t m)
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-               const __grid_constant__ CUtensorMap tmV, const Params prm)
+               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const Params prm)
 {
     using C = Cfg<D>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -325,7 +371,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             mbar_init(&s_empty[g], 4); mbar_init(&pv_done[g], 1);
         }
         fence_mbar_init();
-        tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
+        tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmO);
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
@@ -434,6 +480,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             // this PV releases its V.
 #define SPLAT_PV_PENDING()                                                                               \
     do {                                                                                                 \
+        TRACE(1 + 3 * g, 19);                                                                            \
         mbar_wait(&p_full[g], pcnt & 1);                                                                 \
         ++pcnt;                                                                                          \
         mbar_wait(&v_full[pst], pph);                                                                    \
@@ -447,7 +494,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             mma_commit(&v_empty[pst]);                                                                   \
             if (SEP) mma_commit(&pv_done[g]);                                                            \
         }                                                                                                \
-        TRACE(1, 20 + g);                                                                                \
+        TRACE(1 + 3 * g, 20);                                                                             \
         first = false;                                                                                   \
         pend = false;                                                                                    \
     } while (0)
@@ -471,6 +518,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     if (leader) { mbar_arrive(&k_empty[st]); mbar_arrive(&v_empty[st]); }
                     continue;
                 }
+                TRACE(1 + 3 * g, 9);
                 mbar_wait(&k_full[st], ph);
                 if (SEP && scnt > 0) mbar_wait(&s_empty[g], (scnt - 1) & 1);   // previous S loaded
                 ++scnt;
@@ -487,7 +535,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     mma_commit(&s_full[g]);
                     mma_commit(&k_empty[st]);
                 }
-                TRACE(1, 10 + g);
+                TRACE(1 + 3 * g, 10);
                 if (SEP && pend) SPLAT_PV_PENDING();
                 pend = true;
                 pst = st;
@@ -508,6 +556,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     } else {
         // ------------------------------------------------------------ softmax warps (4..7: A, 8..11: B)
+        // Each group walks only its own query tile's plan entries (qt_ptr range in pair_info);
+        // the fast-index mask of the next entry is prefetched one entry ahead (across unit
+        // boundaries too) so its L2 latency never sits on the critical path.
         if constexpr (SEP) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
         const int g = (warp - 4) >> 2;          // tile group: 0 = A, 1 = B
         const int quad = warp & 3;              // TMEM lane quadrant of this warp
@@ -516,65 +567,75 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const uint32_t s_tm = tmem + lane_off + g * 128;
         const uint32_t o_tm = tmem + lane_off + 256 + g * D;
         const uint32_t p_tm = SEP ? tmem + lane_off + 384 + g * 64 : s_tm;
-        const int use_bit = g == 0 ? kUseA : kUseB, part_bit = g == 0 ? kPartA : kPartB;
         const float c2 = prm.scale_log2;
+        const bool store_leader = quad == 0 && lane == 0;
+        uint8_t *ostage = smem + C::OFF_O + g * kTileBytes64;
+        const uint32_t ostage_u = smem_u32(ostage);
         uint32_t s_cnt = 0, e_cnt = 0;
-        UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
-        EntRegs ner;
-        load_ents(A, nx, lane, ner, g);
+        UnitInfo nx{};
+        if (blockIdx.x < n_units) nx = fetch_unit(A, prm.BH, blockIdx.x);
+        TileRegs ntr;
+        load_tile(A, nx.j0[g], nx.j0[g + 1], lane, ntr);
+        uint4 pf = make_uint4(~0u, ~0u, ~0u, ~0u);     // mask of the next entry to process
+        if (nx.j0[g] < nx.j0[g + 1]) pf = fetch_mask(A, ntr, nx.j0[g], nx.j0[g], quad, r);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const UnitInfo un = nx;
-            const EntRegs er = ner;
-            if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
-            const int pair = un.pair, bh = un.bh;
-            const int t = 2 * pair + g;
+            const TileRegs tr = ntr;
+            const bool has_next = u + (int)gridDim.x < n_units;
+            if (has_next) nx = fetch_unit(A, prm.BH, u + gridDim.x);
+            const int j0 = un.j0[g], j1 = un.j0[g + 1];
+            // next unit's entries and its first mask: issued during this unit's last entry
+#define SPLAT_NEXT_UNIT_PREFETCH()                                                                      \
+    do {                                                                                                \
+        if (has_next) {                                                                                 \
+            load_tile(A, nx.j0[g], nx.j0[g + 1], lane, ntr);                                            \
+            if (nx.j0[g] < nx.j0[g + 1]) pf = fetch_mask(A, ntr, nx.j0[g], nx.j0[g], quad, r);          \
+        }                                                                                               \
+    } while (0)
+            const int t = 2 * un.pair + g;
             if (t >= A.n_qt) {
-                load_ents(A, nx, lane, ner, g);
+                SPLAT_NEXT_UNIT_PREFETCH();
                 continue;
             }
-            const int row = t * 128 + r;
+            const int bh = un.bh;
             float m_run = -INFINITY, l_run = 0.f;
             bool first = true;
-            const int e0 = un.e0, e1 = un.e1;
-            for (int e = e0; e < e1; ++e) {
-                const int ent = ent_at(A, un, er, e);
-                if (!(ent & use_bit)) continue;
-                if (lane == 0 && quad == 0) TRACE(2 + g, 5);
-                const bool partial = (ent & part_bit) != 0;
-                // 32-column chunks of this warp with any valid entry (precomputed per pattern)
-                uint32_t live = (live_at(A, un, er, e) >> (16 * g + 4 * quad)) & 0xFu;
-                uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
-                if (partial) {
-                    const uint4 m4 = A.masks[(size_t)mask_at(A, un, er, e, g) * 128 + r];
-                    mk[0] = m4.x; mk[1] = m4.y; mk[2] = m4.z; mk[3] = m4.w;
-                }
-                if (lane == 0 && quad == 0) TRACE(2 + g, 1);
+            if (j0 == j1) SPLAT_NEXT_UNIT_PREFETCH();
+            for (int j = j0; j < j1; ++j) {
+                if (store_leader) TRACE(2 + g, 5);
+                const uint4 m4 = pf;
+                int mid;
+                uint32_t bits;
+                tile_at(A, tr, j0, j, mid, bits);
+                if (j + 1 < j1) pf = fetch_mask(A, tr, j0, j + 1, quad, r);
+                else SPLAT_NEXT_UNIT_PREFETCH();
+                const uint32_t mk[4] = {m4.x, m4.y, m4.z, m4.w};
+                uint32_t live = (bits >> (4 * quad)) & 0xFu;
+                const uint32_t need = live & ~(bits >> (16 + 4 * quad));
                 mbar_wait(&s_full[g], s_cnt & 1);
                 ++s_cnt;
                 tc_fence_after();
-                if (lane == 0 && quad == 0) TRACE(2 + g, 2);
-                if (prm.dbg & 8) {     // profiling aid: no TMEM traffic from the softmax at all
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&p_full[g]);
-                    if (lane == 0 && quad == 0) TRACE(2 + g, 4);
-                    first = false;
-                    continue;
-                }
+                if (store_leader) TRACE(2 + g, 2);
                 float mx = -INFINITY;
                 float sv[SEP ? 128 : 1];
                 if constexpr (SEP) {
-                    // one pass: the whole S row -> registers, then S goes back to the MMA warp
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) tmem_ld32(s_tm + 32 * w, sv + 32 * w);
+                    // the whole S row -> registers in two halves (the second half's load overlaps
+                    // the first half's mask + max), then S goes back to the MMA warp
+                    tmem_ld32(s_tm, sv);
+                    tmem_ld32(s_tm + 32, sv + 32);
                     tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&s_empty[g]);
+                    tmem_ld32(s_tm + 64, sv + 64);
+                    tmem_ld32(s_tm + 96, sv + 96);
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
+                        if (w == 2) {
+                            tmem_wait_ld();
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&s_empty[g]);
+                        }
                         if (live & (1u << w)) {
-                            if (partial) apply_mask(sv + 32 * w, mk[w]);
+                            if (need & (1u << w)) apply_mask(sv + 32 * w, mk[w]);
                             mx = fmax3(mx, max32(sv + 32 * w), -INFINITY);
                         }
                     }
@@ -590,12 +651,13 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         for (int q = 0; q < 2; ++q) {
                             const int w = 2 * w2 + q;
                             if (live & (1u << w)) {
-                                if (partial) apply_mask(v[q], mk[w]);
+                                if (need & (1u << w)) apply_mask(v[q], mk[w]);
                                 mx = fmax3(mx, max32(v[q]), -INFINITY);
                             }
                         }
                     }
                 }
+                if (store_leader) TRACE(2 + g, 12);
                 mx *= c2;
                 float alpha = 1.f;
                 bool resc = false;
@@ -624,11 +686,13 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                             for (int x = 0; x < 16; ++x) pw[16 * w + x] = 0u;
                         }
                     }
+                    if (store_leader) TRACE(2 + g, 13);
                     if (s_cnt > 1) {
                         // PV of this group's previous tile: complete before O is rescaled or P rewritten
                         mbar_wait(&pv_done[g], (s_cnt - 2) & 1);
                         tc_fence_after();
                     }
+                    if (store_leader) TRACE(2 + g, 14);
                     if (!first && __any_sync(0xffffffffu, resc)) {
 #pragma unroll
                         for (int c = 0; c < D / 32; ++c) {
@@ -667,7 +731,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         for (int q = 0; q < 2; ++q) {
                             const int w = 2 * h + q;
                             if (live & (1u << w)) {
-                                if (partial) apply_mask(v[q], mk[w]);
+                                if (need & (1u << w)) apply_mask(v[q], mk[w]);
                                 exp32(v[q], cc, mm, acc0, acc1, pw + 16 * q);
                             } else {
 #pragma unroll
@@ -677,7 +741,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         tmem_st32(p_tm + 32 * h, reinterpret_cast<const float *>(pw));
                     }
                 }
-                if (lane == 0 && quad == 0) TRACE(2 + g, 3);
                 {
                     float a, b, c, d;
                     unpack2(acc0, a, b);
@@ -688,39 +751,44 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&p_full[g]);
-                if (lane == 0 && quad == 0) TRACE(2 + g, 4);
+                if (store_leader) TRACE(2 + g, 4);
                 first = false;
             }
-            // next unit's metadata, in the shadow of the epilogue
-            load_ents(A, nx, lane, ner, g);
-            if (lane == 0 && quad == 0) TRACE(2 + g, 7);
-            // epilogue: wait for the last PV of this tile, O / l -> bf16 -> HBM
+#undef SPLAT_NEXT_UNIT_PREFETCH
+            // epilogue: wait for the last PV of this tile, O / l -> bf16 -> swizzled SMEM stage ->
+            // TMA store (rows beyond N are clipped by the tensor map)
             mbar_wait(&epi[g], e_cnt & 1);
             ++e_cnt;
             tc_fence_after();
-            if (lane == 0 && quad == 0) TRACE(2 + g, 8);
+            if (store_leader) TRACE(2 + g, 8);
             const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-            __nv_bfloat16 *orow = prm.O + ((size_t)bh * prm.N + row) * D;
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                float o[32];
-                tmem_ld32(o_tm + c * 32, o);
+            for (int c = 0; c < D / 64; ++c) {
+                float o[64];
+                tmem_ld32(o_tm + c * 64, o);
+                tmem_ld32(o_tm + c * 64 + 32, o + 32);
                 tmem_wait_ld();
-                if (row < prm.N) {
+                uint32_t w[32];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        uint4 w4;
-                        w4.x = pack_bf16(inv == 0.f ? 0.f : o[8 * v + 0] * inv, inv == 0.f ? 0.f : o[8 * v + 1] * inv);
-                        w4.y = pack_bf16(inv == 0.f ? 0.f : o[8 * v + 2] * inv, inv == 0.f ? 0.f : o[8 * v + 3] * inv);
-                        w4.z = pack_bf16(inv == 0.f ? 0.f : o[8 * v + 4] * inv, inv == 0.f ? 0.f : o[8 * v + 5] * inv);
-                        w4.w = pack_bf16(inv == 0.f ? 0.f : o[8 * v + 6] * inv, inv == 0.f ? 0.f : o[8 * v + 7] * inv);
-                        *reinterpret_cast<uint4 *>(orow + c * 32 + 8 * v) = w4;
-                    }
+                for (int x = 0; x < 32; ++x)
+                    w[x] = inv == 0.f ? 0u : pack_bf16(o[2 * x] * inv, o[2 * x + 1] * inv);
+                if (store_leader) bulk_wait_read0();      // the stage's previous store has read it
+                named_bar(1 + g, 128);
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch)
+                    st_shared_v4(ostage_u + r * 128 + ((ch ^ (r & 7)) << 4), w[4 * ch], w[4 * ch + 1],
+                                 w[4 * ch + 2], w[4 * ch + 3]);
+                fence_proxy_async_smem();
+                named_bar(1 + g, 128);
+                if (store_leader) {
+                    tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
+                    bulk_commit();
                 }
             }
             tc_fence_before();
-            if (lane == 0 && quad == 0) TRACE(2 + g, 9);
+            if (store_leader) TRACE(2 + g, 9);
         }
+        if (store_leader) bulk_wait0();
     }
     __syncthreads();
     if (warp == 1) {
@@ -734,8 +802,9 @@ template <int D>
 cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, float scale, void *O,
                      cudaStream_t st)
 {
-    CUtensorMap mq, mk, mv;
-    if (!make_map(&mq, Q, BH, A.n, D) || !make_map(&mk, K, BH, A.n, D) || !make_map(&mv, V, BH, A.n, D))
+    CUtensorMap mq, mk, mv, mo;
+    if (!make_map(&mq, Q, BH, A.n, D) || !make_map(&mk, K, BH, A.n, D) || !make_map(&mv, V, BH, A.n, D) ||
+        !make_map(&mo, O, BH, A.n, D))
         return cudaErrorInvalidValue;
     static bool attr_set[64] = {false};
     int dev = 0;
@@ -758,7 +827,7 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     p.dbg = dbg;
     const long long units = (long long)A.n_pairs * BH;
     const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
-    mhsa_tc_kernel<D><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, p);
+    mhsa_tc_kernel<D><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, p);
     return cudaGetLastError();
 }
 
@@ -779,7 +848,7 @@ extern "C" int splat_debug_trace(unsigned long long *out, int *counts)
 {
     cudaMemcpyFromSymbol(out, g_trace, sizeof(g_trace));
     cudaMemcpyFromSymbol(counts, g_trace_n, sizeof(g_trace_n));
-    int z[4] = {0, 0, 0, 0};
+    int z[6] = {0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_trace_n, z, sizeof(z));
     return 0;
 }

@@ -16,16 +16,16 @@ Q, K, V = q.cuda(), k.cuda(), v.cuda()
 O = torch.empty_like(Q)
 a = S.Acsr(cfg.pattern)
 L = S.lib()
-buf = (C.c_ulonglong * (4 * 2048))()
-cnt = (C.c_int * 4)()
+buf = (C.c_ulonglong * (6 * 2048))()
+cnt = (C.c_int * 6)()
 for it in range(3):
     S.splat_sparse_mhsa(a, Q, K, V, O, cfg.scale)
     torch.cuda.synchronize()
     L.splat_debug_trace(buf, cnt)
-arr = np.frombuffer(buf, dtype=np.uint64).reshape(4, 2048)
-names = {0: "producer", 1: "mma", 2: "softmaxA", 3: "softmaxB"}
-t0 = min(int(arr[r][0] & 0xffffffffffff) for r in range(4) if cnt[r] > 0)
-for r in range(4):
+arr = np.frombuffer(buf, dtype=np.uint64).reshape(6, 2048)
+names = {0: "producer", 1: "mmaA", 2: "softmaxA", 3: "softmaxB", 4: "mmaB", 5: "unused"}
+t0 = min(int(arr[r][0] & 0xffffffffffff) for r in range(6) if cnt[r] > 0)
+for r in range(6):
     n = min(cnt[r], 2048)
     ev = [(int(x >> 48), int(x & 0xffffffffffff) - t0) for x in arr[r][:n]]
     print(names[r], "events", cnt[r])
