@@ -31,6 +31,10 @@ struct DevAcsr {
     const uint32_t *qt_bits;    // [n_entries]: chunk live (bit 4 quad + w) / full (bit 16 + 4 quad + w)
     int n_pairs, n_buckets;
     int bucket_start[kMaxBuckets + 1];
+    // single query tiles (split-group fused kernel)
+    const int4 *t_info;         // [n_qt]: (tile, j0, j1, 0), bucketed longest first
+    int t_n_buckets;
+    int t_bucket_start[kMaxBuckets + 1];
 };
 
 cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, int64_t *row_ptr,

@@ -70,6 +70,30 @@ void build_plan(splat_acsr_s &a)
         return (P.qt_ptr[x + 1] - P.qt_ptr[x]) > (P.qt_ptr[y + 1] - P.qt_ptr[y]);
     });
 
+    // ---- single query tiles in cost buckets (floor(log2(entries))), longest first: the work
+    // units of the split-group kernel (d = 64), walked head-major inside a bucket.
+    {
+        auto tb = [&](int t) {
+            int len = P.qt_ptr[t + 1] - P.qt_ptr[t], b = 0;
+            while (len > 1) { len >>= 1; ++b; }
+            return b;
+        };
+        std::vector<int> to(P.n_qt);
+        std::iota(to.begin(), to.end(), 0);
+        std::stable_sort(to.begin(), to.end(), [&](int x, int y) { return tb(x) > tb(y); });
+        P.t_bucket_start.clear();
+        for (int i = 0; i < P.n_qt; ++i)
+            if (i == 0 || tb(to[i]) != tb(to[i - 1])) P.t_bucket_start.push_back(i);
+        P.t_bucket_start.push_back(P.n_qt);
+        P.t_n_buckets = (int)P.t_bucket_start.size() - 1;
+        P.t_info.assign((size_t)P.n_qt * 4, 0);
+        for (int k = 0; k < P.n_qt; ++k) {
+            P.t_info[4 * k + 0] = to[k];
+            P.t_info[4 * k + 1] = P.qt_ptr[to[k]];
+            P.t_info[4 * k + 2] = P.qt_ptr[to[k] + 1];
+        }
+    }
+
     // ---- pairs of adjacent query tiles (2p, 2p+1): union of the two sorted key-tile
     // lists, each entry flagged with which tile uses it and whether it is PARTIAL there.
     P.n_pairs = (P.n_qt + 1) / 2;

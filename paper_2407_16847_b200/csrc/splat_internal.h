@@ -146,12 +146,16 @@ struct Plan {
     std::vector<uint32_t> masks;      // [n_masks][128 rows][4 words]: column mask of each row
     std::vector<int32_t> kv_mask;     // [n_entries]: mask id of each (query tile, key tile) entry (-1: FULL)
     std::vector<uint32_t> qt_bits;    // [n_entries]: per-warp chunk live (bits 0-15) / full (bits 16-31)
+    int t_n_buckets = 0;
+    std::vector<int32_t> t_bucket_start;  // single-tile units: bucket boundaries in t_info order
+    std::vector<int32_t> t_info;          // [n_qt][4]: tile, j0, j1, 0 -- bucketed longest first
     int32_t *d_qt_ptr = nullptr, *d_kv = nullptr, *d_order = nullptr;
     int32_t *d_pair_ptr = nullptr, *d_pair_ent = nullptr, *d_pair_order = nullptr;
     int32_t *d_pair_info = nullptr, *d_pair_mask = nullptr;
     uint32_t *d_pair_live = nullptr, *d_masks = nullptr;
     int32_t *d_kv_mask = nullptr;
     uint32_t *d_qt_bits = nullptr;
+    int32_t *d_t_info = nullptr;
 };
 
 }  // namespace splat

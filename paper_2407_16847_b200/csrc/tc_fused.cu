@@ -54,7 +54,7 @@ struct Cfg {
     static constexpr int kChunks = D / 64;
     static constexpr int kTileBytes = kChunks * kTileBytes64;
     static constexpr int QS = D == 64 ? 2 : 1;   // Q buffers per tile group
-    static constexpr int KS = D == 64 ? 3 : 2;   // K and V ring depth
+    static constexpr int KS = D == 64 ? 4 : 2;   // K and V ring depth
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + 2 * QS * kTileBytes;
     static constexpr int OFF_V = OFF_K + KS * kTileBytes;
@@ -383,14 +383,22 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     // warpgroup 0 (TMA, 2 MMA issuers, 1 idle) hands registers to the two softmax warpgroups,
     // which keep a whole 128-column S row in registers: 128*(168-56) == 256*(224-168).  The
     // setmaxnreg of each role sits inside the role's branch so ptxas can allocate per region.
-    if (warp == 0) {
-        // ------------------------------------------------------------ TMA producer (warp-uniform loop)
+    if (warp == 0 || warp == 3) {
+        // ------------------------------------------------------------ TMA producers (warp-uniform loops)
+        // warp 0: Q_A, Q_B of every unit and K_e of every union entry; warp 3: V_e.  K and V rings
+        // advance independently: a K stage frees when both groups' S = Q K^T have completed, a V
+        // stage only after both PVs, so K can run up to KS entries ahead of the softmax.
         if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        const bool kq = warp == 0;
         int qi[2] = {0, 0}, qc[2] = {0, 0};
         uint32_t qph[2] = {0, 0};
         int ki = 0, kc = 0;
         uint32_t kph = 0;
-        UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
+        uint64_t *full = kq ? k_full : v_full, *empty = kq ? k_empty : v_empty;
+        const CUtensorMap *tm = kq ? &tmK : &tmV;
+        uint8_t *ring = smem + (kq ? C::OFF_K : C::OFF_V);
+        UnitInfo nx{};
+        if (blockIdx.x < n_units) nx = fetch_unit(A, prm.BH, blockIdx.x);
         EntRegs ner;
         load_ents(A, nx, lane, ner);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -398,41 +406,36 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const EntRegs er = ner;
             if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
             const int pair = un.pair, bh = un.bh;
+            if (kq) {
 #pragma unroll
-            for (int g = 0; g < 2; ++g) {
-                const int t = 2 * pair + g;
-                if (t >= A.n_qt) continue;
-                const int slot = g * C::QS + qi[g];
-                if (qc[g] >= C::QS) mbar_wait(&q_empty[slot], qph[g] ^ 1);
-                if (lane == 0) {
-                    mbar_expect_tx(&q_full[slot], C::kTileBytes);
+                for (int g = 0; g < 2; ++g) {
+                    const int t = 2 * pair + g;
+                    if (t >= A.n_qt) continue;
+                    const int slot = g * C::QS + qi[g];
+                    if (qc[g] >= C::QS) mbar_wait(&q_empty[slot], qph[g] ^ 1);
+                    if (lane == 0) {
+                        mbar_expect_tx(&q_full[slot], C::kTileBytes);
 #pragma unroll
-                    for (int c = 0; c < C::kChunks; ++c)
-                        tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ, &q_full[slot],
-                                    64 * c, t * 128, bh);
+                        for (int c = 0; c < C::kChunks; ++c)
+                            tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
+                                        &q_full[slot], 64 * c, t * 128, bh);
+                    }
+                    ++qc[g];
+                    if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
                 }
-                ++qc[g];
-                if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
             }
             const int e0 = un.e0, e1 = un.e1;
             for (int e = e0; e < e1; ++e) {
                 const int kv = ent_at(A, un, er, e) & kKvMask;
                 if (e == e0 + 1) load_ents(A, nx, lane, ner);     // next unit's entries, in the shadow
-                if (kc >= C::KS) {
-                    mbar_wait(&k_empty[ki], kph ^ 1);
-                    mbar_wait(&v_empty[ki], kph ^ 1);
-                }
+                TRACE(kq ? 0 : 5, 30);
+                if (kc >= C::KS) mbar_wait(&empty[ki], kph ^ 1);
+                TRACE(kq ? 0 : 5, 31);
                 if (lane == 0) {
-                    mbar_expect_tx(&k_full[ki], C::kTileBytes);
+                    mbar_expect_tx(&full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
-                        tma_load_3d(smem + C::OFF_K + ki * C::kTileBytes + c * kTileBytes64, &tmK, &k_full[ki],
-                                    64 * c, kv * 128, bh);
-                    mbar_expect_tx(&v_full[ki], C::kTileBytes);
-#pragma unroll
-                    for (int c = 0; c < C::kChunks; ++c)
-                        tma_load_3d(smem + C::OFF_V + ki * C::kTileBytes + c * kTileBytes64, &tmV, &v_full[ki],
-                                    64 * c, kv * 128, bh);
+                        tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * 128, bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -482,6 +485,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     do {                                                                                                 \
         TRACE(1 + 3 * g, 19);                                                                            \
         mbar_wait(&p_full[g], pcnt & 1);                                                                 \
+        TRACE(1 + 3 * g, 21);                                                                            \
         ++pcnt;                                                                                          \
         mbar_wait(&v_full[pst], pph);                                                                    \
         tc_fence_after();                                                                                \
@@ -508,14 +512,19 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 // non-SEP: P lives in S's columns, so the PV must precede the next S.  SEP: the next S
                 // goes first (the PV waits for the softmax); a pending PV is still flushed before
                 // waiting on a stage this group does not use (that stage may need its release).
-                if (pend && (!SEP || !ours)) SPLAT_PV_PENDING();
+                // (SEP, skipped entry in the pending PV's own stage: the stage cannot be refilled
+                // before that PV releases it -- flush first)
+                if (pend && (!SEP || (!ours && pst == st))) SPLAT_PV_PENDING();
                 if (!ours) {
-                    // Not ours: release the stage, but only once it holds this entry.  Every group
+                    // Not ours: release the stages, but only once they hold this entry.  Every group
                     // observes every phase of every stage in order -- parity waits are ambiguous
-                    // as soon as a waiter could lag two phases behind a barrier.
+                    // as soon as a waiter could lag two phases behind a barrier.  (SEP: a pending
+                    // PV of an earlier entry uses another V stage, which cannot advance before that
+                    // PV is issued, so it may stay pending.)
                     mbar_wait(&k_full[st], ph);
+                    if (leader) mbar_arrive(&k_empty[st]);
                     mbar_wait(&v_full[st], ph);
-                    if (leader) { mbar_arrive(&k_empty[st]); mbar_arrive(&v_empty[st]); }
+                    if (leader) mbar_arrive(&v_empty[st]);
                     continue;
                 }
                 TRACE(1 + 3 * g, 9);
@@ -552,8 +561,6 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (++qi == C::QS) { qi = 0; qph ^= 1; }
             }
         }
-    } else if (warp == 3) {
-        if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     } else {
         // ------------------------------------------------------------ softmax warps (4..7: A, 8..11: B)
         // Each group walks only its own query tile's plan entries (qt_ptr range in pair_info);
@@ -572,6 +579,42 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         uint8_t *ostage = smem + C::OFF_O + g * kTileBytes64;
         const uint32_t ostage_u = smem_u32(ostage);
         uint32_t s_cnt = 0, e_cnt = 0;
+        // O / l -> bf16 -> swizzled SMEM stage -> TMA store (rows beyond N clipped by the map)
+        auto epilogue = [&](float l, int t, int bh) {
+            mbar_wait(&epi[g], e_cnt & 1);
+            ++e_cnt;
+            tc_fence_after();
+            if (store_leader) TRACE(2 + g, 8);
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+            for (int c = 0; c < D / 64; ++c) {
+                float o[64];
+                tmem_ld32(o_tm + c * 64, o);
+                tmem_ld32(o_tm + c * 64 + 32, o + 32);
+                tmem_wait_ld();
+                uint32_t w[32];
+#pragma unroll
+                for (int x = 0; x < 32; ++x)
+                    w[x] = inv == 0.f ? 0u : pack_bf16(o[2 * x] * inv, o[2 * x + 1] * inv);
+                if (store_leader) bulk_wait_read0();      // the stage's previous store has read it
+                named_bar(1 + g, 128);
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch)
+                    st_shared_v4(ostage_u + r * 128 + ((ch ^ (r & 7)) << 4), w[4 * ch], w[4 * ch + 1],
+                                 w[4 * ch + 2], w[4 * ch + 3]);
+                fence_proxy_async_smem();
+                named_bar(1 + g, 128);
+                if (store_leader) {
+                    tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
+                    bulk_commit();
+                }
+            }
+            tc_fence_before();
+            if (store_leader) TRACE(2 + g, 9);
+        };
+        bool pe_on = false;          // deferred epilogue of the previous unit (SEP)
+        float pe_l = 0.f;
+        int pe_t = 0, pe_bh = 0;
         UnitInfo nx{};
         if (blockIdx.x < n_units) nx = fetch_unit(A, prm.BH, blockIdx.x);
         TileRegs ntr;
@@ -687,6 +730,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         }
                     }
                     if (store_leader) TRACE(2 + g, 13);
+                    if (pe_on) {             // the previous unit's epilogue (first tile of a unit only)
+                        epilogue(pe_l, pe_t, pe_bh);
+                        pe_on = false;
+                    }
                     if (s_cnt > 1) {
                         // PV of this group's previous tile: complete before O is rescaled or P rewritten
                         mbar_wait(&pv_done[g], (s_cnt - 2) & 1);
@@ -755,39 +802,452 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 first = false;
             }
 #undef SPLAT_NEXT_UNIT_PREFETCH
-            // epilogue: wait for the last PV of this tile, O / l -> bf16 -> swizzled SMEM stage ->
-            // TMA store (rows beyond N are clipped by the tensor map)
-            mbar_wait(&epi[g], e_cnt & 1);
+            // epilogue.  SEP: deferred into the next unit's first tile (after its exponentials), so
+            // the wait for this unit's last PV overlaps them; the first PV of the next unit
+            // (accumulate = 0) is issued only after that tile's P, i.e. after O was read out.
+            if constexpr (SEP) {
+                if (j0 == j1) epilogue(l_run, t, bh);      // degenerate: no entry to defer into
+                else { pe_on = true; pe_l = l_run; pe_t = t; pe_bh = bh; }
+            } else {
+                epilogue(l_run, t, bh);
+            }
+        }
+        if (pe_on) epilogue(pe_l, pe_t, pe_bh);
+        if (store_leader) bulk_wait0();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ================================================================ split-group kernel (d = 64)
+//
+// The two tile groups of a CTA run fully independent pipelines (own Q/K/V rings, own
+// producer and MMA warps) over their own stream of single-query-tile work units (bucketed
+// longest first, head-major inside a bucket; group g of CTA c takes units 2c + g + 2k * grid).
+// Sharing K/V loads between two query tiles (the paired kernel above) couples the groups
+// through one ring: a group that does not use an entry still has to wait for its loads, and a
+// long tile stalls its partner.  At d = 64 both groups' rings fit in SMEM, so they are split.
+//
+//   warp 0 / 3 : TMA producer of group 0 / 1 (Q ring of 2, K and V rings of 2)
+//   warp 1 / 2 : MMA issuer of group 0 / 1: S(j) = Q K_j^T as soon as K_j is resident and the
+//                softmax has read S(j-1); then O += P(j-1) V_(j-1).  The pending PV carries
+//                across unit boundaries, so the next unit's first S overlaps the last softmax.
+//   warps 4-7 / 8-11 : softmax of group 0 / 1 (as in the paired kernel, deferred epilogue).
+// TMEM: S_g [128g, 128g+128), O_g [256+64g, +64), P_g [384+64g, +64).
+struct SCfg {
+    static constexpr int QS = 2, KS = 2;
+    static constexpr int TB = kTileBytes64;                      // 16 KB: 128 rows x 64 bf16
+    static constexpr int OFF_Q = 0, OFF_K = QS * TB, OFF_V = OFF_K + KS * TB, OFF_O = OFF_V + KS * TB;
+    static constexpr int GROUP = OFF_O + TB;                     // 112 KB per group
+    static constexpr int OFF_BAR = 2 * GROUP;
+    // per group: q_full[QS] q_empty[QS] k_full[KS] k_empty[KS] v_full[KS] v_empty[KS]
+    //            s_full s_empty p_full pv_done epi
+    static constexpr int NB = 2 * QS + 4 * KS + 5;
+    static constexpr int SMEM = OFF_BAR + 2 * NB * 8 + 16 + 1024;
+};
+
+struct TUnit {
+    int t, bh, j0, j1;
+};
+
+__device__ __forceinline__ TUnit fetch_tunit(const DevAcsr &A, int BH, int v)
+{
+    int k = 0, bh = 0;
+    for (int b = 0; b < A.t_n_buckets; ++b) {
+        const int nb = A.t_bucket_start[b + 1] - A.t_bucket_start[b];
+        const int ub = nb * BH;
+        if (v < ub) {
+            bh = v / nb;
+            k = A.t_bucket_start[b] + v % nb;
+            break;
+        }
+        v -= ub;
+    }
+    const int4 x = A.t_info[k];
+    return TUnit{x.x, bh, x.y, x.z};
+}
+
+// key-tile index of the unit's entries, cached in a (uniformly executing) warp's registers
+struct KvRegs {
+    int r[2];
+};
+
+__device__ __forceinline__ void load_kv(const DevAcsr &A, const TUnit &un, int lane, KvRegs &kr)
+{
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int j = un.j0 + lane + 32 * k;
+        kr.r[k] = j < un.j1 ? (A.kv[j] & kKvMask) : 0;
+    }
+}
+
+__device__ __forceinline__ int kv_at(const DevAcsr &A, const TUnit &un, const KvRegs &kr, int j)
+{
+    const int i = j - un.j0;
+    if (i < 64) return __shfl_sync(0xffffffffu, i < 32 ? kr.r[0] : kr.r[1], i & 31);
+    return A.kv[j] & kKvMask;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const Params prm)
+{
+    using C = SCfg;
+    constexpr int D = 64;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // group of this warp: producers 0 / 3, MMA 1 / 2, softmax 4-7 / 8-11
+    const int g = warp >= 4 ? (warp - 4) >> 2 : (warp == 0 || warp == 1 ? 0 : 1);
+    uint8_t *gs = smem + g * C::GROUP;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR) + g * C::NB;
+    uint64_t *q_full = bars, *q_empty = q_full + C::QS;
+    uint64_t *k_full = q_empty + C::QS, *k_empty = k_full + C::KS;
+    uint64_t *v_full = k_empty + C::KS, *v_empty = v_full + C::KS;
+    uint64_t *s_full = v_empty + C::KS, *s_empty = s_full + 1, *p_full = s_empty + 1;
+    uint64_t *pv_done = p_full + 1, *epi = pv_done + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(reinterpret_cast<uint64_t *>(smem + C::OFF_BAR) + 2 * C::NB);
+    const DevAcsr &A = prm.A;
+    const int n_units = A.n_qt * prm.BH;
+    const int first_unit = 2 * blockIdx.x + g, unit_stride = 2 * gridDim.x;
+#ifdef SPLAT_TRACE
+    int tr_n = 0;
+#endif
+
+    if (threadIdx.x == 0) {
+        for (int gg = 0; gg < 2; ++gg) {
+            uint64_t *b = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR) + gg * C::NB;
+            for (int i = 0; i < 2 * C::QS + 4 * C::KS; ++i) mbar_init(&b[i], 1);
+            const int o = 2 * C::QS + 4 * C::KS;
+            mbar_init(&b[o + 0], 1);   // s_full  (MMA commit)
+            mbar_init(&b[o + 1], 4);   // s_empty (4 softmax warps)
+            mbar_init(&b[o + 2], 4);   // p_full  (4 softmax warps)
+            mbar_init(&b[o + 3], 1);   // pv_done (MMA commit)
+            mbar_init(&b[o + 4], 1);   // epi     (MMA commit)
+        }
+        fence_mbar_init();
+        tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmO);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 || warp == 3) {
+        // ------------------------------------------------------------ TMA producer of group g
+        // Issue order K(j), V(j-1): V(j-1) waits for the PV of j-3 to free its stage, and the K
+        // loads run one entry ahead of it so S never waits for a V release.
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        int qi = 0, qc = 0, ki = 0, kc = 0, vi = 0, vc = 0;
+        uint32_t qph = 0, kph = 0, vph = 0;
+        bool pv = false;            // V of the previous entry still to load
+        int pv_kv = 0, pv_bh = 0;
+        auto load_v = [&]() {
+            if (vc >= C::KS) mbar_wait(&v_empty[vi], vph ^ 1);
+            if (lane == 0) {
+                mbar_expect_tx(&v_full[vi], C::TB);
+                tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * 128, pv_bh);
+            }
+            ++vc;
+            if (++vi == C::KS) { vi = 0; vph ^= 1; }
+            pv = false;
+        };
+        TUnit nx{0, 0, 0, 0};
+        if (first_unit < n_units) nx = fetch_tunit(A, prm.BH, first_unit);
+        KvRegs nkr;
+        load_kv(A, nx, lane, nkr);
+        for (int v = first_unit; v < n_units; v += unit_stride) {
+            const TUnit un = nx;
+            const KvRegs kr = nkr;
+            if (v + unit_stride < n_units) nx = fetch_tunit(A, prm.BH, v + unit_stride);
+            if (qc >= C::QS) mbar_wait(&q_empty[qi], qph ^ 1);
+            if (lane == 0) {
+                mbar_expect_tx(&q_full[qi], C::TB);
+                tma_load_3d(gs + C::OFF_Q + qi * C::TB, &tmQ, &q_full[qi], 0, un.t * 128, un.bh);
+            }
+            ++qc;
+            if (++qi == C::QS) { qi = 0; qph ^= 1; }
+            for (int j = un.j0; j < un.j1; ++j) {
+                const int kv = kv_at(A, un, kr, j);
+                if (j == un.j0 + 1) load_kv(A, nx, lane, nkr);   // next unit's entries, in the shadow
+                TRACE(g == 0 ? 0 : 5, 30);
+                if (kc >= C::KS) mbar_wait(&k_empty[ki], kph ^ 1);
+                TRACE(g == 0 ? 0 : 5, 31);
+                if (lane == 0) {
+                    mbar_expect_tx(&k_full[ki], C::TB);
+                    tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * 128, un.bh);
+                }
+                ++kc;
+                if (++ki == C::KS) { ki = 0; kph ^= 1; }
+                if (pv) load_v();
+                pv = true;
+                pv_kv = kv;
+                pv_bh = un.bh;
+            }
+            if (un.j1 - un.j0 <= 1) load_kv(A, nx, lane, nkr);
+        }
+        if (pv) load_v();
+    } else if (warp == 1 || warp == 2) {
+        // ------------------------------------------------------------ MMA issuer of group g
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        constexpr uint32_t idS = idesc_bf16(128, 128, false);
+        constexpr uint32_t idO = idesc_bf16(128, D, true);
+        const uint32_t sQ = smem_u32(gs + C::OFF_Q), sK = smem_u32(gs + C::OFF_K), sV = smem_u32(gs + C::OFF_V);
+        const bool leader = lane == 0;
+        const uint32_t s_tm = tmem + g * 128, o_tm = tmem + 256 + g * D, p_tm = tmem + 384 + g * 64;
+        int qi = 0;
+        uint32_t qph = 0, pcnt = 0, scnt = 0, gent = 0;
+        // the pending PV (entry whose P the softmax is computing)
+        bool pend = false, p_first = false, p_last = false;
+        int pst = 0, pq = 0;
+        uint32_t pph = 0;
+        auto flush_pv = [&]() {
+            mbar_wait(p_full, pcnt & 1);
+            ++pcnt;
+            mbar_wait(&v_full[pst], pph);
+            tc_fence_after();
+            const uint32_t vbase = sV + pst * C::TB;
+            if (leader) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    if (!(prm.dbg & 1))
+                        mma_bf16_ts(o_tm, p_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024), idO,
+                                    (p_first && kk == 0) ? 0u : 1u);
+                mma_commit(&v_empty[pst]);
+                mma_commit(pv_done);
+                if (p_last) {
+                    mma_commit(epi);
+                    mma_commit(&q_empty[pq]);
+                }
+            }
+            TRACE(1 + 3 * g, 20);
+            pend = false;
+        };
+        TUnit nx{0, 0, 0, 0};
+        if (first_unit < n_units) nx = fetch_tunit(A, prm.BH, first_unit);
+        for (int v = first_unit; v < n_units; v += unit_stride) {
+            const TUnit un = nx;
+            if (v + unit_stride < n_units) nx = fetch_tunit(A, prm.BH, v + unit_stride);
+            mbar_wait(&q_full[qi], qph);
+            const uint32_t qb = sQ + qi * C::TB;
+            if (un.j0 == un.j1) {      // no entries: the epilogue writes zeros
+                if (pend) flush_pv();
+                if (leader) { mma_commit(epi); mma_commit(&q_empty[qi]); }
+            }
+            for (int j = un.j0; j < un.j1; ++j) {
+                const int st = gent % C::KS;
+                const uint32_t ph = (gent / C::KS) & 1;
+                ++gent;
+                TRACE(1 + 3 * g, 9);
+                mbar_wait(&k_full[st], ph);
+                if (scnt > 0) mbar_wait(s_empty, (scnt - 1) & 1);   // softmax has read the previous S
+                ++scnt;
+                tc_fence_after();
+                const uint32_t kbase = sK + st * C::TB;
+                if (leader) {
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk)
+                        if (!(prm.dbg & 1))
+                            mma_bf16_ss(s_tm, sdesc_sw128(qb + kk * 32, 16, 1024), sdesc_sw128(kbase + kk * 32, 16, 1024),
+                                        idS, kk > 0 ? 1u : 0u);
+                    mma_commit(s_full);
+                    mma_commit(&k_empty[st]);
+                }
+                TRACE(1 + 3 * g, 10);
+                if (pend) flush_pv();
+                pend = true;
+                pst = st;
+                pph = ph;
+                p_first = j == un.j0;
+                p_last = j == un.j1 - 1;
+                pq = qi;
+            }
+            if (++qi == C::QS) { qi = 0; qph ^= 1; }
+        }
+        if (pend) flush_pv();
+    } else {
+        // ------------------------------------------------------------ softmax warps of group g
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+        const int quad = warp & 3;              // TMEM lane quadrant of this warp
+        const int r = quad * 32 + lane;         // row within the query tile
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const uint32_t s_tm = tmem + lane_off + g * 128;
+        const uint32_t o_tm = tmem + lane_off + 256 + g * D;
+        const uint32_t p_tm = tmem + lane_off + 384 + g * 64;
+        const float c2 = prm.scale_log2;
+        const bool store_leader = quad == 0 && lane == 0;
+        uint8_t *ostage = gs + C::OFF_O;
+        const uint32_t ostage_u = smem_u32(ostage);
+        uint32_t s_cnt = 0, e_cnt = 0;
+        auto epilogue = [&](float l, int t, int bh) {
+            mbar_wait(epi, e_cnt & 1);
             ++e_cnt;
             tc_fence_after();
             if (store_leader) TRACE(2 + g, 8);
-            const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            float o[64];
+            tmem_ld32(o_tm, o);
+            tmem_ld32(o_tm + 32, o + 32);
+            tmem_wait_ld();
+            uint32_t w[32];
 #pragma unroll
-            for (int c = 0; c < D / 64; ++c) {
-                float o[64];
-                tmem_ld32(o_tm + c * 64, o);
-                tmem_ld32(o_tm + c * 64 + 32, o + 32);
-                tmem_wait_ld();
-                uint32_t w[32];
+            for (int x = 0; x < 32; ++x) w[x] = inv == 0.f ? 0u : pack_bf16(o[2 * x] * inv, o[2 * x + 1] * inv);
+            if (store_leader) bulk_wait_read0();      // the stage's previous store has read it
+            named_bar(1 + g, 128);
 #pragma unroll
-                for (int x = 0; x < 32; ++x)
-                    w[x] = inv == 0.f ? 0u : pack_bf16(o[2 * x] * inv, o[2 * x + 1] * inv);
-                if (store_leader) bulk_wait_read0();      // the stage's previous store has read it
-                named_bar(1 + g, 128);
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch)
-                    st_shared_v4(ostage_u + r * 128 + ((ch ^ (r & 7)) << 4), w[4 * ch], w[4 * ch + 1],
-                                 w[4 * ch + 2], w[4 * ch + 3]);
-                fence_proxy_async_smem();
-                named_bar(1 + g, 128);
-                if (store_leader) {
-                    tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
-                    bulk_commit();
-                }
+            for (int ch = 0; ch < 8; ++ch)
+                st_shared_v4(ostage_u + r * 128 + ((ch ^ (r & 7)) << 4), w[4 * ch], w[4 * ch + 1], w[4 * ch + 2],
+                             w[4 * ch + 3]);
+            fence_proxy_async_smem();
+            named_bar(1 + g, 128);
+            if (store_leader) {
+                tma_store_3d(&tmO, ostage, 0, t * 128, bh);
+                bulk_commit();
             }
             tc_fence_before();
             if (store_leader) TRACE(2 + g, 9);
+        };
+        bool pe_on = false;          // deferred epilogue of the previous unit
+        float pe_l = 0.f;
+        int pe_t = 0, pe_bh = 0;
+        TUnit nx{0, 0, 0, 0};
+        if (first_unit < n_units) nx = fetch_tunit(A, prm.BH, first_unit);
+        TileRegs ntr;
+        load_tile(A, nx.j0, nx.j1, lane, ntr);
+        uint4 pf = make_uint4(~0u, ~0u, ~0u, ~0u);     // mask of the next entry to process
+        if (nx.j0 < nx.j1) pf = fetch_mask(A, ntr, nx.j0, nx.j0, quad, r);
+        for (int v = first_unit; v < n_units; v += unit_stride) {
+            const TUnit un = nx;
+            const TileRegs tr = ntr;
+            const bool has_next = v + unit_stride < n_units;
+            if (has_next) nx = fetch_tunit(A, prm.BH, v + unit_stride);
+            const int j0 = un.j0, j1 = un.j1;
+#define SPLAT_NEXT_UNIT_PREFETCH()                                                                      \
+    do {                                                                                                \
+        if (has_next) {                                                                                 \
+            load_tile(A, nx.j0, nx.j1, lane, ntr);                                                      \
+            if (nx.j0 < nx.j1) pf = fetch_mask(A, ntr, nx.j0, nx.j0, quad, r);                          \
+        }                                                                                               \
+    } while (0)
+            float m_run = -INFINITY, l_run = 0.f;
+            bool first = true;
+            if (j0 == j1) {
+                SPLAT_NEXT_UNIT_PREFETCH();
+                if (pe_on) { epilogue(pe_l, pe_t, pe_bh); pe_on = false; }
+                epilogue(0.f, un.t, un.bh);
+                continue;
+            }
+            for (int j = j0; j < j1; ++j) {
+                if (store_leader) TRACE(2 + g, 5);
+                const uint4 m4 = pf;
+                int mid;
+                uint32_t bits;
+                tile_at(A, tr, j0, j, mid, bits);
+                if (j + 1 < j1) pf = fetch_mask(A, tr, j0, j + 1, quad, r);
+                else SPLAT_NEXT_UNIT_PREFETCH();
+                const uint32_t mk[4] = {m4.x, m4.y, m4.z, m4.w};
+                uint32_t live = (bits >> (4 * quad)) & 0xFu;
+                const uint32_t need = live & ~(bits >> (16 + 4 * quad));
+                mbar_wait(s_full, s_cnt & 1);
+                ++s_cnt;
+                tc_fence_after();
+                if (store_leader) TRACE(2 + g, 2);
+                float mx = -INFINITY;
+                float sv[128];
+                // the whole S row -> registers in two halves (the second half's load overlaps the
+                // first half's mask + max), then S goes back to the MMA warp
+                tmem_ld32(s_tm, sv);
+                tmem_ld32(s_tm + 32, sv + 32);
+                tmem_wait_ld();
+                tmem_ld32(s_tm + 64, sv + 64);
+                tmem_ld32(s_tm + 96, sv + 96);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    if (w == 2) {
+                        tmem_wait_ld();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(s_empty);
+                    }
+                    if (live & (1u << w)) {
+                        if (need & (1u << w)) apply_mask(sv + 32 * w, mk[w]);
+                        mx = fmax3(mx, max32(sv + 32 * w), -INFINITY);
+                    }
+                }
+                if (store_leader) TRACE(2 + g, 12);
+                mx *= c2;
+                float alpha = 1.f;
+                bool resc = false;
+                if (mx > m_run + kRescaleThresh) {
+                    if (m_run != -INFINITY) {
+                        alpha = ex2(m_run - mx);
+                        resc = true;
+                    }
+                    m_run = mx;
+                    l_run *= alpha;
+                }
+                const float mref = m_run == -INFINITY ? 0.f : m_run;
+                const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
+                uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
+                if (prm.dbg & 2) live = 0;
+                uint32_t pw[64];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    if (live & (1u << w)) {
+                        exp32(sv + 32 * w, cc, mm, acc0, acc1, pw + 16 * w);
+                    } else {
+#pragma unroll
+                        for (int x = 0; x < 16; ++x) pw[16 * w + x] = 0u;
+                    }
+                }
+                if (store_leader) TRACE(2 + g, 13);
+                if (pe_on) {             // the previous unit's epilogue (first tile of a unit only)
+                    epilogue(pe_l, pe_t, pe_bh);
+                    pe_on = false;
+                }
+                if (s_cnt > 1) {
+                    // PV of this group's previous entry: complete before O is rescaled or P rewritten
+                    mbar_wait(pv_done, (s_cnt - 2) & 1);
+                    tc_fence_after();
+                }
+                if (store_leader) TRACE(2 + g, 14);
+                if (!first && __any_sync(0xffffffffu, resc)) {
+#pragma unroll
+                    for (int c = 0; c < D / 32; ++c) {
+                        float o[32];
+                        tmem_ld32(o_tm + c * 32, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int x = 0; x < 32; ++x) o[x] *= alpha;
+                        tmem_st32(o_tm + c * 32, o);
+                    }
+                }
+                tmem_st32(p_tm, reinterpret_cast<const float *>(pw));
+                tmem_st32(p_tm + 32, reinterpret_cast<const float *>(pw + 32));
+                {
+                    float a, b, c, d;
+                    unpack2(acc0, a, b);
+                    unpack2(acc1, c, d);
+                    l_run += (a + b) + (c + d);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full);
+                if (store_leader) TRACE(2 + g, 4);
+                first = false;
+            }
+#undef SPLAT_NEXT_UNIT_PREFETCH
+            pe_on = true;
+            pe_l = l_run;
+            pe_t = un.t;
+            pe_bh = un.bh;
         }
+        if (pe_on) epilogue(pe_l, pe_t, pe_bh);
         if (store_leader) bulk_wait0();
     }
     __syncthreads();
@@ -831,6 +1291,39 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     return cudaGetLastError();
 }
 
+cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, float scale,
+                           void *O, cudaStream_t st)
+{
+    CUtensorMap mq, mk, mv, mo;
+    if (!make_map(&mq, Q, BH, A.n, 64) || !make_map(&mk, K, BH, A.n, 64) || !make_map(&mv, V, BH, A.n, 64) ||
+        !make_map(&mo, O, BH, A.n, 64))
+        return cudaErrorInvalidValue;
+    static bool attr_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        cudaError_t e = cudaFuncSetAttribute(mhsa_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SCfg::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set[dev & 63] = true;
+    }
+    Params p;
+    p.A = A;
+    p.BH = BH;
+    p.N = A.n;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.O = reinterpret_cast<__nv_bfloat16 *>(O);
+    static const int dbg = [] {
+        const char *e = getenv("SPLAT_TC_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    p.dbg = dbg;
+    const long long units = (long long)A.n_qt * BH;
+    const long long ctas = (units + 1) / 2;
+    const int grid = (int)(ctas < num_sms(dev) ? ctas : num_sms(dev));
+    mhsa_split_kernel<<<grid, kThreads, SCfg::SMEM, st>>>(mq, mk, mv, mo, p);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 extern "C" int splat_debug_hang(unsigned long long *out)
@@ -857,6 +1350,11 @@ cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const
                            float scale, void *O, cudaStream_t st, int *n_launch)
 {
     *n_launch = 1;
+    static const bool paired64 = [] {
+        const char *e = getenv("SPLAT_TC_PAIRED64");     // diagnostics: the paired kernel at d = 64
+        return e && atoi(e) != 0;
+    }();
+    if (d == 64 && !paired64) return launch_split64(A, Q, K, V, BH, scale, O, st);
     if (d == 64) return launch_d<64>(A, Q, K, V, BH, scale, O, st);
     if (d == 128) return launch_d<128>(A, Q, K, V, BH, scale, O, st);
     return cudaErrorNotSupported;

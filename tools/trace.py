@@ -23,7 +23,7 @@ for it in range(3):
     torch.cuda.synchronize()
     L.splat_debug_trace(buf, cnt)
 arr = np.frombuffer(buf, dtype=np.uint64).reshape(6, 2048)
-names = {0: "producer", 1: "mmaA", 2: "softmaxA", 3: "softmaxB", 4: "mmaB", 5: "unused"}
+names = {0: "producer", 1: "mmaA", 2: "softmaxA", 3: "softmaxB", 4: "mmaB", 5: "vprod"}
 t0 = min(int(arr[r][0] & 0xffffffffffff) for r in range(6) if cnt[r] > 0)
 for r in range(6):
     n = min(cnt[r], 2048)
