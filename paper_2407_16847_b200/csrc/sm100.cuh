@@ -88,6 +88,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         }
     }
 }
+#elif defined(SPLAT_SPIN)
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    while (!mbar_test(bar, parity)) {
+    }
+}
+#elif defined(SPLAT_WAIT_HINT)
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    const uint32_t a = smem_u32(bar);
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity), "n"(SPLAT_WAIT_HINT)
+            : "memory");
+    }
+}
 #else
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
@@ -136,6 +157,17 @@ __device__ __forceinline__ void named_bar(int id, int n)
 __device__ __forceinline__ void fence_proxy_async_smem()
 {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// One lane of a converged warp (elect.sync).  Issuing tcgen05 ops under this predicate, with
+// every operand warp-uniform (e.g. broadcast with __shfl_sync(.., 0)), lets ptxas keep the
+// descriptors in uniform registers and issue UTCHMMAs back to back; under `lane == 0` it wraps
+// each one in an ELECT / R2UR waterfall loop instead.
+__device__ __forceinline__ bool elect_one()
+{
+    uint32_t p;
+    asm volatile("{\n\t.reg .pred q;\n\telect.sync _|q, 0xffffffff;\n\tselp.u32 %0, 1, 0, q;\n\t}" : "=r"(p));
+    return p != 0;
 }
 
 // ----------------------------------------------------------------- tcgen05

@@ -452,15 +452,17 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         // both groups are done with them (empty barriers count two arrivals; a group that skips
         // an entry arrives once the entry is resident).
         if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-        const int g = warp - 1;
+        // uniform values (see elect_one): descriptors stay in uniform registers
+        const int g = __shfl_sync(0xffffffffu, warp - 1, 0);
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
         constexpr uint32_t idS = idesc_bf16(128, 128, false);
         constexpr uint32_t idO = idesc_bf16(128, D, true);
         const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
         const uint32_t sV = smem_u32(smem + C::OFF_V);
         const bool leader = lane == 0;
         const int use_bit = g == 0 ? kUseA : kUseB;
-        const uint32_t s_tm = tmem + g * 128, o_tm = tmem + 256 + g * D;
-        const uint32_t p_tm = SEP ? tmem + 384 + g * 64 : s_tm;
+        const uint32_t s_tm = tmem_u + g * 128, o_tm = tmem_u + 256 + g * D;
+        const uint32_t p_tm = SEP ? tmem_u + 384 + g * 64 : s_tm;
         int qi = 0;
         uint32_t qph = 0, pcnt = 0, scnt = 0;
         uint32_t gent = 0;                                   // global entry counter (ring position)
@@ -468,7 +470,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         EntRegs ner;
         load_ents(A, nx, lane, ner);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const UnitInfo un = nx;
+            UnitInfo un = nx;
+            un.pair = __shfl_sync(0xffffffffu, un.pair, 0);
+            un.e0 = __shfl_sync(0xffffffffu, un.e0, 0);
+            un.e1 = __shfl_sync(0xffffffffu, un.e1, 0);
             const EntRegs er = ner;
             if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
             const bool active = 2 * un.pair + g < A.n_qt;
@@ -490,7 +495,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         mbar_wait(&v_full[pst], pph);                                                                    \
         tc_fence_after();                                                                                \
         const uint32_t vbase = sV + pst * C::kTileBytes;                                                 \
-        if (leader) {                                                                                    \
+        if (elect_one()) {                                                                               \
             _Pragma("unroll") for (int kk = 0; kk < 8; ++kk)                                             \
                 if (!(prm.dbg & 1))                                                                      \
                     mma_bf16_ts(o_tm, p_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024), \
@@ -498,12 +503,13 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             mma_commit(&v_empty[pst]);                                                                   \
             if (SEP) mma_commit(&pv_done[g]);                                                            \
         }                                                                                                \
+        __syncwarp();                                                                                    \
         TRACE(1 + 3 * g, 20);                                                                             \
         first = false;                                                                                   \
         pend = false;                                                                                    \
     } while (0)
             for (int e = un.e0; e < un.e1; ++e) {
-                const int ent = ent_at(A, un, er, e);
+                const int ent = __shfl_sync(0xffffffffu, ent_at(A, un, er, e), 0);
                 const int st = gent % C::KS;
                 const uint32_t ph = (gent / C::KS) & 1;
                 ++gent;
@@ -533,7 +539,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 ++scnt;
                 tc_fence_after();
                 const uint32_t kbase = sK + st * C::kTileBytes;
-                if (leader) {
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;
@@ -544,6 +550,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     mma_commit(&s_full[g]);
                     mma_commit(&k_empty[st]);
                 }
+                __syncwarp();
                 TRACE(1 + 3 * g, 10);
                 if (SEP && pend) SPLAT_PV_PENDING();
                 pend = true;
@@ -554,10 +561,11 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 #undef SPLAT_PV_PENDING
             if (un.e1 - un.e0 <= 1) load_ents(A, nx, lane, ner);
             if (active) {
-                if (leader) {
+                if (elect_one()) {
                     mma_commit(&epi[g]);
                     mma_commit(&q_empty[slot]);
                 }
+                __syncwarp();
                 if (++qi == C::QS) { qi = 0; qph ^= 1; }
             }
         }
@@ -993,12 +1001,23 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         if (pv) load_v();
     } else if (warp == 1 || warp == 2) {
         // ------------------------------------------------------------ MMA issuer of group g
+        // Everything this role computes is made provably warp-uniform (group index, TMEM base and
+        // unit fields broadcast with __shfl_sync) and MMAs / commits are issued under elect.sync,
+        // so the descriptors live in uniform registers and the UTCHMMAs issue back to back.
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        const int gu = __shfl_sync(0xffffffffu, g, 0);
+        const uint32_t tmu = __shfl_sync(0xffffffffu, tmem, 0);
+        uint8_t *gsu = smem + gu * C::GROUP;
+        uint64_t *bu = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR) + gu * C::NB;
+        uint64_t *uq_full = bu, *uq_empty = uq_full + C::QS, *uk_full = uq_empty + C::QS, *uk_empty = uk_full + C::KS;
+        uint64_t *uv_full = uk_empty + C::KS, *uv_empty = uv_full + C::KS;
+        uint64_t *us_full = uv_empty + C::KS, *us_empty = us_full + 1, *up_full = us_empty + 1;
+        uint64_t *upv_done = up_full + 1, *uepi = upv_done + 1;
         constexpr uint32_t idS = idesc_bf16(128, 128, false);
         constexpr uint32_t idO = idesc_bf16(128, D, true);
-        const uint32_t sQ = smem_u32(gs + C::OFF_Q), sK = smem_u32(gs + C::OFF_K), sV = smem_u32(gs + C::OFF_V);
-        const bool leader = lane == 0;
-        const uint32_t s_tm = tmem + g * 128, o_tm = tmem + 256 + g * D, p_tm = tmem + 384 + g * 64;
+        const uint32_t sQ = smem_u32(gsu + C::OFF_Q), sK = smem_u32(gsu + C::OFF_K), sV = smem_u32(gsu + C::OFF_V);
+        const uint32_t s_tm = tmu + gu * 128, o_tm = tmu + 256 + gu * D, p_tm = tmu + 384 + gu * 64;
+        const bool no_mma = (prm.dbg & 1) != 0;
         int qi = 0;
         uint32_t qph = 0, pcnt = 0, scnt = 0, gent = 0;
         // the pending PV (entry whose P the softmax is computing)
@@ -1006,64 +1025,70 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         int pst = 0, pq = 0;
         uint32_t pph = 0;
         auto flush_pv = [&]() {
-            mbar_wait(p_full, pcnt & 1);
+            mbar_wait(up_full, pcnt & 1);
             ++pcnt;
-            mbar_wait(&v_full[pst], pph);
+            mbar_wait(&uv_full[pst], pph);
             tc_fence_after();
             const uint32_t vbase = sV + pst * C::TB;
-            if (leader) {
+            if (elect_one()) {
+                if (!no_mma) {
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    if (!(prm.dbg & 1))
+                    for (int kk = 0; kk < 8; ++kk)
                         mma_bf16_ts(o_tm, p_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024), idO,
                                     (p_first && kk == 0) ? 0u : 1u);
-                mma_commit(&v_empty[pst]);
-                mma_commit(pv_done);
+                }
+                mma_commit(&uv_empty[pst]);
+                mma_commit(upv_done);
                 if (p_last) {
-                    mma_commit(epi);
-                    mma_commit(&q_empty[pq]);
+                    mma_commit(uepi);
+                    mma_commit(&uq_empty[pq]);
                 }
             }
+            __syncwarp();
             TRACE(1 + 3 * g, 20);
             pend = false;
         };
         TUnit nx{0, 0, 0, 0};
         if (first_unit < n_units) nx = fetch_tunit(A, prm.BH, first_unit);
         for (int v = first_unit; v < n_units; v += unit_stride) {
-            const TUnit un = nx;
+            const int uj0 = __shfl_sync(0xffffffffu, nx.j0, 0), uj1 = __shfl_sync(0xffffffffu, nx.j1, 0);
             if (v + unit_stride < n_units) nx = fetch_tunit(A, prm.BH, v + unit_stride);
-            mbar_wait(&q_full[qi], qph);
+            mbar_wait(&uq_full[qi], qph);
             const uint32_t qb = sQ + qi * C::TB;
-            if (un.j0 == un.j1) {      // no entries: the epilogue writes zeros
+            if (uj0 == uj1) {      // no entries: the epilogue writes zeros
                 if (pend) flush_pv();
-                if (leader) { mma_commit(epi); mma_commit(&q_empty[qi]); }
+                if (elect_one()) { mma_commit(uepi); mma_commit(&uq_empty[qi]); }
+                __syncwarp();
             }
-            for (int j = un.j0; j < un.j1; ++j) {
+            for (int j = uj0; j < uj1; ++j) {
                 const int st = gent % C::KS;
                 const uint32_t ph = (gent / C::KS) & 1;
                 ++gent;
                 TRACE(1 + 3 * g, 9);
-                mbar_wait(&k_full[st], ph);
-                if (scnt > 0) mbar_wait(s_empty, (scnt - 1) & 1);   // softmax has read the previous S
+                mbar_wait(&uk_full[st], ph);
+                TRACE(1 + 3 * g, 11);
+                if (scnt > 0) mbar_wait(us_empty, (scnt - 1) & 1);   // softmax has read the previous S
                 ++scnt;
                 tc_fence_after();
                 const uint32_t kbase = sK + st * C::TB;
-                if (leader) {
+                if (elect_one()) {
+                    if (!no_mma) {
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        if (!(prm.dbg & 1))
+                        for (int kk = 0; kk < D / 16; ++kk)
                             mma_bf16_ss(s_tm, sdesc_sw128(qb + kk * 32, 16, 1024), sdesc_sw128(kbase + kk * 32, 16, 1024),
                                         idS, kk > 0 ? 1u : 0u);
-                    mma_commit(s_full);
-                    mma_commit(&k_empty[st]);
+                    }
+                    mma_commit(us_full);
+                    mma_commit(&uk_empty[st]);
                 }
+                __syncwarp();
                 TRACE(1 + 3 * g, 10);
                 if (pend) flush_pv();
                 pend = true;
                 pst = st;
                 pph = ph;
-                p_first = j == un.j0;
-                p_last = j == un.j1 - 1;
+                p_first = j == uj0;
+                p_last = j == uj1 - 1;
                 pq = qi;
             }
             if (++qi == C::QS) { qi = 0; qph ^= 1; }
