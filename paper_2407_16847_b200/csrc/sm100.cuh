@@ -249,6 +249,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t *r)
         : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16_zero(uint32_t taddr)
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(0u)
+        : "memory");
+}
+
 // UMMA shared-memory matrix descriptor, SWIZZLE_128B (sm_100 layout: start>>4 at
 // [0,14), LBO>>4 at [16,30), SBO>>4 at [32,46), version 1 at [46,48), layout 2 at [61,64)).
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes)

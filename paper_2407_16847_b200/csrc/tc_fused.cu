@@ -957,8 +957,12 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         auto load_v = [&]() {
             if (vc >= C::KS) mbar_wait(&v_empty[vi], vph ^ 1);
             if (lane == 0) {
-                mbar_expect_tx(&v_full[vi], C::TB);
-                tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * 128, pv_bh);
+                if (prm.dbg & 16) {          // profiling aid: no TMA traffic (garbage K/V)
+                    mbar_arrive(&v_full[vi]);
+                } else {
+                    mbar_expect_tx(&v_full[vi], C::TB);
+                    tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * 128, pv_bh);
+                }
             }
             ++vc;
             if (++vi == C::KS) { vi = 0; vph ^= 1; }
@@ -986,8 +990,12 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 if (kc >= C::KS) mbar_wait(&k_empty[ki], kph ^ 1);
                 TRACE(g == 0 ? 0 : 5, 31);
                 if (lane == 0) {
-                    mbar_expect_tx(&k_full[ki], C::TB);
-                    tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * 128, un.bh);
+                    if (prm.dbg & 16) {
+                        mbar_arrive(&k_full[ki]);
+                    } else {
+                        mbar_expect_tx(&k_full[ki], C::TB);
+                        tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * 128, un.bh);
+                    }
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
