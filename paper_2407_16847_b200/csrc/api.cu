@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -104,6 +105,15 @@ void free_device(splat_acsr_s *a)
 {
     if (a->device < 0) return;
     DeviceGuard g(a->device);
+    for (splat_acsr_s *sub : {a->sub_band, a->sub_str}) {
+        if (sub) {
+            free_device(sub);
+            delete sub;
+        }
+    }
+    a->sub_band = a->sub_str = nullptr;
+    cudaFree(a->d_lse);
+    a->d_lse = nullptr;
     cudaFree(a->d_seg);
     cudaFree(a->d_nseg);
     cudaFree(a->d_row_ptr);
@@ -191,14 +201,16 @@ bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
 using namespace splat;
 
-extern "C" {
+namespace {
 
-splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, splat_acsr *out)
+// The whole handle build (metadata + plan, device copies); `internal` patterns (the residue
+// decomposition's sub-patterns) skip the public descriptor validation.
+splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_acsr *out, bool internal)
 {
     clear_error();
     if (!p || !out) return set_error(SPLAT_ERR_INVALID_ARG, "null pattern or out pointer");
     *out = nullptr;
-    splat_status st = validate_pattern(*p);
+    splat_status st = internal ? SPLAT_OK : validate_pattern(*p);
     if (st != SPLAT_OK) return st;
     splat_acsr_s *a = new (std::nothrow) splat_acsr_s();
     if (!a) return set_error(SPLAT_ERR_OOM, "host allocation failed");
@@ -314,6 +326,51 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
     }
     *out = a;
     return SPLAT_OK;
+}
+
+// Residue decomposition of STRIDED_LOCAL(l) (see splat_acsr_s::sub_band): applicable when the
+// residue classes tile the sequence exactly (N % l == 0) and whole classes fill a 128-row tile
+// (nk = N / l divides 128, nk >= 2).
+void build_residue_split(splat_acsr_s *a, void *stream)
+{
+    const splat_pattern &p = a->pat;
+    if (p.kind != SPLAT_STRIDED_LOCAL || a->device < 0) return;
+    const int N = a->n, l = p.stride;
+    if (l < 2 || N % l != 0) return;
+    const int nk = N / l;
+    if (nk < 2 || nk > 128 || 128 % nk != 0) return;
+    splat_pattern band{}, str{};
+    band.kind = SPLAT_WINDOW;
+    band.seq_len = N;
+    band.lo = l - 1;
+    band.hi = 0;
+    str.kind = kKindResiduePrev;
+    str.seq_len = N;
+    str.block = nk;
+    splat_acsr hb = nullptr, hs = nullptr;
+    if (build_impl(&band, a->device, stream, &hb, true) != SPLAT_OK) { clear_error(); return; }
+    if (build_impl(&str, a->device, stream, &hs, true) != SPLAT_OK) {
+        clear_error();
+        free_device(hb);
+        delete hb;
+        return;
+    }
+    a->sub_band = hb;
+    a->sub_str = hs;
+    a->rv_l = l;
+    a->rv_nk = nk;
+    a->rv_R = 128 / nk;
+}
+
+}  // namespace
+
+extern "C" {
+
+splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, splat_acsr *out)
+{
+    splat_status st = build_impl(p, device, stream, out, false);
+    if (st == SPLAT_OK) build_residue_split(*out, stream);
+    return st;
 }
 
 splat_status splat_acsr_info(splat_acsr a, int32_t *n, int64_t *nnz, int32_t *max_segs, double *density)
@@ -432,7 +489,23 @@ splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const
     DeviceGuard g(a->device);
     cudaError_t e;
     int nl = 1;
-    if (dt == SPLAT_BF16)
+    static const bool no_split = [] {
+        const char *v = getenv("SPLAT_NO_RESIDUE_SPLIT");     // diagnostics: the single-pass plan
+        return v && atoi(v) != 0;
+    }();
+    if (dt == SPLAT_BF16 && d == 128 && a->sub_band && !no_split) {
+        // residue decomposition: handle-owned lse scratch, grown on the first call with this B*H
+        const size_t need = (size_t)B * H * a->n;
+        if (a->lse_cap < need) {
+            cudaFree(a->d_lse);
+            a->d_lse = nullptr;
+            a->lse_cap = 0;
+            if ((e = cudaMalloc(&a->d_lse, need * sizeof(float))) != cudaSuccess) return cuda_fail(e, "lse scratch");
+            a->lse_cap = need;
+        }
+        e = launch_mhsa_tc_residue(dev_view(a->sub_band), dev_view(a->sub_str), a->rv_l, a->rv_nk, a->rv_R, a->d_lse,
+                                   Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
+    } else if (dt == SPLAT_BF16)
         e = launch_mhsa_tc(dev_view(a), Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
     else
         e = launch_mhsa_simt(dev_view(a), Q, K, V, false, B * H, d, scale, O, (cudaStream_t)stream);

@@ -54,6 +54,11 @@ cudaError_t launch_mhsa_simt(const DevAcsr &A, const void *Q, const void *K, con
 // when the configuration is outside what they implement.
 cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, int d,
                            float scale, void *O, cudaStream_t st, int *n_launch);
+// Residue decomposition of STRIDED_LOCAL (splat_acsr_s::sub_band): pass 1 over the strided
+// component in residue-major order, pass 2 over the causal band merging both partial softmaxes.
+cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int l, int nk, int R, float *lse,
+                                   const void *Q, const void *K, const void *V, int BH, int d, float scale, void *O,
+                                   cudaStream_t st, int *n_launch);
 cudaError_t launch_rsddmm_tc(const DevAcsr &A, const void *Q, const void *K, int BH, int d, float scale, float *S,
                              cudaStream_t st);
 cudaError_t launch_rspmm_tc(const DevAcsr &A, const void *P, const void *V, int BH, int d, void *O,

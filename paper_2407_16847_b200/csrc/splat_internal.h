@@ -25,6 +25,12 @@ struct Seg {
     int32_t start, step, count;
 };
 
+// Internal pattern kind (never accepted from the ABI): the strided component of STRIDED_LOCAL(l)
+// in residue-major row order.  With nk = N / l rows per residue (field `block`), permuted row
+// r = rho * nk + k is natural row rho + l k, and it attends permuted keys rho * nk + m, m < k
+// (natural keys j = rho + l m = i - l (k - m)): one affine run (rho nk, 1, k) per row.
+constexpr int32_t kKindResiduePrev = 100;
+
 SPLAT_HD int imin(int a, int b) { return a < b ? a : b; }
 SPLAT_HD int imax(int a, int b) { return a > b ? a : b; }
 
@@ -110,6 +116,11 @@ SPLAT_HD int row_segments(const splat_pattern &p, int i, Seg *s)
         }
         break;
     }
+    case kKindResiduePrev: {
+        const int nk = p.block;
+        SPLAT_ADD((i / nk) * nk, 1, i % nk);
+        break;
+    }
     case SPLAT_STRIDED_LOCAL: {
         int l = p.stride;
         if (i < l || l == 1) {
@@ -175,6 +186,16 @@ struct splat_acsr_s {
     uint8_t *d_nseg = nullptr;
     int64_t *d_row_ptr = nullptr;
     splat::Plan plan;
+    // Residue decomposition of STRIDED_LOCAL(l): the mask is the
+    // disjoint union of a causal band WINDOW(l-1, 0) (natural order) and the strided keys
+    // i - l m, m >= 1, which become a dense strictly-causal block per residue class i mod l
+    // (row classes by residue of the stride).  The fused kernel runs the
+    // strided part on residue-major views of Q/K/V/O (4-D tensor maps) and merges the two
+    // partial softmaxes in the band pass's epilogue.  Null when not applicable.
+    splat_acsr_s *sub_band = nullptr, *sub_str = nullptr;
+    int32_t rv_l = 0, rv_nk = 0, rv_R = 0;   // stride, rows per residue (N / l), residues per 128-row tile
+    float *d_lse = nullptr;                   // [B*H*N] log2-sum-exp of the strided pass (grown on demand)
+    size_t lse_cap = 0;
 };
 
 namespace splat {

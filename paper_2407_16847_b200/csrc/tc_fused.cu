@@ -74,6 +74,12 @@ struct Params {
     float scale_log2;
     __nv_bfloat16 *O;
     int dbg;        // profiling aid only (SPLAT_TC_DEBUG): 1 = no MMAs issued, 2 = no softmax math
+    // residue decomposition (splat_acsr_s::sub_band), paired kernel only:
+    //   pass 1 (view = 1): tiles are residue-major (4-D maps, R residues x nk rows); the epilogue
+    //                      stores O_s / l_s to the natural rows of O and lse2 = m + log2(l) to lse
+    //   pass 2 (merge = 1): natural band tiles; the epilogue merges with O_s (read from O) and lse
+    int view, merge, rv_R, rv_nk, rv_l;
+    float *lse;
 };
 
 // Profiling aid (SPLAT_TC_DEBUG & 4): clock64 timestamps of pipeline events in CTA 0.
@@ -417,8 +423,12 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         mbar_expect_tx(&q_full[slot], C::kTileBytes);
 #pragma unroll
                         for (int c = 0; c < C::kChunks; ++c)
-                            tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
-                                        &q_full[slot], 64 * c, t * 128, bh);
+                            if (prm.view)
+                                tma_load_4d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
+                                            &q_full[slot], 64 * c, 0, t * prm.rv_R, bh);
+                            else
+                                tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
+                                            &q_full[slot], 64 * c, t * 128, bh);
                     }
                     ++qc[g];
                     if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
@@ -435,7 +445,11 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     mbar_expect_tx(&full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
-                        tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * 128, bh);
+                        if (prm.view)
+                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, 0,
+                                        kv * prm.rv_R, bh);
+                        else
+                            tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * 128, bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -588,12 +602,29 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const uint32_t ostage_u = smem_u32(ostage);
         uint32_t s_cnt = 0, e_cnt = 0;
         // O / l -> bf16 -> swizzled SMEM stage -> TMA store (rows beyond N clipped by the map)
-        auto epilogue = [&](float l, int t, int bh) {
+        auto epilogue = [&](float l, float m, int t, int bh) {
             mbar_wait(&epi[g], e_cnt & 1);
             ++e_cnt;
             tc_fence_after();
             if (store_leader) TRACE(2 + g, 8);
-            const float inv = l > 0.f ? 1.f / l : 0.f;
+            float inv = l > 0.f ? 1.f / l : 0.f;
+            // residue decomposition: natural row of this thread's tile row
+            const int nat = prm.view ? (t * prm.rv_R + r / prm.rv_nk) + prm.rv_l * (r % prm.rv_nk) : t * 128 + r;
+            const bool in_range = nat < prm.N;
+            float a_s = 0.f;                      // merge weight of the strided partial (pass 2)
+            if (prm.view && in_range)
+                prm.lse[(size_t)bh * prm.N + nat] = l > 0.f ? m + __log2f(l) : -INFINITY;
+            if (prm.merge) {
+                // O = (O_b 2^(m_b - M) + O_s 2^(lse_s - M)) / (l_b 2^(m_b - M) + 2^(lse_s - M))
+                const float lse_s = in_range ? prm.lse[(size_t)bh * prm.N + nat] : -INFINITY;
+                const float lse_b = l > 0.f ? m + __log2f(l) : -INFINITY;
+                const float M = fmaxf(lse_b, lse_s);
+                const float a_b = l > 0.f ? ex2(m - M) : 0.f;
+                a_s = lse_s == -INFINITY ? 0.f : ex2(lse_s - M);
+                const float den = l * a_b + a_s;
+                inv = den > 0.f ? a_b / den : 0.f;
+                a_s = den > 0.f ? a_s / den : 0.f;
+            }
 #pragma unroll
             for (int c = 0; c < D / 64; ++c) {
                 float o[64];
@@ -601,9 +632,22 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 tmem_ld32(o_tm + c * 64 + 32, o + 32);
                 tmem_wait_ld();
                 uint32_t w[32];
+                if (prm.merge) {
+                    uint4 os[8];
+                    const uint4 *src = reinterpret_cast<const uint4 *>(prm.O + ((size_t)bh * prm.N + nat) * D + 64 * c);
 #pragma unroll
-                for (int x = 0; x < 32; ++x)
-                    w[x] = inv == 0.f ? 0u : pack_bf16(o[2 * x] * inv, o[2 * x + 1] * inv);
+                    for (int q = 0; q < 8; ++q) os[q] = in_range ? src[q] : make_uint4(0u, 0u, 0u, 0u);
+                    const uint32_t *ow = reinterpret_cast<const uint32_t *>(os);
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) {
+                        const float s0 = __uint_as_float(ow[x] << 16), s1 = __uint_as_float(ow[x] & 0xffff0000u);
+                        w[x] = pack_bf16(o[2 * x] * inv + s0 * a_s, o[2 * x + 1] * inv + s1 * a_s);
+                    }
+                } else {
+#pragma unroll
+                    for (int x = 0; x < 32; ++x)
+                        w[x] = inv == 0.f ? 0u : pack_bf16(o[2 * x] * inv, o[2 * x + 1] * inv);
+                }
                 if (store_leader) bulk_wait_read0();      // the stage's previous store has read it
                 named_bar(1 + g, 128);
 #pragma unroll
@@ -613,7 +657,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 fence_proxy_async_smem();
                 named_bar(1 + g, 128);
                 if (store_leader) {
-                    tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
+                    if (prm.view) tma_store_4d(&tmO, ostage, 64 * c, 0, t * prm.rv_R, bh);
+                    else tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
                     bulk_commit();
                 }
             }
@@ -621,7 +666,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             if (store_leader) TRACE(2 + g, 9);
         };
         bool pe_on = false;          // deferred epilogue of the previous unit (SEP)
-        float pe_l = 0.f;
+        float pe_l = 0.f, pe_m = 0.f;
         int pe_t = 0, pe_bh = 0;
         UnitInfo nx{};
         if (blockIdx.x < n_units) nx = fetch_unit(A, prm.BH, blockIdx.x);
@@ -739,7 +784,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     }
                     if (store_leader) TRACE(2 + g, 13);
                     if (pe_on) {             // the previous unit's epilogue (first tile of a unit only)
-                        epilogue(pe_l, pe_t, pe_bh);
+                        epilogue(pe_l, pe_m, pe_t, pe_bh);
                         pe_on = false;
                     }
                     if (s_cnt > 1) {
@@ -814,13 +859,13 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             // the wait for this unit's last PV overlaps them; the first PV of the next unit
             // (accumulate = 0) is issued only after that tile's P, i.e. after O was read out.
             if constexpr (SEP) {
-                if (j0 == j1) epilogue(l_run, t, bh);      // degenerate: no entry to defer into
-                else { pe_on = true; pe_l = l_run; pe_t = t; pe_bh = bh; }
+                if (j0 == j1) epilogue(l_run, m_run, t, bh);      // degenerate: no entry to defer into
+                else { pe_on = true; pe_l = l_run; pe_m = m_run; pe_t = t; pe_bh = bh; }
             } else {
-                epilogue(l_run, t, bh);
+                epilogue(l_run, m_run, t, bh);
             }
         }
-        if (pe_on) epilogue(pe_l, pe_t, pe_bh);
+        if (pe_on) epilogue(pe_l, pe_m, pe_t, pe_bh);
         if (store_leader) bulk_wait0();
     }
     __syncthreads();
@@ -1291,14 +1336,25 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 }
 
 // ---------------------------------------------------------------- host side
+// Residue-decomposition pass arguments (Params::view / merge); all zero for a plain launch.
+struct ResidueArgs {
+    int view = 0, merge = 0, R = 0, nk = 0, l = 0;
+    float *lse = nullptr;
+};
+
 template <int D>
 cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, float scale, void *O,
-                     cudaStream_t st)
+                     cudaStream_t st, const ResidueArgs &ra = ResidueArgs())
 {
     CUtensorMap mq, mk, mv, mo;
-    if (!make_map(&mq, Q, BH, A.n, D) || !make_map(&mk, K, BH, A.n, D) || !make_map(&mv, V, BH, A.n, D) ||
-        !make_map(&mo, O, BH, A.n, D))
+    if (ra.view) {
+        if (!make_map_residue(&mq, Q, BH, A.n, D, ra.l, ra.nk, ra.R) || !make_map_residue(&mk, K, BH, A.n, D, ra.l, ra.nk, ra.R) ||
+            !make_map_residue(&mv, V, BH, A.n, D, ra.l, ra.nk, ra.R) || !make_map_residue(&mo, O, BH, A.n, D, ra.l, ra.nk, ra.R))
+            return cudaErrorInvalidValue;
+    } else if (!make_map(&mq, Q, BH, A.n, D) || !make_map(&mk, K, BH, A.n, D) || !make_map(&mv, V, BH, A.n, D) ||
+               !make_map(&mo, O, BH, A.n, D)) {
         return cudaErrorInvalidValue;
+    }
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1318,6 +1374,12 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
         return e ? atoi(e) : 0;
     }();
     p.dbg = dbg;
+    p.view = ra.view;
+    p.merge = ra.merge;
+    p.rv_R = ra.R;
+    p.rv_nk = ra.nk;
+    p.rv_l = ra.l;
+    p.lse = ra.lse;
     const long long units = (long long)A.n_pairs * BH;
     const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
     mhsa_tc_kernel<D><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, p);
@@ -1339,7 +1401,7 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
         if (e != cudaSuccess) return e;
         attr_set[dev & 63] = true;
     }
-    Params p;
+    Params p{};
     p.A = A;
     p.BH = BH;
     p.N = A.n;
@@ -1377,6 +1439,26 @@ extern "C" int splat_debug_trace(unsigned long long *out, int *counts)
     int z[6] = {0, 0, 0, 0, 0, 0};
     cudaMemcpyToSymbol(g_trace_n, z, sizeof(z));
     return 0;
+}
+
+cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int l, int nk, int R, float *lse,
+                                   const void *Q, const void *K, const void *V, int BH, int d, float scale, void *O,
+                                   cudaStream_t st, int *n_launch)
+{
+    *n_launch = 2;
+    if (d != 128) return cudaErrorNotSupported;
+    ResidueArgs r1;
+    r1.view = 1;
+    r1.R = R;
+    r1.nk = nk;
+    r1.l = l;
+    r1.lse = lse;
+    cudaError_t e = launch_d<128>(str, Q, K, V, BH, scale, O, st, r1);     // pass 1: strided keys, residue-major
+    if (e != cudaSuccess) return e;
+    ResidueArgs r2;
+    r2.merge = 1;
+    r2.lse = lse;
+    return launch_d<128>(band, Q, K, V, BH, scale, O, st, r2);           // pass 2: causal band + merge
 }
 
 cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, int d,

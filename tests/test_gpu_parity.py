@@ -159,7 +159,14 @@ SMALL_BF16 = [
     Config("strided_d64", Pattern("strided", 600, stride=7), 1, 2, 64, "bf16", 208),
     Config("blocked_d64", Pattern("blocked", 640, block=96), 2, 1, 64, "bf16", 209),
     Config("tiny_n", Pattern("window", 5, lo=1, hi=1), 1, 1, 64, "bf16", 210),
+    # STRIDED_LOCAL with N % l == 0 and N/l | 128: residue decomposition (strided pass on
+    # residue-major views + band pass with the merge), R = 2, 1, 4, 16 residues per tile
+    Config("st_res_nk64", Pattern("strided_local", 1024, stride=16, causal=1), 1, 3, 128, "bf16", 211),
+    Config("st_res_nk128", Pattern("strided_local", 2048, stride=16, causal=1), 1, 2, 128, "bf16", 212),
+    Config("st_res_nk32", Pattern("strided_local", 512, stride=16, causal=1), 2, 1, 128, "bf16", 213),
+    Config("st_res_nk8", Pattern("strided_local", 256, stride=32, causal=1), 1, 2, 128, "bf16", 214),
 ]
+RESIDUE = [c for c in SMALL_BF16 if c.name.startswith("st_res")]
 
 
 @pytest.mark.parametrize("cfg", SMALL_BF16, ids=lambda c: c.name)
@@ -180,7 +187,7 @@ def test_bf16_fused_and_unfused_small(cfg):
         assert maxabs(Pd[bh].float().cpu(), p) <= TOL_BF16
 
 
-@pytest.mark.parametrize("cfg", SMALL_BF16[:5], ids=lambda c: c.name)
+@pytest.mark.parametrize("cfg", SMALL_BF16[:5] + RESIDUE, ids=lambda c: c.name)
 def test_bf16_uniform_attention_pin(cfg):
     # Q = 0 -> p_ij = 1/nnz_i; V one-hot (V[j,t] = [t == j mod d]) -> O_i[t] = #{j: j = t mod d}/nnz_i
     N, d = cfg.N, cfg.d
@@ -200,9 +207,10 @@ def test_bf16_uniform_attention_pin(cfg):
     assert maxabs(Of[0, 0].float().cpu(), want) <= 4e-3
 
 
-def test_bf16_stress_large_scores():
-    # Q scaled by 8: score std ~2.7, exercises the online-softmax rescaling (SURVEY C-5)
-    cfg = SMALL_BF16[0]
+@pytest.mark.parametrize("cfg", [SMALL_BF16[0], RESIDUE[0]], ids=lambda c: c.name)
+def test_bf16_stress_large_scores(cfg):
+    # Q scaled by 8: score std ~2.7, exercises the online-softmax rescaling (SURVEY C-5) and, for
+    # the residue decomposition, the merge of two partial softmaxes with far-apart maxima
     q, k, v = make_qkv(cfg)
     q = (q.float() * 8).to(torch.bfloat16)
     a = S.Acsr(cfg.pattern, device=DEV)
