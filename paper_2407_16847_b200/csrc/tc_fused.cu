@@ -1225,6 +1225,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 int mid;
                 uint32_t bits;
                 tile_at(A, tr, j0, j, mid, bits);
+                bits = __shfl_sync(0xffffffffu, bits, 0);     // provably warp-uniform -> uniform branches
                 if (j + 1 < j1) pf = fetch_mask(A, tr, j0, j + 1, quad, r);
                 else SPLAT_NEXT_UNIT_PREFETCH();
                 const uint32_t mk[4] = {m4.x, m4.y, m4.z, m4.w};
