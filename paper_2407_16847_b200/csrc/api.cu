@@ -196,6 +196,17 @@ splat_status check_d(splat_dtype dt, int d)
 
 bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
+// residue decomposition available and not disabled (SPLAT_NO_RESIDUE_SPLIT=1: diagnostics, the
+// single-pass natural-order plan)
+bool use_residue_split(const splat_acsr_s *a)
+{
+    static const bool off = [] {
+        const char *v = getenv("SPLAT_NO_RESIDUE_SPLIT");
+        return v && atoi(v) != 0;
+    }();
+    return a->sub_band != nullptr && !off;
+}
+
 }  // namespace
 }  // namespace splat
 
@@ -437,11 +448,16 @@ splat_status splat_rsddmm(splat_acsr a, const void *Q, const void *K, splat_dtyp
     if (!Q || !K || !S) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
     if (!aligned16(Q) || !aligned16(K) || !aligned16(S)) return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
     DeviceGuard g(a->device);
-    cudaError_t e = dt == SPLAT_BF16
-                        ? launch_rsddmm_tc(dev_view(a), Q, K, B * H, d, scale, S, (cudaStream_t)stream)
-                        : launch_rsddmm_simt(dev_view(a), Q, K, false, B * H, d, scale, S, (cudaStream_t)stream);
+    int nl = 1;
+    cudaError_t e;
+    if (dt == SPLAT_BF16 && use_residue_split(a))
+        e = launch_unfused_residue(true, dev_view(a->sub_band), dev_view(a->sub_str), dev_view(a), a->rv_l, a->rv_nk,
+                                   a->rv_R, Q, K, B * H, d, scale, S, (cudaStream_t)stream, &nl);
+    else
+        e = dt == SPLAT_BF16 ? launch_rsddmm_tc(dev_view(a), Q, K, B * H, d, scale, S, (cudaStream_t)stream)
+                             : launch_rsddmm_simt(dev_view(a), Q, K, false, B * H, d, scale, S, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "splat_rsddmm launch");
-    note_launches(1);
+    note_launches(nl);
     return SPLAT_OK;
 }
 
@@ -469,10 +485,16 @@ splat_status splat_rspmm(splat_acsr a, const void *P, const void *V, splat_dtype
     if (!P || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
     if (!aligned16(P) || !aligned16(V) || !aligned16(O)) return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
     DeviceGuard g(a->device);
-    cudaError_t e = dt == SPLAT_BF16 ? launch_rspmm_tc(dev_view(a), P, V, B * H, d, O, (cudaStream_t)stream)
-                                     : launch_rspmm_simt(dev_view(a), P, V, false, B * H, d, O, (cudaStream_t)stream);
+    int nl = 1;
+    cudaError_t e;
+    if (dt == SPLAT_BF16 && use_residue_split(a))
+        e = launch_unfused_residue(false, dev_view(a->sub_band), dev_view(a->sub_str), dev_view(a), a->rv_l, a->rv_nk,
+                                   a->rv_R, P, V, B * H, d, 0.f, O, (cudaStream_t)stream, &nl);
+    else
+        e = dt == SPLAT_BF16 ? launch_rspmm_tc(dev_view(a), P, V, B * H, d, O, (cudaStream_t)stream)
+                             : launch_rspmm_simt(dev_view(a), P, V, false, B * H, d, O, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "splat_rspmm launch");
-    note_launches(1);
+    note_launches(nl);
     return SPLAT_OK;
 }
 
@@ -489,11 +511,7 @@ splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const
     DeviceGuard g(a->device);
     cudaError_t e;
     int nl = 1;
-    static const bool no_split = [] {
-        const char *v = getenv("SPLAT_NO_RESIDUE_SPLIT");     // diagnostics: the single-pass plan
-        return v && atoi(v) != 0;
-    }();
-    if (dt == SPLAT_BF16 && d == 128 && a->sub_band && !no_split) {
+    if (dt == SPLAT_BF16 && d == 128 && use_residue_split(a)) {
         // residue decomposition: handle-owned lse scratch, grown on the first call with this B*H
         const size_t need = (size_t)B * H * a->n;
         if (a->lse_cap < need) {

@@ -59,6 +59,11 @@ cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const
 cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int l, int nk, int R, float *lse,
                                    const void *Q, const void *K, const void *V, int BH, int d, float scale, void *O,
                                    cudaStream_t st, int *n_launch);
+// Unfused R-SDDMM (sddmm = true: X = Q, Y = K, out = S) or R-SpMM (X = P, Y = V, out = O) over the
+// residue decomposition: pass 1 on the strided sub-pattern (residue-major views), pass 2 on the band.
+cudaError_t launch_unfused_residue(bool sddmm, const DevAcsr &band, const DevAcsr &str, const DevAcsr &nat, int l,
+                                   int nk, int R, const void *X, const void *Y, int BH, int d, float scale, void *out,
+                                   cudaStream_t st, int *n_launch);
 cudaError_t launch_rsddmm_tc(const DevAcsr &A, const void *Q, const void *K, int BH, int d, float scale, float *S,
                              cudaStream_t st);
 cudaError_t launch_rspmm_tc(const DevAcsr &A, const void *P, const void *V, int BH, int d, void *O,

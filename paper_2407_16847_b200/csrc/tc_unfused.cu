@@ -49,7 +49,29 @@ struct ParamsU {
     float *S;                    // SDDMM output
     const __nv_bfloat16 *P;      // SpMM input (ACSR order)
     __nv_bfloat16 *O;            // SpMM output
+    // residue decomposition of STRIDED_LOCAL (splat_acsr_s::sub_band): A is a sub-handle, the
+    // S / P arrays are in the NATURAL handle's ACSR order.  pass 1: strided component on
+    // residue-major views (tile row r -> natural row (t R + r / nk) + l (r % nk)); its keys are
+    // the first i / l entries of the natural row.  pass 2: causal band in natural order, after
+    // the row's i / l stride entries; R-SpMM adds pass 1's O.
+    int pass, rv_l, rv_nk, rv_R;
+    const int64_t *nat_row_ptr;
+    long long nat_nnz;
 };
+
+// natural row of tile row r (pass 1: residue-major tile)
+__device__ __forceinline__ int nat_row(const ParamsU &prm, int t, int r)
+{
+    return prm.pass == 1 ? (t * prm.rv_R + r / prm.rv_nk) + prm.rv_l * (r % prm.rv_nk) : t * 128 + r;
+}
+
+// 3-D (natural) or 4-D (residue-major, pass 1) tile load of 128 rows starting at tile `tile`
+__device__ __forceinline__ void load_tile_rows(const ParamsU &prm, void *dst, const CUtensorMap *m, uint64_t *bar,
+                                               int c0, int tile, int bh)
+{
+    if (prm.pass == 1) tma_load_4d(dst, m, bar, c0, 0, tile * prm.rv_R, bh);
+    else tma_load_3d(dst, m, bar, c0, tile * 128, bh);
+}
 
 __device__ __forceinline__ void unit_tile(const DevAcsr &A, int u, int &bh, int &t)
 {
@@ -91,6 +113,19 @@ __device__ __forceinline__ void row_info(const DevAcsr &A, int row, long long &b
         for (int q = 0; q < 4; ++q)
             if (q < ns) R.g[q] = A.seg[(size_t)row * 4 + q];
     }
+}
+
+// (b,h) element offset of tile row r's ACSR row in S / P, and the runs of the row in A's pattern
+// (residue passes: the runs of the sub-pattern row, the base of the natural row)
+__device__ __forceinline__ long long row_offset(const ParamsU &prm, int bh, int t, int r, RowRuns &R)
+{
+    const DevAcsr &A = prm.A;
+    long long base;
+    row_info(A, t * 128 + r, base, R);
+    if (prm.pass == 0) return (long long)bh * A.nnz + base;
+    const int i = nat_row(prm, t, r);
+    if (i >= A.n) return 0;
+    return (long long)bh * prm.nat_nnz + prm.nat_row_ptr[i] + (prm.pass == 2 ? i / prm.rv_l : 0);
 }
 
 // ============================================================================ R-SDDMM
@@ -151,7 +186,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 mbar_expect_tx(&q_full[qi], C::kTileBytes);
 #pragma unroll
                 for (int c = 0; c < C::kChunks; ++c)
-                    tma_load_3d(smem + C::OFF_Q + qi * C::kTileBytes + c * kSub, &tmQ, &q_full[qi], 64 * c, t * 128, bh);
+                    load_tile_rows(prm, smem + C::OFF_Q + qi * C::kTileBytes + c * kSub, &tmQ, &q_full[qi], 64 * c, t, bh);
             }
             ++qc;
             if (++qi == C::QS) { qi = 0; qph ^= 1; }
@@ -162,8 +197,8 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     mbar_expect_tx(&k_full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
-                        tma_load_3d(smem + C::OFF_K + ki * C::kTileBytes + c * kSub, &tmK, &k_full[ki], 64 * c,
-                                    kv * 128, bh);
+                        load_tile_rows(prm, smem + C::OFF_K + ki * C::kTileBytes + c * kSub, &tmK, &k_full[ki], 64 * c,
+                                       kv, bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -226,10 +261,8 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             i += (uint32_t)(e1 - e0);
             if (e >= e1) continue;
             const int row = t * 128 + r;
-            long long base;
             RowRuns R;
-            row_info(A, row, base, R);
-            const long long rowoff = (long long)bh * A.nnz + base;
+            const long long rowoff = row_offset(prm, bh, t, r, R);
             for (; e < e1; e += kNWG) {
                 const int ent = A.kv[e];
                 const int c0 = (ent & kKvMask) * 128;
@@ -339,8 +372,8 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     mbar_expect_tx(&v_full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
-                        tma_load_3d(smem + C::OFF_V + ki * C::kTileBytes + c * kSub, &tmV, &v_full[ki], 64 * c,
-                                    kv * 128, bh);
+                        load_tile_rows(prm, smem + C::OFF_V + ki * C::kTileBytes + c * kSub, &tmV, &v_full[ki], 64 * c,
+                                       kv, bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -386,7 +419,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
         uint8_t *ptile = smem + C::OFF_P + eg * 2 * kSub;
         const uint32_t below = (1u << lane) - 1u;
         const unsigned short *Pg = reinterpret_cast<const unsigned short *>(prm.P);
-        const long long total = (long long)prm.BH * A.nnz;   // elements of P
+        const long long total = (long long)prm.BH * (prm.pass ? prm.nat_nnz : A.nnz);   // elements of P
         uint32_t i = 0, k = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
@@ -397,10 +430,8 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             const int row = t * 128 + r;
             if (e < e1) {
                 const int nrows = min(32, A.n - (t * 128 + quad * 32));
-                long long base;
                 RowRuns R;
-                row_info(A, row, base, R);
-                const long long rowoff = (long long)bh * A.nnz + base;
+                const long long rowoff = row_offset(prm, bh, t, r, R);
                 for (; e < e1; e += kNWGP) {
                     const int ent = A.kv[e];
                     const int c0 = (ent & kKvMask) * 128;
@@ -497,7 +528,8 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                 mbar_wait(&o_full[ob], (uo >> 1) & 1);
                 tc_fence_after();
                 const bool empty = e0 == e1;   // no key tile: O = 0
-                __nv_bfloat16 *orow = prm.O + ((size_t)bh * A.n + row) * D;
+                const int nrow = nat_row(prm, t, r);
+                __nv_bfloat16 *orow = prm.O + ((size_t)bh * A.n + nrow) * D;
 #pragma unroll
                 for (int c = 0; c < D / 32; ++c) {
                     float o[32];
@@ -506,6 +538,19 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     if (empty) {
 #pragma unroll
                         for (int x = 0; x < 32; ++x) o[x] = 0.f;
+                    }
+                    if (prm.pass == 2 && row < A.n) {
+                        // O = O_band + O_strided (pass 1 wrote the strided part to this row)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            const uint4 w4 = *reinterpret_cast<const uint4 *>(orow + c * 32 + 8 * v);
+                            const uint32_t ww[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                o[8 * v + 2 * q] += __uint_as_float(ww[q] << 16);
+                                o[8 * v + 2 * q + 1] += __uint_as_float(ww[q] & 0xffff0000u);
+                            }
+                        }
                     }
                     if (row < A.n) {
 #pragma unroll
@@ -573,7 +618,101 @@ cudaError_t launch_spmm_d(const DevAcsr &A, const void *P, const void *V, int BH
     return cudaGetLastError();
 }
 
+struct UPass {
+    int pass = 0, l = 0, nk = 0, R = 0;
+    const int64_t *nat_row_ptr = nullptr;
+    long long nat_nnz = 0;
+};
+
+void apply_pass(ParamsU &p, const UPass &ps)
+{
+    p.pass = ps.pass;
+    p.rv_l = ps.l;
+    p.rv_nk = ps.nk;
+    p.rv_R = ps.R;
+    p.nat_row_ptr = ps.nat_row_ptr;
+    p.nat_nnz = ps.nat_nnz;
+}
+
+bool maps_for(CUtensorMap *m, const void *X, int BH, int N, int D, const UPass &ps)
+{
+    return ps.pass == 1 ? make_map_residue(m, X, BH, N, D, ps.l, ps.nk, ps.R) : make_map(m, X, BH, N, D);
+}
+
+template <int D>
+cudaError_t launch_sddmm_pass(const DevAcsr &A, const UPass &ps, const void *Q, const void *K, int BH, float scale,
+                              float *S, cudaStream_t st)
+{
+    CUtensorMap mq, mk;
+    if (!maps_for(&mq, Q, BH, A.n, D, ps) || !maps_for(&mk, K, BH, A.n, D, ps)) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(rsddmm_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgS<D>::SMEM);
+    if (e != cudaSuccess) return e;
+    ParamsU p{};
+    p.A = A;
+    p.BH = BH;
+    p.scale = scale;
+    p.S = S;
+    apply_pass(p, ps);
+    rsddmm_tc_kernel<D><<<grid_for((long long)A.n_qt * BH), kThreadsU, CfgS<D>::SMEM, st>>>(mq, mk, p);
+    return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_spmm_pass(const DevAcsr &A, const UPass &ps, const void *P, const void *V, int BH, void *O,
+                             cudaStream_t st)
+{
+    CUtensorMap mv;
+    if (!maps_for(&mv, V, BH, A.n, D, ps)) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(rspmm_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, CfgP<D>::SMEM);
+    if (e != cudaSuccess) return e;
+    ParamsU p{};
+    p.A = A;
+    p.BH = BH;
+    p.P = reinterpret_cast<const __nv_bfloat16 *>(P);
+    p.O = reinterpret_cast<__nv_bfloat16 *>(O);
+    apply_pass(p, ps);
+    rspmm_tc_kernel<D><<<grid_for((long long)A.n_qt * BH), kThreadsP, CfgP<D>::SMEM, st>>>(mv, p);
+    return cudaGetLastError();
+}
+
 }  // namespace
+
+cudaError_t launch_unfused_residue(bool sddmm, const DevAcsr &band, const DevAcsr &str, const DevAcsr &nat, int l,
+                                   int nk, int R, const void *X, const void *Y, int BH, int d, float scale, void *out,
+                                   cudaStream_t st, int *n_launch)
+{
+    *n_launch = 2;
+    UPass p1, p2;
+    p1.pass = 1;
+    p2.pass = 2;
+    p1.l = p2.l = l;
+    p1.nk = p2.nk = nk;
+    p1.R = p2.R = R;
+    p1.nat_row_ptr = p2.nat_row_ptr = nat.row_ptr;
+    p1.nat_nnz = p2.nat_nnz = nat.nnz;
+    cudaError_t e;
+    if (sddmm) {
+        float *S = reinterpret_cast<float *>(out);
+        if (d == 64) {
+            if ((e = launch_sddmm_pass<64>(str, p1, X, Y, BH, scale, S, st)) != cudaSuccess) return e;
+            return launch_sddmm_pass<64>(band, p2, X, Y, BH, scale, S, st);
+        }
+        if (d == 128) {
+            if ((e = launch_sddmm_pass<128>(str, p1, X, Y, BH, scale, S, st)) != cudaSuccess) return e;
+            return launch_sddmm_pass<128>(band, p2, X, Y, BH, scale, S, st);
+        }
+    } else {
+        if (d == 64) {
+            if ((e = launch_spmm_pass<64>(str, p1, X, Y, BH, out, st)) != cudaSuccess) return e;
+            return launch_spmm_pass<64>(band, p2, X, Y, BH, out, st);
+        }
+        if (d == 128) {
+            if ((e = launch_spmm_pass<128>(str, p1, X, Y, BH, out, st)) != cudaSuccess) return e;
+            return launch_spmm_pass<128>(band, p2, X, Y, BH, out, st);
+        }
+    }
+    return cudaErrorNotSupported;
+}
 
 cudaError_t launch_rsddmm_tc(const DevAcsr &A, const void *Q, const void *K, int BH, int d, float scale, float *S,
                              cudaStream_t st)

@@ -165,6 +165,8 @@ SMALL_BF16 = [
     Config("st_res_nk128", Pattern("strided_local", 2048, stride=16, causal=1), 1, 2, 128, "bf16", 212),
     Config("st_res_nk32", Pattern("strided_local", 512, stride=16, causal=1), 2, 1, 128, "bf16", 213),
     Config("st_res_nk8", Pattern("strided_local", 256, stride=32, causal=1), 1, 2, 128, "bf16", 214),
+    # d = 64: the fused kernel keeps the natural plan, the unfused primitives split
+    Config("st_res_d64", Pattern("strided_local", 1024, stride=16, causal=1), 1, 2, 64, "bf16", 215),
 ]
 RESIDUE = [c for c in SMALL_BF16 if c.name.startswith("st_res")]
 
