@@ -73,6 +73,30 @@ rsddmm_simt_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K, 
     }
 }
 
+// 4 consecutive P values from 4 probabilities: one 8-byte (bf16) or 16-byte (fp32) store
+__device__ __forceinline__ void store4(__nv_bfloat16 *p, float a, float b, float c, float d)
+{
+    uint2 w;
+    w.x = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) | ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
+    w.y = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(c)) | ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(d)) << 16);
+    *reinterpret_cast<uint2 *>(p) = w;
+}
+__device__ __forceinline__ void store4(float *p, float a, float b, float c, float d)
+{
+    *reinterpret_cast<float4 *>(p) = make_float4(a, b, c, d);
+}
+
+__device__ __forceinline__ float ex2f(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Row softmax over the ACSR row (the softmax of each input row of the ACSR, which
+// stores only the non-zeros; reading R-1).  Warp per row, three streaming passes over the row --
+// max, sum of exp, write -- with 16-byte loads of S on the aligned body of the row (the second and
+// third reads hit L2); exp(x - m) = 2^((x - m) log2 e) on MUFU.EX2.
 template <typename TP>
 __global__ void __launch_bounds__(kWarps * 32)
 softmax_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P)
@@ -80,26 +104,74 @@ softmax_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P)
     const RowId r = row_of_warp(A.n);
     const int lane = threadIdx.x & 31;
     if (r.i >= A.n) return;
-    const long long b = A.row_ptr[r.i], len = A.row_ptr[r.i + 1] - b;
+    const long long b = A.row_ptr[r.i];
+    const int len = (int)(A.row_ptr[r.i + 1] - b);
     if (len <= 0) return;
-    const float *s = S + (size_t)r.bh * A.nnz + b;
-    TP *p = P + (size_t)r.bh * A.nnz + b;
+    const long long e0 = (long long)r.bh * A.nnz + b;       // element index of the row start
+    const float *s = S + e0;
+    TP *p = P + e0;
+    const int head = min(len, (int)((4 - (e0 & 3)) & 3));  // elements before the first 16-byte boundary
+    const int nv = (len - head) >> 2;                        // aligned float4 groups
+    const int tail0 = head + 4 * nv;
+    const float4 *s4 = reinterpret_cast<const float4 *>(s + head);
+    constexpr float L2E = 1.4426950408889634f;
     float m = -INFINITY, l = 0.f;
-    for (long long x = lane; x < len; x += 32) {
-        const float v = s[x];
-        const float mn = fmaxf(m, v);
-        l = l * expf(m - mn) + expf(v - mn);
-        m = mn;
-    }
+    if (len > 2048) {
+        // long rows (their re-reads would miss L2): one online pass for max and sum
+        // (the sum is rescaled when the running max grows), then the write pass
+        auto add = [&](float vmax, float s0) {   // s0 = sum of 2^((v - vmax) log2 e) of the group
+            const float mn = fmaxf(m, vmax);
+            l = l * ex2f((m - mn) * L2E) + s0 * ex2f((vmax - mn) * L2E);
+            m = mn;
+        };
+        if (lane < head) add(s[lane], 1.f);
+#pragma unroll 4
+        for (int q = lane; q < nv; q += 32) {
+            const float4 v = s4[q];
+            const float vm = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)), vmL = vm * L2E;
+            add(vm, (ex2f(fmaf(v.x, L2E, -vmL)) + ex2f(fmaf(v.y, L2E, -vmL))) +
+                        (ex2f(fmaf(v.z, L2E, -vmL)) + ex2f(fmaf(v.w, L2E, -vmL))));
+        }
+        for (int x = tail0 + lane; x < len; x += 32) add(s[x], 1.f);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), l2 = __shfl_xor_sync(0xffffffffu, l, o);
-        const float mn = fmaxf(m, m2);
-        l = (m == -INFINITY ? 0.f : l * expf(m - mn)) + (m2 == -INFINITY ? 0.f : l2 * expf(m2 - mn));
-        m = mn;
+        for (int o = 16; o > 0; o >>= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, m, o), l2 = __shfl_xor_sync(0xffffffffu, l, o);
+            const float mn = fmaxf(m, m2);
+            l = (m == -INFINITY ? 0.f : l * ex2f((m - mn) * L2E)) + (m2 == -INFINITY ? 0.f : l2 * ex2f((m2 - mn) * L2E));
+            m = mn;
+        }
+    } else {
+        if (lane < head) m = s[lane];
+#pragma unroll 4
+        for (int q = lane; q < nv; q += 32) {
+            const float4 v = s4[q];
+            m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        }
+        for (int x = tail0 + lane; x < len; x += 32) m = fmaxf(m, s[x]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const float mL0 = m * L2E;
+        if (lane < head) l = ex2f(fmaf(s[lane], L2E, -mL0));
+#pragma unroll 4
+        for (int q = lane; q < nv; q += 32) {
+            const float4 v = s4[q];
+            l += (ex2f(fmaf(v.x, L2E, -mL0)) + ex2f(fmaf(v.y, L2E, -mL0))) + (ex2f(fmaf(v.z, L2E, -mL0)) + ex2f(fmaf(v.w, L2E, -mL0)));
+        }
+        for (int x = tail0 + lane; x < len; x += 32) l += ex2f(fmaf(s[x], L2E, -mL0));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
     }
+    const float mL = m * L2E;
     const float inv = 1.f / l;
-    for (long long x = lane; x < len; x += 32) p[x] = from_f<TP>(expf(s[x] - m) * inv);
+    if (lane < head) p[lane] = from_f<TP>(ex2f(fmaf(s[lane], L2E, -mL)) * inv);
+    TP *p4 = p + head;
+#pragma unroll 4
+    for (int q = lane; q < nv; q += 32) {
+        const float4 v = s4[q];
+        store4(p4 + 4 * q, ex2f(fmaf(v.x, L2E, -mL)) * inv, ex2f(fmaf(v.y, L2E, -mL)) * inv,
+               ex2f(fmaf(v.z, L2E, -mL)) * inv, ex2f(fmaf(v.w, L2E, -mL)) * inv);
+    }
+    for (int x = tail0 + lane; x < len; x += 32) p[x] = from_f<TP>(ex2f(fmaf(s[x], L2E, -mL)) * inv);
 }
 
 template <typename T>
