@@ -59,6 +59,14 @@ struct ParamsU {
     long long nat_nnz;
 };
 
+// predicated 4-byte global store (no branch / reconvergence per element)
+__device__ __forceinline__ void st_pred_f32(float *addr, float v, uint32_t pred)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.global.f32 [%0], %1;\n\t}" ::"l"(addr), "f"(v),
+                 "r"(pred)
+                 : "memory");
+}
+
 // natural row of tile row r (pass 1: residue-major tile)
 __device__ __forceinline__ int nat_row(const ParamsU &prm, int t, int r)
 {
@@ -137,9 +145,11 @@ struct CfgS {
     static constexpr int KS = D == 64 ? 4 : 3;
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + QS * kTileBytes;
-    static constexpr int OFF_TOFF = OFF_K + KS * kTileBytes;                 // [kNWG][2][128] int64
-    static constexpr int OFF_TMASK = OFF_TOFF + kNWG * 2 * 128 * 8;         // [kNWG][2][128] uint4
-    static constexpr int OFF_BAR = OFF_TMASK + kNWG * 2 * 128 * 16;
+    // per (epilogue group, buffer, query row, key quad): {offset of the quad's first non-zero
+    // relative to the tile base, row mask word of the quad} -- one LDS.64 per stored row
+    static constexpr int OFF_TQ = OFF_K + KS * kTileBytes;                   // [kNWG][2][128][4] int2
+    static constexpr int OFF_TBASE = OFF_TQ + kNWG * 2 * 128 * 4 * 8;       // [kNWG][2] int64
+    static constexpr int OFF_BAR = OFF_TBASE + kNWG * 2 * 8;
     static constexpr int NBAR = 2 * QS + 2 * KS + 2 * kNWG;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
     static_assert(SMEM <= 232448, "shared memory budget");
@@ -245,10 +255,9 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         // (TMEM lanes = key columns 32 quad .. 32 quad + 31) stores every query row's values.
         const int eg = (warp - 2) >> 2, quad = warp & 3, r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        long long *toff = reinterpret_cast<long long *>(smem + C::OFF_TOFF) + eg * 256;
-        uint4 *tmask = reinterpret_cast<uint4 *>(smem + C::OFF_TMASK) + eg * 256;
+        int2 *tq = reinterpret_cast<int2 *>(smem + C::OFF_TQ) + eg * 2 * 128 * 4;
+        long long *tbase = reinterpret_cast<long long *>(smem + C::OFF_TBASE) + eg * 2;
         const uint32_t below = (1u << lane) - 1u;
-        const int col = 32 * quad + lane;
         float *const Sg = prm.S;
         const float scale = prm.scale;
         uint32_t i = 0, k = 0;   // i: CTA tile counter, k: this group's tile counter
@@ -267,14 +276,29 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 const int ent = A.kv[e];
                 const int c0 = (ent & kKvMask) * 128;
                 const bool partial = (ent & kPartialBit) != 0;
-                const int tb = (k & 1) * 128;
+                const int tb = k & 1;
                 uint4 m4 = make_uint4(~0u, ~0u, ~0u, ~0u);
                 if (partial) m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
-                toff[tb + r] = row < A.n ? rowoff + rank_before(R, c0) : -1ll;
-                tmask[tb + r] = m4;
+                if (row >= A.n) m4 = make_uint4(0u, 0u, 0u, 0u);
+                // Thread r publishes, per key quad q, the offset of row r's first non-zero in the
+                // quad's 32 columns (relative to the tile base = row 0's first non-zero; a tile
+                // spans < 2^31 entries) and the row mask word: one LDS.64 per stored row.
+                const long long o0 = row < A.n ? rowoff + rank_before(R, c0) : 0ll;
+                if (r == 0) tbase[tb] = o0;
+                const long long t0 = __shfl_sync(0xffffffffu, o0, 0);     // valid in warp 0 only
+                int2 *dst = tq + (tb * 128 + r) * 4;
+                const int p1 = __popc(m4.x), p2 = p1 + __popc(m4.y), p3 = p2 + __popc(m4.z);
+                (void)t0;
+                wg_sync(1 + eg);          // tbase of this buffer published (row 0 lives in warp quad 0)
+                const int rel = (int)(o0 - tbase[tb]);
+                dst[0] = make_int2(rel, (int)m4.x);
+                dst[1] = make_int2(rel + p1, (int)m4.y);
+                dst[2] = make_int2(rel + p2, (int)m4.z);
+                dst[3] = make_int2(rel + p3, (int)m4.w);
                 wg_sync(1 + eg);
                 mbar_wait(&s_full[eg], k & 1);
                 tc_fence_after();
+                float *const base = Sg + tbase[tb];
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     float v[32];
@@ -285,22 +309,11 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&s_empty[eg]);
                     }
-                    if (!partial) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const long long o = toff[tb + 32 * c + j];
-                            if (o >= 0) Sg[o + col] = scale * v[j];
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const long long o = toff[tb + 32 * c + j];
-                            const uint4 mm = tmask[tb + 32 * c + j];
-                            const uint32_t mw = quad == 0 ? mm.x : quad == 1 ? mm.y : quad == 2 ? mm.z : mm.w;
-                            const int pre = (quad > 0 ? __popc(mm.x) : 0) + (quad > 1 ? __popc(mm.y) : 0) +
-                                            (quad > 2 ? __popc(mm.z) : 0);
-                            if (o >= 0 && ((mw >> lane) & 1u)) Sg[o + pre + __popc(mw & below)] = scale * v[j];
-                        }
+                    for (int j = 0; j < 32; ++j) {
+                        const int2 q = tq[(tb * 128 + 32 * c + j) * 4 + quad];
+                        const uint32_t mw = (uint32_t)q.y;
+                        st_pred_f32(base + q.x + __popc(mw & below), scale * v[j], (mw >> lane) & 1u);
                     }
                 }
                 ++k;
