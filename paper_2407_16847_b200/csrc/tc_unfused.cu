@@ -36,10 +36,13 @@ using namespace sm100;
 #endif
 constexpr int kNWG = SPLAT_UNF_NWG;               // epilogue / gather warpgroups
 constexpr int kThreadsU = 64 + 128 * kNWG;        // warp 0 TMA, warp 1 MMA, then the warpgroups
+#ifndef SPLAT_UNF_RB
+#define SPLAT_UNF_RB 4
+#endif
 constexpr int kNWGP = 3;                          // SpMM gather warpgroups (+ 1 epilogue warpgroup)
 constexpr int kThreadsP = 64 + 128 + 128 * kNWGP;
 constexpr int kSub = 128 * 128;                   // [128 rows x 64 bf16] swizzle-128B sub-tile (16 KB)
-constexpr int kRB = 4;                            // SpMM gather, PARTIAL tiles: rows per load batch
+constexpr int kRB = SPLAT_UNF_RB;                 // SpMM gather, PARTIAL tiles: rows per load batch
 constexpr int kRF = 8;                            // SpMM gather, FULL tiles: rows per load batch
 
 struct ParamsU {
