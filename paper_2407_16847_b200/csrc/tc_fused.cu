@@ -394,7 +394,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         // warp 0: Q_A, Q_B of every unit and K_e of every union entry; warp 3: V_e.  K and V rings
         // advance independently: a K stage frees when both groups' S = Q K^T have completed, a V
         // stage only after both PVs, so K can run up to KS entries ahead of the softmax.
-        if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
         const bool kq = warp == 0;
         int qi[2] = {0, 0}, qc[2] = {0, 0};
         uint32_t qph[2] = {0, 0};
@@ -465,7 +465,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         // descriptors live in uniform registers; lane 0 issues.  K/V stages are released when
         // both groups are done with them (empty barriers count two arrivals; a group that skips
         // an entry arrives once the entry is resident).
-        if constexpr (SEP) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
         // uniform values (see elect_one): descriptors stay in uniform registers
         const int g = __shfl_sync(0xffffffffu, warp - 1, 0);
         const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
@@ -588,7 +588,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         // Each group walks only its own query tile's plan entries (qt_ptr range in pair_info);
         // the fast-index mask of the next entry is prefetched one entry ahead (across unit
         // boundaries too) so its L2 latency never sits on the critical path.
-        if constexpr (SEP) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
         const int g = (warp - 4) >> 2;          // tile group: 0 = A, 1 = B
         const int quad = warp & 3;              // TMEM lane quadrant of this warp
         const int r = quad * 32 + lane;         // row within the query tile
@@ -713,44 +713,27 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 tc_fence_after();
                 if (store_leader) TRACE(2 + g, 2);
                 float mx = -INFINITY;
-                float sv[SEP ? 128 : 1];
-                if constexpr (SEP) {
-                    // the whole S row -> registers in two halves (the second half's load overlaps
-                    // the first half's mask + max), then S goes back to the MMA warp
-                    tmem_ld32(s_tm, sv);
-                    tmem_ld32(s_tm + 32, sv + 32);
-                    tmem_wait_ld();
-                    tmem_ld32(s_tm + 64, sv + 64);
-                    tmem_ld32(s_tm + 96, sv + 96);
+                float sv[128];
+                // the whole S row -> registers in two halves (the second half's load overlaps the
+                // first half's mask + max); SEP: then S goes back to the MMA warp
+                tmem_ld32(s_tm, sv);
+                tmem_ld32(s_tm + 32, sv + 32);
+                tmem_wait_ld();
+                tmem_ld32(s_tm + 64, sv + 64);
+                tmem_ld32(s_tm + 96, sv + 96);
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        if (w == 2) {
-                            tmem_wait_ld();
+                for (int w = 0; w < 4; ++w) {
+                    if (w == 2) {
+                        tmem_wait_ld();
+                        if constexpr (SEP) {
                             tc_fence_before();
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&s_empty[g]);
                         }
-                        if (live & (1u << w)) {
-                            if (need & (1u << w)) apply_mask(sv + 32 * w, mk[w]);
-                            mx = fmax3(mx, max32(sv + 32 * w), -INFINITY);
-                        }
                     }
-                } else {
-                    // pass 1 of 2 (d = 128 keeps no S row in registers): row max over the live chunks
-#pragma unroll
-                    for (int w2 = 0; w2 < 2; ++w2) {
-                        float v[2][32];
-                        tmem_ld32(s_tm + 64 * w2, v[0]);
-                        tmem_ld32(s_tm + 64 * w2 + 32, v[1]);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int q = 0; q < 2; ++q) {
-                            const int w = 2 * w2 + q;
-                            if (live & (1u << w)) {
-                                if (need & (1u << w)) apply_mask(v[q], mk[w]);
-                                mx = fmax3(mx, max32(v[q]), -INFINITY);
-                            }
-                        }
+                    if (live & (1u << w)) {
+                        if (need & (1u << w)) apply_mask(sv + 32 * w, mk[w]);
+                        mx = fmax3(mx, max32(sv + 32 * w), -INFINITY);
                     }
                 }
                 if (store_leader) TRACE(2 + g, 12);
@@ -769,20 +752,21 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
                 uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
                 if (prm.dbg & 2) live = 0;
-                if constexpr (SEP) {
-                    // exponentials first (registers), so the previous PV has long finished when
-                    // O is rescaled and P rewritten
-                    uint32_t pw[64];
+                // exponentials first (registers): SEP -- the previous PV has long finished when O is
+                // rescaled and P rewritten; non-SEP -- P overwrites S's columns (all of S is in
+                // registers already) and S(j) was computed after PV(j-1), so O is final here
+                uint32_t pw[64];
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        if (live & (1u << w)) {
-                            exp32(sv + 32 * w, cc, mm, acc0, acc1, pw + 16 * w);
-                        } else {
+                for (int w = 0; w < 4; ++w) {
+                    if (live & (1u << w)) {
+                        exp32(sv + 32 * w, cc, mm, acc0, acc1, pw + 16 * w);
+                    } else {
 #pragma unroll
-                            for (int x = 0; x < 16; ++x) pw[16 * w + x] = 0u;
-                        }
+                        for (int x = 0; x < 16; ++x) pw[16 * w + x] = 0u;
                     }
-                    if (store_leader) TRACE(2 + g, 13);
+                }
+                if (store_leader) TRACE(2 + g, 13);
+                if constexpr (SEP) {
                     if (pe_on) {             // the previous unit's epilogue (first tile of a unit only)
                         epilogue(pe_l, pe_m, pe_t, pe_bh);
                         pe_on = false;
@@ -792,55 +776,21 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         mbar_wait(&pv_done[g], (s_cnt - 2) & 1);
                         tc_fence_after();
                     }
-                    if (store_leader) TRACE(2 + g, 14);
-                    if (!first && __any_sync(0xffffffffu, resc)) {
+                }
+                if (store_leader) TRACE(2 + g, 14);
+                if (!first && __any_sync(0xffffffffu, resc)) {
 #pragma unroll
-                        for (int c = 0; c < D / 32; ++c) {
-                            float o[32];
-                            tmem_ld32(o_tm + c * 32, o);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int x = 0; x < 32; ++x) o[x] *= alpha;
-                            tmem_st32(o_tm + c * 32, o);
-                        }
-                    }
-                    tmem_st32(p_tm, reinterpret_cast<const float *>(pw));
-                    tmem_st32(p_tm + 32, reinterpret_cast<const float *>(pw + 32));
-                } else {
-                    if (!first && __any_sync(0xffffffffu, resc)) {
-                        // O holds every earlier PV of this tile: S_g(j) was computed after PV_g(j-1)
-#pragma unroll
-                        for (int c = 0; c < D / 32; ++c) {
-                            float o[32];
-                            tmem_ld32(o_tm + c * 32, o);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int x = 0; x < 32; ++x) o[x] *= alpha;
-                            tmem_st32(o_tm + c * 32, o);
-                        }
-                    }
-                    // pass 2: chunks 2h, 2h+1 are read before P columns [32h, 32h+32) overwrite them
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        uint32_t pw[32];
-                        float v[2][32];
-                        tmem_ld32(s_tm + 64 * h, v[0]);
-                        tmem_ld32(s_tm + 64 * h + 32, v[1]);
+                    for (int c = 0; c < D / 32; ++c) {
+                        float o[32];
+                        tmem_ld32(o_tm + c * 32, o);
                         tmem_wait_ld();
 #pragma unroll
-                        for (int q = 0; q < 2; ++q) {
-                            const int w = 2 * h + q;
-                            if (live & (1u << w)) {
-                                if (need & (1u << w)) apply_mask(v[q], mk[w]);
-                                exp32(v[q], cc, mm, acc0, acc1, pw + 16 * q);
-                            } else {
-#pragma unroll
-                                for (int x = 0; x < 16; ++x) pw[16 * q + x] = 0u;
-                            }
-                        }
-                        tmem_st32(p_tm + 32 * h, reinterpret_cast<const float *>(pw));
+                        for (int x = 0; x < 32; ++x) o[x] *= alpha;
+                        tmem_st32(o_tm + c * 32, o);
                     }
                 }
+                tmem_st32(p_tm, reinterpret_cast<const float *>(pw));
+                tmem_st32(p_tm + 32, reinterpret_cast<const float *>(pw + 32));
                 {
                     float a, b, c, d;
                     unpack2(acc0, a, b);
