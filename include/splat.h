@@ -227,9 +227,13 @@ splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const
  * end-to-end path a user without device-resident tensors takes):
  * cudaMemcpyAsync of Qh, Kh, Vh into the caller-owned device staging
  * buffers dQ, dK, dV, splat_sparse_mhsa into dO, cudaMemcpyAsync of dO into
- * Oh -- all enqueued on `stream`, asynchronous (synchronise the stream
- * before reading Oh).  Host buffers should be page-locked for the copies to
- * be asynchronous.  Shapes, dtypes and errors as splat_sparse_mhsa.
+ * Oh.  The (b, h) slices are pipelined in chunks over three handle-owned
+ * streams (host->device copy of chunk c+1 and device->host copy of chunk c-1
+ * overlap the kernel on chunk c; (b, h) slices are independent, Eq. 1 per
+ * head); `stream` waits for all of it, so the call is asynchronous
+ * with respect to the host exactly as before (synchronise `stream` before
+ * reading Oh).  Host buffers should be page-locked for the copies to be
+ * asynchronous.  Shapes, dtypes and errors as splat_sparse_mhsa.
  * ------------------------------------------------------------------------- */
 splat_status splat_sparse_mhsa_host(splat_acsr a, const void *Qh, const void *Kh, const void *Vh,
                                     splat_dtype dt, int32_t B, int32_t H, int32_t d, float scale,

@@ -114,6 +114,11 @@ void free_device(splat_acsr_s *a)
     a->sub_band = a->sub_str = nullptr;
     cudaFree(a->d_lse);
     a->d_lse = nullptr;
+    for (int i = 0; i < 3; ++i)
+        if (a->hs[i]) cudaStreamDestroy((cudaStream_t)a->hs[i]);
+    for (int i = 0; i < 2; ++i)
+        for (int c = 0; c < 16; ++c)
+            if (a->hev[i][c]) cudaEventDestroy((cudaEvent_t)a->hev[i][c]);
     cudaFree(a->d_seg);
     cudaFree(a->d_nseg);
     cudaFree(a->d_row_ptr);
@@ -540,17 +545,58 @@ splat_status splat_sparse_mhsa_host(splat_acsr a, const void *Qh, const void *Kh
     if (st == SPLAT_OK) st = check_d(dt, d);
     if (st != SPLAT_OK) return st;
     if (!Qh || !Kh || !Vh || !Oh) return set_error(SPLAT_ERR_INVALID_ARG, "null host pointer");
-    const size_t bytes = (size_t)B * H * a->n * d * (dt == SPLAT_BF16 ? 2 : 4);
+    if (!dQ || !dK || !dV || !dO) return set_error(SPLAT_ERR_INVALID_ARG, "null device pointer");
+    const int BH = B * H;
+    const size_t slice = (size_t)a->n * d * (dt == SPLAT_BF16 ? 2 : 4);    // bytes per (b, h)
     DeviceGuard g(a->device);
     cudaStream_t cs = (cudaStream_t)stream;
-    cudaError_t e = cudaMemcpyAsync(dQ, Qh, bytes, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dK, Kh, bytes, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dV, Vh, bytes, cudaMemcpyHostToDevice, cs);
-    if (e != cudaSuccess) return cuda_fail(e, "host->device copy");
-    st = splat_sparse_mhsa(a, dQ, dK, dV, dt, B, H, d, scale, dO, stream);
-    if (st != SPLAT_OK) return st;
-    e = cudaMemcpyAsync(Oh, dO, bytes, cudaMemcpyDeviceToHost, cs);
-    if (e != cudaSuccess) return cuda_fail(e, "device->host copy");
+    cudaError_t e = cudaSuccess;
+    // handle-owned pipeline streams / events, created on first use
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+        if (!a->hs[i]) e = cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t *>(&a->hs[i]), cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+        for (int c = 0; c < 16 && e == cudaSuccess; ++c)
+            if (!a->hev[i][c]) e = cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t *>(&a->hev[i][c]), cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "pipeline streams");
+    cudaStream_t s_in = (cudaStream_t)a->hs[0], s_k = (cudaStream_t)a->hs[1], s_out = (cudaStream_t)a->hs[2];
+    // chunks of (b, h) slices: enough to overlap, each still filling the GPU
+    const int nch = BH >= 8 ? 8 : BH;
+    cudaEvent_t start = (cudaEvent_t)a->hev[0][15], done_k[8], done_in[8];
+    for (int c = 0; c < nch; ++c) {
+        done_in[c] = (cudaEvent_t)a->hev[0][c];
+        done_k[c] = (cudaEvent_t)a->hev[1][c];
+    }
+    // everything the caller enqueued on `stream` before this call happens first
+    if ((e = cudaEventRecord(start, cs)) != cudaSuccess) return cuda_fail(e, "event");
+    cudaStreamWaitEvent(s_in, start, 0);
+    cudaStreamWaitEvent(s_k, start, 0);
+    cudaStreamWaitEvent(s_out, start, 0);
+    int nl = 0;
+    for (int c = 0; c < nch && e == cudaSuccess; ++c) {
+        const int b0 = (int)((long long)BH * c / nch), b1 = (int)((long long)BH * (c + 1) / nch);
+        const size_t off = slice * b0, bytes = slice * (b1 - b0);
+        auto hp = [&](const void *p) { return static_cast<const char *>(p) + off; };
+        auto dp = [&](void *p) { return static_cast<char *>(p) + off; };
+        e = cudaMemcpyAsync(dp(dQ), hp(Qh), bytes, cudaMemcpyHostToDevice, s_in);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dp(dK), hp(Kh), bytes, cudaMemcpyHostToDevice, s_in);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dp(dV), hp(Vh), bytes, cudaMemcpyHostToDevice, s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(done_in[c], s_in);
+        if (e != cudaSuccess) break;
+        cudaStreamWaitEvent(s_k, done_in[c], 0);
+        st = splat_sparse_mhsa(a, dp(dQ), dp(dK), dp(dV), dt, 1, b1 - b0, d, scale, dp(dO), s_k);
+        if (st != SPLAT_OK) return st;
+        nl += g_launches;
+        if ((e = cudaEventRecord(done_k[c], s_k)) != cudaSuccess) break;
+        cudaStreamWaitEvent(s_out, done_k[c], 0);
+        e = cudaMemcpyAsync(static_cast<char *>(Oh) + off, static_cast<char *>(dO) + off, bytes, cudaMemcpyDeviceToHost,
+                            s_out);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "pipelined host copies");
+    // the caller's stream waits for the last copy-out (and, through it, for everything else)
+    cudaEvent_t fin = (cudaEvent_t)a->hev[1][15];
+    if ((e = cudaEventRecord(fin, s_out)) != cudaSuccess || (e = cudaStreamWaitEvent(cs, fin, 0)) != cudaSuccess)
+        return cuda_fail(e, "pipeline join");
+    note_launches(nl);
     return SPLAT_OK;
 }
 

@@ -196,6 +196,9 @@ struct splat_acsr_s {
     int32_t rv_l = 0, rv_nk = 0, rv_R = 0;   // stride, rows per residue (N / l), residues per 128-row tile
     float *d_lse = nullptr;                   // [B*H*N] log2-sum-exp of the strided pass (grown on demand)
     size_t lse_cap = 0;
+    // splat_sparse_mhsa_host pipeline: copy-in, compute and copy-out streams + per-chunk events
+    void *hs[3] = {nullptr, nullptr, nullptr};
+    void *hev[2][16] = {};
 };
 
 namespace splat {

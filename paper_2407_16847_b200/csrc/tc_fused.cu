@@ -276,6 +276,9 @@ __device__ __forceinline__ float max32(const float *v)
 // Number of the 32 exponentials of a chunk evaluated on the FMA pipe instead of MUFU (the MUFU
 // does 16 ex2/clk/SM against 8192 bf16 FLOP/clk on the tensor pipe: at d = 64 it is the
 // co-bottleneck).  Multiple of 4.
+#ifndef SPLAT_NEMU128
+#define SPLAT_NEMU128 4       // d = 128 (MUFU has more slack against the tensor pipe there)
+#endif
 #ifndef SPLAT_NEMU
 #define SPLAT_NEMU 8
 #endif
@@ -309,6 +312,7 @@ __device__ __forceinline__ void exp2_emu2(uint64_t z, float &ra, float &rb)
 }
 
 // p = exp2(s*c - m) for 32 scores -> 16 packed bf16 pairs; row-sum partials in acc0/acc1.
+template <int NEMU = SPLAT_NEMU>
 __device__ __forceinline__ void exp32(const float *v, uint64_t cc, uint64_t mm, uint64_t &acc0, uint64_t &acc1,
                                       uint32_t *pw)
 {
@@ -317,7 +321,7 @@ __device__ __forceinline__ void exp32(const float *v, uint64_t cc, uint64_t mm, 
         const uint64_t z0 = ffma2(pack2(v[x], v[x + 1]), cc, mm);
         const uint64_t z1 = ffma2(pack2(v[x + 2], v[x + 3]), cc, mm);
         float a, b, c, d;
-        if (x < SPLAT_NEMU) {
+        if (x < NEMU) {
             exp2_emu2(z0, a, b);
             exp2_emu2(z1, c, d);
         } else {
@@ -759,7 +763,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
                     if (live & (1u << w)) {
-                        exp32(sv + 32 * w, cc, mm, acc0, acc1, pw + 16 * w);
+                        exp32<D == 64 ? SPLAT_NEMU : SPLAT_NEMU128>(sv + 32 * w, cc, mm, acc0, acc1, pw + 16 * w);
                     } else {
 #pragma unroll
                         for (int x = 0; x < 16; ++x) pw[16 * w + x] = 0u;

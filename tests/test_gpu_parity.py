@@ -316,3 +316,21 @@ def test_full_mistral_sampled_heads_and_rows():
             r1 = min(cfg.N, r0 + 200)
             ref = O.attention(cfg.pattern, qs[bh], ks[bh], vs[bh], cfg.scale, rows=(r0, r1))
             assert maxabs(Ov[bh, r0:r1].float().cpu(), ref) <= TOL_BF16, (bh, r0)
+
+
+@pytest.mark.parametrize("cfg", [SMALL_BF16[0], RESIDUE[0], SMALL_BF16[4]], ids=lambda c: c.name)
+def test_host_path_pipelined_equals_device_call(cfg):
+    # splat_sparse_mhsa_host pipelines (b,h) chunks over three streams; the result must be
+    # bitwise the device-resident call's (same kernels, same per-(b,h) work, no atomics)
+    q, k, v = make_qkv(cfg)
+    a = S.Acsr(cfg.pattern, device=DEV)
+    Qd, Kd, Vd = dev(q), dev(k), dev(v)
+    Od = torch.empty_like(Qd)
+    S.splat_sparse_mhsa(a, Qd, Kd, Vd, Od, cfg.scale)
+    torch.cuda.synchronize()
+    qh, kh, vh = (x.contiguous().pin_memory() for x in (q, k, v))
+    oh = torch.empty_like(qh).pin_memory()
+    dQ, dK, dV, dO = (torch.empty_like(Qd) for _ in range(4))
+    S.splat_sparse_mhsa_host(a, qh, kh, vh, oh, cfg.scale, dQ, dK, dV, dO)
+    torch.cuda.synchronize()
+    assert torch.equal(oh, Od.cpu())
