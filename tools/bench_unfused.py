@@ -5,6 +5,7 @@ launching stream, L2 flushed before each launch) and its algorithmic HBM traffic
   R-SDDMM  : Q + K read (2 N d bytes each per head, bf16) + S written (4 B per non-zero)
   softmax  : S read (4 B / nnz) + P written (2 B / nnz for bf16)
   R-SpMM   : P read (2 B / nnz) + V read + O written (2 N d bytes each per head)
+Also the ACSR build + plan wall time (rows a1/a2, once per pattern).
 Not part of the bench contract; the fused kernel is the hot path bench.py times.
 """
 import argparse
@@ -46,6 +47,17 @@ def main():
         nbh = cfg.B * cfg.H
         if cfg.dtype != "bf16":
             continue
+        # row a1/a2: ACSR build + tile plan (synchronous, once per pattern): wall time of the call,
+        # median of 5 (device kernels + host planner + metadata upload)
+        import time
+        tb = []
+        for _ in range(5):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            a = S.Acsr(cfg.pattern, device=dev)
+            tb.append(time.perf_counter() - t0)
+            a.destroy()
+        build_ms = sorted(tb)[2] * 1e3
         a = S.Acsr(cfg.pattern, device=dev)
         # keep S (fp32) under ~60 GB
         cap = max(1, int(60e9 // (a.nnz * 6)))
@@ -66,7 +78,8 @@ def main():
         qkv = cfg.N * cfg.d * 2 * nbh
         byts = {"rsddmm": 2 * qkv + 4 * a.nnz * nbh, "softmax": 6 * a.nnz * nbh,
                 "rspmm": 2 * a.nnz * nbh + 2 * qkv}
-        out = {"config": name, "bh": nbh, "nnz_per_head": a.nnz}
+        out = {"config": name, "bh": nbh, "nnz_per_head": a.nnz, "acsr_build_ms": build_ms,
+               "acsr_meta_bytes": 81 * cfg.N}
         for k, fn in calls.items():
             for _ in range(3):
                 fn()
