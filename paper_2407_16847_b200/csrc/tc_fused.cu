@@ -853,7 +853,12 @@ struct SCfg {
     // per group: q_full[QS] q_empty[QS] k_full[KS] k_empty[KS] v_full[KS] v_empty[KS]
     //            s_full s_empty p_full pv_done epi
     static constexpr int NB = 2 * QS + 4 * KS + 5;
-    static constexpr int SMEM = OFF_BAR + 2 * NB * 8 + 16 + 1024;
+    // per group and Q slot: the unit's first kInfo plan entries (mask id, chunk bits), written by
+    // the producer before it arms q_full -- the softmax reads them with one broadcast LDS
+    static constexpr int kInfo = 32;
+    static constexpr int OFF_INFO = OFF_BAR + 2 * NB * 8;        // [2 groups][QS][kInfo] int2
+    static constexpr int SMEM = OFF_INFO + 2 * QS * kInfo * 8 + 16 + 1024;
+    static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 struct TUnit {
@@ -916,7 +921,8 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     uint64_t *v_full = k_empty + C::KS, *v_empty = v_full + C::KS;
     uint64_t *s_full = v_empty + C::KS, *s_empty = s_full + 1, *p_full = s_empty + 1;
     uint64_t *pv_done = p_full + 1, *epi = pv_done + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(reinterpret_cast<uint64_t *>(smem + C::OFF_BAR) + 2 * C::NB);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_INFO + 2 * C::QS * C::kInfo * 8);
+    int2 *info = reinterpret_cast<int2 *>(smem + C::OFF_INFO) + g * C::QS * C::kInfo;   // [QS][kInfo]
     const DevAcsr &A = prm.A;
     const int n_units = A.n_qt * prm.BH;
     const int first_unit = 2 * blockIdx.x + g, unit_stride = 2 * gridDim.x;
@@ -976,6 +982,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             const KvRegs kr = nkr;
             if (v + unit_stride < n_units) nx = fetch_tunit(A, prm.BH, v + unit_stride);
             if (qc >= C::QS) mbar_wait(&q_empty[qi], qph ^ 1);
+            if (lane < un.j1 - un.j0 && lane < C::kInfo)
+                info[qi * C::kInfo + lane] = make_int2(A.kv_mask[un.j0 + lane], (int)A.qt_bits[un.j0 + lane]);
+            __syncwarp();                     // the table is published by lane 0's arrive (release)
             if (lane == 0) {
                 mbar_expect_tx(&q_full[qi], C::TB);
                 tma_load_3d(gs + C::OFF_Q + qi * C::TB, &tmQ, &q_full[qi], 0, un.t * 128, un.bh);
@@ -1148,21 +1157,38 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         int pe_t = 0, pe_bh = 0;
         TUnit nx{0, 0, 0, 0};
         if (first_unit < n_units) nx = fetch_tunit(A, prm.BH, first_unit);
-        TileRegs ntr;
-        load_tile(A, nx.j0, nx.j1, lane, ntr);
+        // the unit's entry table (mask id, bits) of Q slot qs, entry index i = j - j0
+        int qs = 0;
+        uint32_t qph = 0;
+        auto entry = [&](int slot, int j0_, int j_) {
+            const int i = j_ - j0_;
+            return i < C::kInfo ? info[slot * C::kInfo + i] : make_int2(A.kv_mask[j_], (int)A.qt_bits[j_]);
+        };
+        auto mask_for = [&](int2 e) {       // row mask of this thread for entry e (ones if unneeded)
+            const uint32_t bits = (uint32_t)e.y;
+            const uint32_t need = (bits >> (4 * quad)) & ~(bits >> (16 + 4 * quad)) & 0xFu;
+            uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);
+            if (need && e.x >= 0) m = A.masks[(size_t)e.x * 128 + r];
+            return m;
+        };
         uint4 pf = make_uint4(~0u, ~0u, ~0u, ~0u);     // mask of the next entry to process
-        if (nx.j0 < nx.j1) pf = fetch_mask(A, ntr, nx.j0, nx.j0, quad, r);
+        if (nx.j0 < nx.j1) {
+            mbar_wait(&q_full[0], 0);
+            pf = mask_for(entry(0, nx.j0, nx.j0));
+        }
         for (int v = first_unit; v < n_units; v += unit_stride) {
             const TUnit un = nx;
-            const TileRegs tr = ntr;
             const bool has_next = v + unit_stride < n_units;
             if (has_next) nx = fetch_tunit(A, prm.BH, v + unit_stride);
             const int j0 = un.j0, j1 = un.j1;
+            const int slot = qs;
+            mbar_wait(&q_full[slot], qph);            // the unit's entry table is published
+            if (++qs == C::QS) { qs = 0; qph ^= 1; }
 #define SPLAT_NEXT_UNIT_PREFETCH()                                                                      \
     do {                                                                                                \
-        if (has_next) {                                                                                 \
-            load_tile(A, nx.j0, nx.j1, lane, ntr);                                                      \
-            if (nx.j0 < nx.j1) pf = fetch_mask(A, ntr, nx.j0, nx.j0, quad, r);                          \
+        if (has_next && nx.j0 < nx.j1) {                                                                \
+            mbar_wait(&q_full[qs], qph);                                                                \
+            pf = mask_for(entry(qs, nx.j0, nx.j0));                                                     \
         }                                                                                               \
     } while (0)
             float m_run = -INFINITY, l_run = 0.f;
@@ -1176,11 +1202,8 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             for (int j = j0; j < j1; ++j) {
                 if (store_leader) TRACE(2 + g, 5);
                 const uint4 m4 = pf;
-                int mid;
-                uint32_t bits;
-                tile_at(A, tr, j0, j, mid, bits);
-                bits = __shfl_sync(0xffffffffu, bits, 0);     // provably warp-uniform -> uniform branches
-                if (j + 1 < j1) pf = fetch_mask(A, tr, j0, j + 1, quad, r);
+                const uint32_t bits = (uint32_t)entry(slot, j0, j).y;
+                if (j + 1 < j1) pf = mask_for(entry(slot, j0, j + 1));
                 else SPLAT_NEXT_UNIT_PREFETCH();
                 const uint32_t mk[4] = {m4.x, m4.y, m4.z, m4.w};
                 uint32_t live = (bits >> (4 * quad)) & 0xFu;
