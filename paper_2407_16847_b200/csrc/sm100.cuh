@@ -70,7 +70,7 @@ __device__ __forceinline__ bool mbar_test(const uint64_t *bar, uint32_t parity)
 // Debug build: a wait that spins too long records, per (block, warp), the first stuck barrier
 // (smem address, parity) and gives up; once anything is stuck every later wait returns, so the
 // kernel terminates and the host can read the records.
-__device__ unsigned long long g_hang[1 + 148 * 16];
+__device__ unsigned long long g_hang[1 + 148 * 32];
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     const uint32_t a = smem_u32(bar);
@@ -80,8 +80,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         if (n == (1ll << 22)) {
             atomicAdd(&g_hang[0], 1ull);
             const int w = threadIdx.x >> 5;
-            if (blockIdx.x < 148 && w < 16 && (threadIdx.x & 31) == 0 && g_hang[1 + blockIdx.x * 16 + w] == 0ull)
-                g_hang[1 + blockIdx.x * 16 + w] = (1ull << 63) | ((unsigned long long)(clock64() & 0x7fffff) << 40) |
+            if (blockIdx.x < 148 && w < 32 && (threadIdx.x & 31) == 0 && g_hang[1 + blockIdx.x * 32 + w] == 0ull)
+                g_hang[1 + blockIdx.x * 32 + w] = (1ull << 63) | ((unsigned long long)(clock64() & 0x7fffff) << 40) |
                                                   ((unsigned long long)parity << 32) | a;
             n = 0;
             if (*(volatile unsigned long long *)&g_hang[0] > 64ull) g_hang[0] = 100000ull;
