@@ -334,3 +334,34 @@ def test_host_path_pipelined_equals_device_call(cfg):
     S.splat_sparse_mhsa_host(a, qh, kh, vh, oh, cfg.scale, dQ, dK, dV, dO)
     torch.cuda.synchronize()
     assert torch.equal(oh, Od.cpu())
+
+
+EDGE = [
+    # N = 1: a single query row attending only itself (O = V exactly up to bf16)
+    Config("n1_d64", Pattern("window", 1, lo=0, hi=0), 1, 2, 64, "bf16", 301),
+    Config("n1_d128", Pattern("window", 1, lo=0, hi=0), 1, 1, 128, "bf16", 302),
+    # N just past one tile, one row in the last tile
+    Config("n129", Pattern("window", 129, lo=3, hi=3), 1, 2, 64, "bf16", 303),
+    # many (b, h) units on a tiny N: more work units than group slots, several per CTA
+    Config("many_heads", Pattern("window", 256, lo=16, hi=16), 8, 80, 64, "bf16", 304),
+    Config("many_heads_d128", Pattern("blocked", 384, block=128), 4, 50, 128, "bf16", 305),
+    # full density (every tile FULL, no masks) and a dilated pattern with sparse chunks
+    Config("dense_d64", Pattern("window", 384, lo=384, hi=384), 1, 2, 64, "bf16", 306),
+    Config("dilated_d64", Pattern("dilated", 700, stride=7, radius=40), 1, 2, 64, "bf16", 307),
+]
+
+
+@pytest.mark.parametrize("cfg", EDGE, ids=lambda c: c.name)
+def test_bf16_fused_edge_cases(cfg):
+    q, k, v = make_qkv(cfg)
+    a = S.Acsr(cfg.pattern, device=DEV)
+    Q, K, V = dev(q), dev(k), dev(v)
+    Of = torch.empty_like(Q)
+    S.splat_sparse_mhsa(a, Q, K, V, Of, cfg.scale)
+    torch.cuda.synchronize()
+    shp = (cfg.BH, cfg.N, cfg.d)
+    heads = range(cfg.BH) if cfg.BH <= 8 else [0, 1, cfg.BH // 2, cfg.BH - 2, cfg.BH - 1]
+    refs = oracle_heads(cfg.pattern, q.view(shp), k.view(shp), v.view(shp), cfg.scale, heads)
+    Of = Of.view(shp).float().cpu()
+    for bh, o in zip(heads, refs):
+        assert maxabs(Of[bh], o) <= TOL_BF16, (cfg.name, bh)
