@@ -33,15 +33,22 @@
  *     row i at offset row_ptr[i] + x; within a row, columns ascend).  Base
  *     pointers must be 16-byte aligned.
  *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
- *     asynchronous on it and never allocate, synchronise or copy to host.
+ *     asynchronous on it and never synchronise or copy to host.  Exceptions:
+ *     the strided-row decomposition allocates its lse scratch (4*B*H*N bytes,
+ *     handle-owned) on the first call with a larger B*H, and
+ *     splat_sparse_mhsa_host creates its pipeline streams on first use.
  *   - The return status covers argument validation and the launch
  *     (cudaGetLastError -> SPLAT_ERR_CUDA); a kernel fault surfaces at the
  *     caller's next synchronisation.
  *   - On any error, splat_last_error() returns a thread-local message.
  *   - There is no CPU fallback: a compute call on a handle without a device
  *     (device < 0) fails with SPLAT_ERR_INVALID_ARG.
- *   - Handles are immutable after build: concurrent calls on different
- *     streams are safe.
+ *   - The handle's metadata and plan are immutable after build, but a handle
+ *     also owns mutable device state used by the compute calls (the fused
+ *     d = 64 kernel's work counter, the strided-row lse scratch): compute
+ *     calls on ONE handle must be ordered (one stream, or event-ordered);
+ *     use one handle per concurrent stream.  Different handles are
+ *     independent.
  */
 #ifndef SPLAT_H_
 #define SPLAT_H_

@@ -135,6 +135,7 @@ void free_device(splat_acsr_s *a)
     cudaFree(a->plan.d_kv_mask);
     cudaFree(a->plan.d_qt_bits);
     cudaFree(a->plan.d_t_info);
+    cudaFree(a->plan.d_sched);
 }
 
 void finish_host_meta(splat_acsr_s *a)
@@ -170,6 +171,7 @@ DevAcsr dev_view(const splat_acsr_s *a)
     A.n_buckets = a->plan.n_buckets;
     for (int b = 0; b <= a->plan.n_buckets && b <= kMaxBuckets; ++b) A.bucket_start[b] = a->plan.bucket_start[b];
     A.t_info = reinterpret_cast<const int4 *>(a->plan.d_t_info);
+    A.sched = a->plan.d_sched;
     A.t_n_buckets = a->plan.t_n_buckets;
     for (int b = 0; b <= a->plan.t_n_buckets && b <= kMaxBuckets; ++b) A.t_bucket_start[b] = a->plan.t_bucket_start[b];
     return A;
@@ -302,7 +304,8 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
         (e = cudaMalloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_qt_bits, sizeof(uint32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_t_info, sizeof(int32_t) * 4 * P.n_qt)) != cudaSuccess) {
+        (e = cudaMalloc(&P.d_t_info, sizeof(int32_t) * 4 * P.n_qt)) != cudaSuccess ||
+        (e = cudaMalloc(&P.d_sched, 2 * sizeof(unsigned long long))) != cudaSuccess) {
         free_device(a);
         delete a;
         return cuda_fail(e, "plan allocation");
@@ -334,6 +337,7 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
         e = cudaMemcpyAsync(P.d_qt_bits, P.qt_bits.data(), sizeof(uint32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_t_info, P.t_info.data(), sizeof(int32_t) * 4 * P.n_qt, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P.d_sched, 0, 2 * sizeof(unsigned long long), cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) {
         free_device(a);

@@ -35,6 +35,7 @@ struct DevAcsr {
     const int4 *t_info;         // [n_qt]: (tile, j0, j1, 0), bucketed longest first
     int t_n_buckets;
     int t_bucket_start[kMaxBuckets + 1];
+    unsigned long long *sched;  // [2]: dynamic work counter + done counter of the split kernel
 };
 
 cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, int64_t *row_ptr,

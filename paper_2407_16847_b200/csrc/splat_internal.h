@@ -167,6 +167,7 @@ struct Plan {
     int32_t *d_kv_mask = nullptr;
     uint32_t *d_qt_bits = nullptr;
     int32_t *d_t_info = nullptr;
+    unsigned long long *d_sched = nullptr;   // [2] split-kernel work / done counters (zero between launches)
 };
 
 }  // namespace splat

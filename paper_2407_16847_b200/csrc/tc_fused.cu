@@ -80,6 +80,7 @@ struct Params {
     //   pass 2 (merge = 1): natural band tiles; the epilogue merges with O_s (read from O) and lse
     int view, merge, rv_R, rv_nk, rv_l;
     float *lse;
+    unsigned long long *sched;   // split kernel: [work counter, done counter], zero between launches
 };
 
 // Profiling aid (SPLAT_TC_DEBUG & 4): clock64 timestamps of pipeline events in CTA 0.
@@ -857,7 +858,8 @@ struct SCfg {
     // the producer before it arms q_full -- the softmax reads them with one broadcast LDS
     static constexpr int kInfo = 32;
     static constexpr int OFF_INFO = OFF_BAR + 2 * NB * 8;        // [2 groups][QS][kInfo] int2
-    static constexpr int SMEM = OFF_INFO + 2 * QS * kInfo * 8 + 16 + 1024;
+    static constexpr int OFF_HDR = OFF_INFO + 2 * QS * kInfo * 8;  // [2 groups][QS] int4: unit (t, bh, j0, j1)
+    static constexpr int SMEM = OFF_HDR + 2 * QS * 16 + 16 + 1024;
     static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -921,11 +923,11 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     uint64_t *v_full = k_empty + C::KS, *v_empty = v_full + C::KS;
     uint64_t *s_full = v_empty + C::KS, *s_empty = s_full + 1, *p_full = s_empty + 1;
     uint64_t *pv_done = p_full + 1, *epi = pv_done + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_INFO + 2 * C::QS * C::kInfo * 8);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_HDR + 2 * C::QS * 16);
     int2 *info = reinterpret_cast<int2 *>(smem + C::OFF_INFO) + g * C::QS * C::kInfo;   // [QS][kInfo]
+    int4 *hdr = reinterpret_cast<int4 *>(smem + C::OFF_HDR) + g * C::QS;               // [QS]
     const DevAcsr &A = prm.A;
     const int n_units = A.n_qt * prm.BH;
-    const int first_unit = 2 * blockIdx.x + g, unit_stride = 2 * gridDim.x;
 #ifdef SPLAT_TRACE
     int tr_n = 0;
 #endif
@@ -973,18 +975,35 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             if (++vi == C::KS) { vi = 0; vph ^= 1; }
             pv = false;
         };
-        TUnit nx{0, 0, 0, 0};
-        if (first_unit < n_units) nx = fetch_tunit(A, prm.BH, first_unit);
+        // Dynamic schedule: the producer grabs the next unit from the handle's work counter (units
+        // are bucketed longest first, so greedy grabbing balances the long global-row tiles) and
+        // publishes it -- header (tile, bh, j0, j1) and entry table -- to the group's MMA and
+        // softmax warps with the Q slot's q_full; a header with tile -1 ends the stream.
+        auto grab = [&]() {
+            int v = 0;
+            if (lane == 0) v = (int)atomicAdd(prm.sched, 1ull);
+            v = __shfl_sync(0xffffffffu, v, 0);
+            return v < n_units ? fetch_tunit(A, prm.BH, v) : TUnit{-1, 0, 0, 0};
+        };
+        TUnit nx = grab();
         KvRegs nkr;
         load_kv(A, nx, lane, nkr);
-        for (int v = first_unit; v < n_units; v += unit_stride) {
+        while (true) {
             const TUnit un = nx;
             const KvRegs kr = nkr;
-            if (v + unit_stride < n_units) nx = fetch_tunit(A, prm.BH, v + unit_stride);
             if (qc >= C::QS) mbar_wait(&q_empty[qi], qph ^ 1);
+            if (un.t < 0) {
+                if (lane == 0) {
+                    hdr[qi] = make_int4(-1, 0, 0, 0);
+                    mbar_arrive(&q_full[qi]);
+                }
+                break;
+            }
+            nx = grab();                      // next unit, fetched in the shadow of this one
             if (lane < un.j1 - un.j0 && lane < C::kInfo)
                 info[qi * C::kInfo + lane] = make_int2(A.kv_mask[un.j0 + lane], (int)A.qt_bits[un.j0 + lane]);
-            __syncwarp();                     // the table is published by lane 0's arrive (release)
+            if (lane == 0) hdr[qi] = make_int4(un.t, un.bh, un.j0, un.j1);
+            __syncwarp();                     // header + table published by lane 0's arrive (release)
             if (lane == 0) {
                 mbar_expect_tx(&q_full[qi], C::TB);
                 tma_load_3d(gs + C::OFF_Q + qi * C::TB, &tmQ, &q_full[qi], 0, un.t * 128, un.bh);
@@ -1064,12 +1083,13 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             TRACE(1 + 3 * g, 20);
             pend = false;
         };
-        TUnit nx{0, 0, 0, 0};
-        if (first_unit < n_units) nx = fetch_tunit(A, prm.BH, first_unit);
-        for (int v = first_unit; v < n_units; v += unit_stride) {
-            const int uj0 = __shfl_sync(0xffffffffu, nx.j0, 0), uj1 = __shfl_sync(0xffffffffu, nx.j1, 0);
-            if (v + unit_stride < n_units) nx = fetch_tunit(A, prm.BH, v + unit_stride);
+        int4 *uhdr = reinterpret_cast<int4 *>(smem + C::OFF_HDR) + gu * C::QS;
+        while (true) {
             mbar_wait(&uq_full[qi], qph);
+            const int4 h4 = uhdr[qi];
+            const int ut = __shfl_sync(0xffffffffu, h4.x, 0);
+            if (ut < 0) break;
+            const int uj0 = __shfl_sync(0xffffffffu, h4.z, 0), uj1 = __shfl_sync(0xffffffffu, h4.w, 0);
             const uint32_t qb = sQ + qi * C::TB;
             if (uj0 == uj1) {      // no entries: the epilogue writes zeros
                 if (pend) flush_pv();
@@ -1155,8 +1175,6 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         bool pe_on = false;          // deferred epilogue of the previous unit
         float pe_l = 0.f;
         int pe_t = 0, pe_bh = 0;
-        TUnit nx{0, 0, 0, 0};
-        if (first_unit < n_units) nx = fetch_tunit(A, prm.BH, first_unit);
         // the unit's entry table (mask id, bits) of Q slot qs, entry index i = j - j0
         int qs = 0;
         uint32_t qph = 0;
@@ -1172,24 +1190,24 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             return m;
         };
         uint4 pf = make_uint4(~0u, ~0u, ~0u, ~0u);     // mask of the next entry to process
-        if (nx.j0 < nx.j1) {
+        {
             mbar_wait(&q_full[0], 0);
-            pf = mask_for(entry(0, nx.j0, nx.j0));
+            const int4 h0 = hdr[0];
+            if (h0.x >= 0 && h0.z < h0.w) pf = mask_for(entry(0, h0.z, h0.z));
         }
-        for (int v = first_unit; v < n_units; v += unit_stride) {
-            const TUnit un = nx;
-            const bool has_next = v + unit_stride < n_units;
-            if (has_next) nx = fetch_tunit(A, prm.BH, v + unit_stride);
-            const int j0 = un.j0, j1 = un.j1;
+        while (true) {
             const int slot = qs;
-            mbar_wait(&q_full[slot], qph);            // the unit's entry table is published
+            mbar_wait(&q_full[slot], qph);            // the unit's header and entry table are published
+            const int4 h4 = hdr[slot];
+            if (h4.x < 0) break;
+            const TUnit un{h4.x, h4.y, h4.z, h4.w};
             if (++qs == C::QS) { qs = 0; qph ^= 1; }
+            const int j0 = un.j0, j1 = un.j1;
 #define SPLAT_NEXT_UNIT_PREFETCH()                                                                      \
     do {                                                                                                \
-        if (has_next && nx.j0 < nx.j1) {                                                                \
-            mbar_wait(&q_full[qs], qph);                                                                \
-            pf = mask_for(entry(qs, nx.j0, nx.j0));                                                     \
-        }                                                                                               \
+        mbar_wait(&q_full[qs], qph);                                                                    \
+        const int4 hn = hdr[qs];                                                                        \
+        if (hn.x >= 0 && hn.z < hn.w) pf = mask_for(entry(qs, hn.z, hn.z));                            \
     } while (0)
             float m_run = -INFINITY, l_run = 0.f;
             bool first = true;
@@ -1311,6 +1329,16 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
+    // the last CTA to finish resets the work counter for the next launch on this handle (every
+    // grab of every CTA happened before its increment of the done counter)
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(prm.sched + 1, 1ull) == (unsigned long long)gridDim.x - 1ull) {
+            prm.sched[0] = 0ull;
+            prm.sched[1] = 0ull;
+            __threadfence();
+        }
+    }
 }
 
 // ---------------------------------------------------------------- host side
@@ -1390,6 +1418,8 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
         return e ? atoi(e) : 0;
     }();
     p.dbg = dbg;
+    p.sched = A.sched;
+    if (!p.sched) return cudaErrorInvalidValue;
     const long long units = (long long)A.n_qt * BH;
     const long long ctas = (units + 1) / 2;
     const int grid = (int)(ctas < num_sms(dev) ? ctas : num_sms(dev));
