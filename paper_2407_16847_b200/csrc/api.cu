@@ -125,12 +125,8 @@ void free_device(splat_acsr_s *a)
     cudaFree(a->plan.d_qt_ptr);
     cudaFree(a->plan.d_kv);
     cudaFree(a->plan.d_order);
-    cudaFree(a->plan.d_pair_ptr);
     cudaFree(a->plan.d_pair_ent);
-    cudaFree(a->plan.d_pair_order);
     cudaFree(a->plan.d_pair_info);
-    cudaFree(a->plan.d_pair_mask);
-    cudaFree(a->plan.d_pair_live);
     cudaFree(a->plan.d_masks);
     cudaFree(a->plan.d_kv_mask);
     cudaFree(a->plan.d_qt_bits);
@@ -158,12 +154,8 @@ DevAcsr dev_view(const splat_acsr_s *a)
     A.kv = a->plan.d_kv;
     A.order = a->plan.d_order;
     A.n_qt = a->plan.n_qt;
-    A.pair_ptr = a->plan.d_pair_ptr;
     A.pair_ent = a->plan.d_pair_ent;
-    A.pair_order = a->plan.d_pair_order;
     A.pair_info = reinterpret_cast<const int4 *>(a->plan.d_pair_info);
-    A.pair_mask = reinterpret_cast<const int2 *>(a->plan.d_pair_mask);
-    A.pair_live = a->plan.d_pair_live;
     A.masks = reinterpret_cast<const uint4 *>(a->plan.d_masks);
     A.kv_mask = a->plan.d_kv_mask;
     A.qt_bits = a->plan.d_qt_bits;
@@ -295,12 +287,8 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
     if ((e = cudaMalloc(&P.d_qt_ptr, sizeof(int32_t) * (P.n_qt + 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_kv, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_order, sizeof(int32_t) * P.n_qt)) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_pair_ptr, sizeof(int32_t) * (P.n_pairs + 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_ent, sizeof(int32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_pair_order, sizeof(int32_t) * P.n_pairs)) != cudaSuccess ||
         (e = cudaMalloc(&P.d_pair_info, sizeof(int32_t) * 8 * P.n_pairs)) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_pair_mask, sizeof(int32_t) * 2 * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_pair_live, sizeof(uint32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_qt_bits, sizeof(uint32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
@@ -315,20 +303,10 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
         e = cudaMemcpyAsync(P.d_kv, P.kv.data(), sizeof(int32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_order, P.order.data(), sizeof(int32_t) * P.n_qt, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(P.d_pair_ptr, P.pair_ptr.data(), sizeof(int32_t) * (P.n_pairs + 1), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && P.n_pair_entries > 0)
         e = cudaMemcpyAsync(P.d_pair_ent, P.pair_ent.data(), sizeof(int32_t) * P.n_pair_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(P.d_pair_order, P.pair_order.data(), sizeof(int32_t) * P.n_pairs, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_pair_info, P.pair_info.data(), sizeof(int32_t) * 8 * P.n_pairs, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess && P.n_pair_entries > 0)
-        e = cudaMemcpyAsync(P.d_pair_mask, P.pair_mask.data(), sizeof(int32_t) * 2 * P.n_pair_entries,
-                            cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess && P.n_pair_entries > 0)
-        e = cudaMemcpyAsync(P.d_pair_live, P.pair_live.data(), sizeof(uint32_t) * P.n_pair_entries,
-                            cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && !P.masks.empty())
         e = cudaMemcpyAsync(P.d_masks, P.masks.data(), sizeof(uint32_t) * P.masks.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && P.n_entries > 0)

@@ -20,12 +20,8 @@ struct DevAcsr {
     const int32_t *order;   // [n_qt]
     int n_qt;
     // query-tile pairs (fused kernel)
-    const int32_t *pair_ptr;    // [n_pairs+1]
     const int32_t *pair_ent;    // kv | kUseA | kUseB | kPartA | kPartB
-    const int32_t *pair_order;  // [n_pairs], bucketed longest first
     const int4 *pair_info;      // [n_pairs][2]: (pair, e0, e1, jA0), (jA1, jB1, 0, 0) in pair_order order
-    const int2 *pair_mask;      // [n_pair_entries]: mask id for tile A / B (-1: none)
-    const uint32_t *pair_live;  // [n_pair_entries]: chunk liveness per (group, warp quad)
     const uint4 *masks;         // [n_masks][128]: row column masks
     const int32_t *kv_mask;     // [n_entries]: mask id per (query tile, key tile) entry, -1 = FULL
     const uint32_t *qt_bits;    // [n_entries]: chunk live (bit 4 quad + w) / full (bit 16 + 4 quad + w)

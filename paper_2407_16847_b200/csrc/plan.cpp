@@ -155,7 +155,6 @@ void build_plan(splat_acsr_s &a)
     // of reading A-7 evaluated once per pattern, shared by every (b, h)), and per-warp chunk
     // liveness of every entry.
     P.pair_mask.assign((size_t)P.n_pair_entries * 2, -1);
-    P.pair_live.assign(P.n_pair_entries, 0u);
     // qt_bits per query-tile entry: bit 4 quad + w = chunk w (32 key columns) has a valid entry
     // in some row of warp quad; bit 16 + 4 quad + w = every row of the warp has all 32 columns
     // (the softmax skips the fast-index mask there).
@@ -167,10 +166,7 @@ void build_plan(splat_acsr_s &a)
             for (int g = 0; g < 2; ++g) {
                 const int t = 2 * p + g;
                 if (!(ent & (g == 0 ? kUseA : kUseB))) continue;
-                if (!(ent & (g == 0 ? kPartA : kPartB))) {
-                    P.pair_live[e] |= 0xFFFFu << (16 * g);
-                    continue;
-                }
+                if (!(ent & (g == 0 ? kPartA : kPartB))) continue;
                 const size_t base = P.masks.size();
                 P.masks.resize(base + 128 * 4, 0u);
                 uint32_t *m = &P.masks[base];
@@ -186,8 +182,6 @@ void build_plan(splat_acsr_s &a)
                         const int first = start + ((lo - start + step - 1) / step) * step;
                         for (int c = first; c <= hi; c += step) m[4 * r + ((c - c0) >> 5)] |= 1u << ((c - c0) & 31);
                     }
-                    for (int w = 0; w < 4; ++w)
-                        if (m[4 * r + w]) P.pair_live[e] |= 1u << (16 * g + 4 * (r >> 5) + w);
                 }
                 P.pair_mask[(size_t)e * 2 + g] = (int32_t)(base / (128 * 4));
                 uint32_t bits = 0;

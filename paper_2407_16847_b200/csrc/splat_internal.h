@@ -153,7 +153,6 @@ struct Plan {
     std::vector<int32_t> pair_ptr, pair_ent, pair_order, bucket_start;
     std::vector<int32_t> pair_info;   // [n_pairs][8]: pair, e0, e1, jA0, jA1, jB1, 0, 0 -- in pair_order order
     std::vector<int32_t> pair_mask;   // [n_pair_entries][2]: mask id of tile A / B (-1: FULL or unused)
-    std::vector<uint32_t> pair_live;  // [n_pair_entries]: bit 16g + 4 quad + w = chunk w live for warp quad
     std::vector<uint32_t> masks;      // [n_masks][128 rows][4 words]: column mask of each row
     std::vector<int32_t> kv_mask;     // [n_entries]: mask id of each (query tile, key tile) entry (-1: FULL)
     std::vector<uint32_t> qt_bits;    // [n_entries]: per-warp chunk live (bits 0-15) / full (bits 16-31)
@@ -161,9 +160,8 @@ struct Plan {
     std::vector<int32_t> t_bucket_start;  // single-tile units: bucket boundaries in t_info order
     std::vector<int32_t> t_info;          // [n_qt][4]: tile, j0, j1, 0 -- bucketed longest first
     int32_t *d_qt_ptr = nullptr, *d_kv = nullptr, *d_order = nullptr;
-    int32_t *d_pair_ptr = nullptr, *d_pair_ent = nullptr, *d_pair_order = nullptr;
-    int32_t *d_pair_info = nullptr, *d_pair_mask = nullptr;
-    uint32_t *d_pair_live = nullptr, *d_masks = nullptr;
+    int32_t *d_pair_ent = nullptr, *d_pair_info = nullptr;
+    uint32_t *d_masks = nullptr;
     int32_t *d_kv_mask = nullptr;
     uint32_t *d_qt_bits = nullptr;
     int32_t *d_t_info = nullptr;

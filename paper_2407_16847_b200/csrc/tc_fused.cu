@@ -179,41 +179,15 @@ __device__ __forceinline__ uint4 fetch_mask(const DevAcsr &A, const TileRegs &tr
 // falls back to a global load).
 struct EntRegs {
     int r[4];
-    uint32_t l[4];   // pair_live words of the same entries
-    int m[4];        // mask id of tile group g (softmax warps only)
 };
 
-__device__ __forceinline__ void load_ents(const DevAcsr &A, const UnitInfo &un, int lane, EntRegs &er, int g = -1)
+__device__ __forceinline__ void load_ents(const DevAcsr &A, const UnitInfo &un, int lane, EntRegs &er)
 {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int idx = un.e0 + lane + 32 * k;
         er.r[k] = idx < un.e1 ? A.pair_ent[idx] : 0;
-        er.l[k] = idx < un.e1 ? A.pair_live[idx] : 0u;
-        er.m[k] = (g >= 0 && idx < un.e1) ? (g == 0 ? A.pair_mask[idx].x : A.pair_mask[idx].y) : 0;
     }
-}
-
-__device__ __forceinline__ int mask_at(const DevAcsr &A, const UnitInfo &un, const EntRegs &er, int e, int g)
-{
-    const int i = e - un.e0;
-    if (i < 128) {
-        const int k = i >> 5;
-        const int v = k == 0 ? er.m[0] : (k == 1 ? er.m[1] : (k == 2 ? er.m[2] : er.m[3]));
-        return __shfl_sync(0xffffffffu, v, i & 31);
-    }
-    return g == 0 ? A.pair_mask[e].x : A.pair_mask[e].y;
-}
-
-__device__ __forceinline__ uint32_t live_at(const DevAcsr &A, const UnitInfo &un, const EntRegs &er, int e)
-{
-    const int i = e - un.e0;
-    if (i < 128) {
-        const int k = i >> 5;
-        const uint32_t v = k == 0 ? er.l[0] : (k == 1 ? er.l[1] : (k == 2 ? er.l[2] : er.l[3]));
-        return __shfl_sync(0xffffffffu, v, i & 31);
-    }
-    return A.pair_live[e];
 }
 
 __device__ __forceinline__ int ent_at(const DevAcsr &A, const UnitInfo &un, const EntRegs &er, int e)

@@ -443,7 +443,6 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             const int e0 = A.qt_ptr[t], e1 = A.qt_ptr[t + 1];
             int e = e0 + (int)((eg - (int)(i % kNWGP) + kNWGP) % kNWGP);
             i += (uint32_t)(e1 - e0);
-            const int row = t * 128 + r;
             if (e < e1) {
                 const int nrows = min(32, A.n - (t * 128 + quad * 32));
                 RowRuns R;
