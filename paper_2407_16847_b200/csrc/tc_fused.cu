@@ -1206,21 +1206,18 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 if (store_leader) TRACE(2 + g, 2);
                 float mx = -INFINITY;
                 float sv[128];
-                // the whole S row -> registers in two halves (the second half's load overlaps the
-                // first half's mask + max), then S goes back to the MMA warp
+                // the whole S row -> registers (one wait: under MMA traffic the TMEM load latency,
+                // not the max, dominates), then S goes back to the MMA warp
                 tmem_ld32(s_tm, sv);
                 tmem_ld32(s_tm + 32, sv + 32);
-                tmem_wait_ld();
                 tmem_ld32(s_tm + 64, sv + 64);
                 tmem_ld32(s_tm + 96, sv + 96);
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(s_empty);
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
-                    if (w == 2) {
-                        tmem_wait_ld();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(s_empty);
-                    }
                     if (live & (1u << w)) {
                         if (need & (1u << w)) apply_mask(sv + 32 * w, mk[w]);
                         mx = fmax3(mx, max32(sv + 32 * w), -INFINITY);
