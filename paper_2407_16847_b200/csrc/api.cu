@@ -542,8 +542,13 @@ splat_status splat_sparse_mhsa_host(splat_acsr a, const void *Qh, const void *Kh
     if (e != cudaSuccess) return cuda_fail(e, "pipeline streams");
     cudaStream_t s_in = (cudaStream_t)a->hs[0], s_k = (cudaStream_t)a->hs[1], s_out = (cudaStream_t)a->hs[2];
     // chunks of (b, h) slices: enough to overlap, each still filling the GPU
-    const int nch = BH >= 8 ? 8 : BH;
-    cudaEvent_t start = (cudaEvent_t)a->hev[0][15], done_k[8], done_in[8];
+    static const int max_ch = [] {
+        const char *v = getenv("SPLAT_HOST_CHUNKS");      // tuning knob, <= 15
+        const int c = v ? atoi(v) : 12;
+        return c < 1 ? 1 : (c > 15 ? 15 : c);
+    }();
+    const int nch = BH >= max_ch ? max_ch : BH;
+    cudaEvent_t start = (cudaEvent_t)a->hev[0][15], done_k[15], done_in[15];
     for (int c = 0; c < nch; ++c) {
         done_in[c] = (cudaEvent_t)a->hev[0][c];
         done_k[c] = (cudaEvent_t)a->hev[1][c];
