@@ -62,6 +62,21 @@ struct ParamsU {
     long long nat_nnz;
 };
 
+// Profiling aid (SPLAT_UNF_PROF build): cycles each warp of CTA 0 spends in barrier waits, by
+// call site, and in total; read with splat_debug_unf_prof.
+__device__ unsigned long long g_unf_prof[32][8];
+#ifdef SPLAT_UNF_PROF
+#define PWAIT(SITE, BAR, PH)                                                                    \
+    do {                                                                                        \
+        const unsigned long long t0_ = clock64();                                               \
+        mbar_wait(BAR, PH);                                                                     \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                                         \
+            g_unf_prof[threadIdx.x >> 5][SITE] += clock64() - t0_;                              \
+    } while (0)
+#else
+#define PWAIT(SITE, BAR, PH) mbar_wait(BAR, PH)
+#endif
+
 // predicated 4-byte global store (no branch / reconvergence per element)
 __device__ __forceinline__ void st_pred_f32(float *addr, float v, uint32_t pred)
 {
@@ -338,7 +353,9 @@ struct CfgP {
     static constexpr int KS = D == 64 ? 4 : 2;
     static constexpr int OFF_V = 0;
     static constexpr int OFF_P = OFF_V + KS * kTileBytes;             // [kNWGP] P tiles, 32 KB each
-    static constexpr int OFF_BAR = OFF_P + kNWGP * 2 * kSub;
+    // per gather warpgroup, double-buffered: [128 rows] {P offset of the row's span, row mask}
+    static constexpr int OFF_RI = OFF_P + kNWGP * 2 * kSub;
+    static constexpr int OFF_BAR = OFF_RI + kNWGP * 2 * 128 * 32;
     static constexpr int NBAR = 2 * KS + 2 * kNWGP + 4;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
     static constexpr int TMEM_COLS = 2 * D;                           // O double buffer
@@ -361,6 +378,9 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevAcsr &A = prm.A;
     const int n_units = A.n_qt * prm.BH;
+#ifdef SPLAT_UNF_PROF
+    const unsigned long long t_start = clock64();
+#endif
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::KS; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
@@ -383,7 +403,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             unit_tile(A, u, bh, t);
             for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
                 const int kv = A.kv[e] & kKvMask;
-                if (kc >= C::KS) mbar_wait(&v_empty[ki], kph ^ 1);
+                if (kc >= C::KS) PWAIT(0, &v_empty[ki], kph ^ 1);
                 if (lane == 0) {
                     mbar_expect_tx(&v_full[ki], C::kTileBytes);
 #pragma unroll
@@ -404,12 +424,12 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             int bh, t;
             unit_tile(A, u, bh, t);
             const int ob = uo & 1;
-            if (uo >= 2) mbar_wait(&o_empty[ob], ((uo >> 1) - 1) & 1);
+            if (uo >= 2) PWAIT(1, &o_empty[ob], ((uo >> 1) - 1) & 1);
             bool first = true;
             for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
                 const int pb = np % kNWGP;
-                mbar_wait(&v_full[ki], kph);
-                mbar_wait(&p_full[pb], (np / kNWGP) & 1);
+                PWAIT(2, &v_full[ki], kph);
+                PWAIT(3, &p_full[pb], (np / kNWGP) & 1);
                 ++np;
                 tc_fence_after();
                 const uint32_t vb = sV + ki * C::kTileBytes, pa = sP + pb * 2 * kSub;
@@ -429,10 +449,18 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             __syncwarp();
         }
     } else if (warp >= 6) {
-        // gather warpgroup eg takes P tiles i = eg, eg + kNWGP, ...; warp quad fills query rows
-        // 32 quad .. 32 quad + 31 of the tile.
+        // gather warpgroup eg takes P tiles i = eg, eg + kNWGP, ...  Thread r publishes its query
+        // row's span offset and column mask for the tile; warp q then fills rows q, q + 4, ...
+        // (interleaved, so rows with many non-zeros -- e.g. Longformer's global rows, which all sit
+        // in the first 32 rows of tile 0 -- are spread over the four warps).
         const int eg = (warp - 6) >> 2, quad = warp & 3, r = quad * 32 + lane;
         uint8_t *ptile = smem + C::OFF_P + eg * 2 * kSub;
+        struct RowInfo {
+            long long off;
+            int valid, pad;
+            uint4 m;
+        };
+        RowInfo *ri = reinterpret_cast<RowInfo *>(smem + C::OFF_RI) + eg * 2 * 128;
         const uint32_t below = (1u << lane) - 1u;
         const unsigned short *Pg = reinterpret_cast<const unsigned short *>(prm.P);
         const long long total = (long long)prm.BH * (prm.pass ? prm.nat_nnz : A.nnz);   // elements of P
@@ -444,40 +472,49 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             int e = e0 + (int)((eg - (int)(i % kNWGP) + kNWGP) % kNWGP);
             i += (uint32_t)(e1 - e0);
             if (e < e1) {
-                const int nrows = min(32, A.n - (t * 128 + quad * 32));
                 RowRuns R;
                 const long long rowoff = row_offset(prm, bh, t, r, R);
+                const bool rvalid = t * 128 + r < A.n;
                 for (; e < e1; e += kNWGP) {
                     const int ent = A.kv[e];
                     const int c0 = (ent & kKvMask) * 128;
                     const bool partial = (ent & kPartialBit) != 0;
-                    uint4 m4 = make_uint4(~0u, ~0u, ~0u, ~0u);
-                    if (partial) m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
-                    const long long off = rowoff + rank_before(R, c0);
+                    RowInfo *rb = ri + (k & 1) * 128;
+                    {
+                        uint4 m4 = make_uint4(~0u, ~0u, ~0u, ~0u);
+                        if (partial) m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
+                        RowInfo x;
+                        x.off = rowoff + rank_before(R, c0);
+                        x.valid = rvalid;
+                        x.pad = 0;
+                        x.m = rvalid ? m4 : make_uint4(0u, 0u, 0u, 0u);
+                        rb[r] = x;
+                    }
+                    wg_sync(1 + eg);          // row table of this tile complete (double-buffered)
+                    if (k >= 1) mbar_wait(&p_empty[eg], (k - 1) & 1);
                     if (!partial) {
                         // FULL tile: each row's segment is 128 consecutive values.  Lane l loads the
                         // 8-byte aligned words l (and l+1 when the segment is not 8-byte aligned) and
                         // funnel-shifts columns 4l .. 4l+3 out of them: 8 bytes per lane per row.
-                        for (int r0 = 0; r0 < 32; r0 += kRF) {
+                        for (int j0 = 0; j0 < 32; j0 += kRF) {
                             uint2 c[kRF], x[kRF];
                             int sh[kRF];
 #pragma unroll
                             for (int j = 0; j < kRF; ++j) {
-                                const int rr = r0 + j;
-                                const long long o = __shfl_sync(0xffffffffu, off, rr);
+                                const int rr = quad + 4 * (j0 + j);
+                                const long long o = rb[rr].off;
                                 const long long a = o & ~3ll;
                                 sh[j] = (int)(o - a);
                                 const uint2 *src = reinterpret_cast<const uint2 *>(Pg + a) + lane;
                                 c[j] = x[j] = make_uint2(0u, 0u);
-                                if (rr < nrows) {
+                                if (rb[rr].valid) {
                                     c[j] = __ldg(src);
                                     if (sh[j] && a + 4 * lane + 8 <= total) x[j] = __ldg(src + 1);
                                 }
                             }
-                            if (r0 == 0 && k >= 1) mbar_wait(&p_empty[eg], (k - 1) & 1);
 #pragma unroll
                             for (int j = 0; j < kRF; ++j) {
-                                const int rr = quad * 32 + r0 + j;
+                                const int rr = quad + 4 * (j0 + j);
                                 uint2 v = c[j];
                                 if (sh[j] == 1) v = make_uint2(__funnelshift_r(c[j].x, c[j].y, 16), __funnelshift_r(c[j].y, x[j].x, 16));
                                 else if (sh[j] == 2) v = make_uint2(c[j].y, x[j].x);
@@ -488,37 +525,36 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                             }
                         }
                     } else {
-                    if (k >= 1) mbar_wait(&p_empty[eg], (k - 1) & 1);
-                    // kRB rows per batch: 4 kRB independent loads in flight per lane
-                    for (int r0 = 0; r0 < 32; r0 += kRB) {
-                        unsigned short h[kRB][4];
+                        // kRB rows per batch: 4 kRB independent loads in flight per lane
+                        for (int j0 = 0; j0 < 32; j0 += kRB) {
+                            unsigned short h[kRB][4];
 #pragma unroll
-                        for (int j = 0; j < kRB; ++j) {
-                            const int rr = r0 + j;
-                            const long long o = __shfl_sync(0xffffffffu, off, rr);
-                            const uint32_t mw[4] = {__shfl_sync(0xffffffffu, m4.x, rr), __shfl_sync(0xffffffffu, m4.y, rr),
-                                                    __shfl_sync(0xffffffffu, m4.z, rr), __shfl_sync(0xffffffffu, m4.w, rr)};
-                            const unsigned short *src = Pg + o;
-                            int pre = 0;
+                            for (int j = 0; j < kRB; ++j) {
+                                const int rr = quad + 4 * (j0 + j);
+                                const long long o = rb[rr].off;
+                                const uint4 mm = rb[rr].m;
+                                const uint32_t mw[4] = {mm.x, mm.y, mm.z, mm.w};
+                                const unsigned short *src = Pg + o;
+                                int pre = 0;
 #pragma unroll
-                            for (int w = 0; w < 4; ++w) {
-                                h[j][w] = 0;
-                                if (rr < nrows && ((mw[w] >> lane) & 1u)) h[j][w] = __ldg(src + pre + __popc(mw[w] & below));
-                                pre += __popc(mw[w]);
+                                for (int w = 0; w < 4; ++w) {
+                                    h[j][w] = 0;
+                                    if ((mw[w] >> lane) & 1u) h[j][w] = __ldg(src + pre + __popc(mw[w] & below));
+                                    pre += __popc(mw[w]);
+                                }
+                            }
+#pragma unroll
+                            for (int j = 0; j < kRB; ++j) {
+                                const int rr = quad + 4 * (j0 + j);     // row within the tile
+#pragma unroll
+                                for (int w = 0; w < 4; ++w) {
+                                    // column 32 w + lane -> sub-tile w/2, 16-byte chunk (col & 63) / 8, swizzled by row
+                                    const int cc = (32 * (w & 1) + lane);
+                                    const int byte = rr * 128 + ((((cc >> 3) ^ (rr & 7))) << 4) + (cc & 7) * 2;
+                                    *reinterpret_cast<unsigned short *>(ptile + (w >> 1) * kSub + byte) = h[j][w];
+                                }
                             }
                         }
-#pragma unroll
-                        for (int j = 0; j < kRB; ++j) {
-                            const int rr = quad * 32 + r0 + j;     // row within the tile
-#pragma unroll
-                            for (int w = 0; w < 4; ++w) {
-                                // column 32 w + lane -> sub-tile w/2, 16-byte chunk (col & 63) / 8, swizzled by row
-                                const int cc = (32 * (w & 1) + lane);
-                                const int byte = rr * 128 + ((((cc >> 3) ^ (rr & 7))) << 4) + (cc & 7) * 2;
-                                *reinterpret_cast<unsigned short *>(ptile + (w >> 1) * kSub + byte) = h[j][w];
-                            }
-                        }
-                    }
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -540,7 +576,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             const int e0 = A.qt_ptr[t], e1 = A.qt_ptr[t + 1];
             {
                 const int ob = uo & 1;
-                mbar_wait(&o_full[ob], (uo >> 1) & 1);
+                PWAIT(5, &o_full[ob], (uo >> 1) & 1);
                 tc_fence_after();
                 const bool empty = e0 == e1;   // no key tile: O = 0
                 const int nrow = nat_row(prm, t, r);
@@ -585,6 +621,9 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             }
         }
     }
+#ifdef SPLAT_UNF_PROF
+    if (blockIdx.x == 0 && lane == 0) g_unf_prof[warp][7] = clock64() - t_start;
+#endif
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
@@ -745,3 +784,11 @@ cudaError_t launch_rspmm_tc(const DevAcsr &A, const void *P, const void *V, int 
 }
 
 }  // namespace splat
+
+extern "C" int splat_debug_unf_prof(unsigned long long *out)
+{
+    cudaMemcpyFromSymbol(out, splat::g_unf_prof, sizeof(splat::g_unf_prof));
+    static const unsigned long long z[32 * 8] = {};
+    cudaMemcpyToSymbol(splat::g_unf_prof, z, sizeof(z));
+    return 0;
+}
