@@ -804,6 +804,21 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     }
 }
 
+// Profiling aid (SPLAT_FUSED_PROF build): cycles each warp of CTA 0 spends in each barrier wait
+// of the split kernel (by call site) and in total; read with splat_debug_fused_prof.
+__device__ unsigned long long g_fprof[12][16];
+#ifdef SPLAT_FUSED_PROF
+#define FWAIT(SITE, BAR, PH)                                                                    \
+    do {                                                                                        \
+        const unsigned long long t0_ = clock64();                                               \
+        mbar_wait(BAR, PH);                                                                     \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                                         \
+            g_fprof[threadIdx.x >> 5][SITE] += clock64() - t0_;                                 \
+    } while (0)
+#else
+#define FWAIT(SITE, BAR, PH) mbar_wait(BAR, PH)
+#endif
+
 // ================================================================ split-group kernel (d = 64)
 //
 // The two tile groups of a CTA run fully independent pipelines (own Q/K/V rings, own
@@ -902,6 +917,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     int4 *hdr = reinterpret_cast<int4 *>(smem + C::OFF_HDR) + g * C::QS;               // [QS]
     const DevAcsr &A = prm.A;
     const int n_units = A.n_qt * prm.BH;
+#ifdef SPLAT_FUSED_PROF
+    const unsigned long long t_start = clock64();
+#endif
 #ifdef SPLAT_TRACE
     int tr_n = 0;
 #endif
@@ -936,7 +954,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         bool pv = false;            // V of the previous entry still to load
         int pv_kv = 0, pv_bh = 0;
         auto load_v = [&]() {
-            if (vc >= C::KS) mbar_wait(&v_empty[vi], vph ^ 1);
+            if (vc >= C::KS) FWAIT(10, &v_empty[vi], vph ^ 1);
             if (lane == 0) {
                 if (prm.dbg & 16) {          // profiling aid: no TMA traffic (garbage K/V)
                     mbar_arrive(&v_full[vi]);
@@ -965,7 +983,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         while (true) {
             const TUnit un = nx;
             const KvRegs kr = nkr;
-            if (qc >= C::QS) mbar_wait(&q_empty[qi], qph ^ 1);
+            if (qc >= C::QS) FWAIT(8, &q_empty[qi], qph ^ 1);
             if (un.t < 0) {
                 if (lane == 0) {
                     hdr[qi] = make_int4(-1, 0, 0, 0);
@@ -988,7 +1006,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 const int kv = kv_at(A, un, kr, j);
                 if (j == un.j0 + 1) load_kv(A, nx, lane, nkr);   // next unit's entries, in the shadow
                 TRACE(g == 0 ? 0 : 5, 30);
-                if (kc >= C::KS) mbar_wait(&k_empty[ki], kph ^ 1);
+                if (kc >= C::KS) FWAIT(9, &k_empty[ki], kph ^ 1);
                 TRACE(g == 0 ? 0 : 5, 31);
                 if (lane == 0) {
                     if (prm.dbg & 16) {
@@ -1034,9 +1052,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         int pst = 0, pq = 0;
         uint32_t pph = 0;
         auto flush_pv = [&]() {
-            mbar_wait(up_full, pcnt & 1);
+            FWAIT(6, up_full, pcnt & 1);
             ++pcnt;
-            mbar_wait(&uv_full[pst], pph);
+            FWAIT(7, &uv_full[pst], pph);
             tc_fence_after();
             const uint32_t vbase = sV + pst * C::TB;
             if (elect_one()) {
@@ -1059,7 +1077,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         };
         int4 *uhdr = reinterpret_cast<int4 *>(smem + C::OFF_HDR) + gu * C::QS;
         while (true) {
-            mbar_wait(&uq_full[qi], qph);
+            FWAIT(11, &uq_full[qi], qph);
             const int4 h4 = uhdr[qi];
             const int ut = __shfl_sync(0xffffffffu, h4.x, 0);
             if (ut < 0) break;
@@ -1075,9 +1093,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 const uint32_t ph = (gent / C::KS) & 1;
                 ++gent;
                 TRACE(1 + 3 * g, 9);
-                mbar_wait(&uk_full[st], ph);
+                FWAIT(4, &uk_full[st], ph);
                 TRACE(1 + 3 * g, 11);
-                if (scnt > 0) mbar_wait(us_empty, (scnt - 1) & 1);   // softmax has read the previous S
+                if (scnt > 0) FWAIT(5, us_empty, (scnt - 1) & 1);   // softmax has read the previous S
                 ++scnt;
                 tc_fence_after();
                 const uint32_t kbase = sK + st * C::TB;
@@ -1119,7 +1137,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         const uint32_t ostage_u = smem_u32(ostage);
         uint32_t s_cnt = 0, e_cnt = 0;
         auto epilogue = [&](float l, int t, int bh) {
-            mbar_wait(epi, e_cnt & 1);
+            FWAIT(2, epi, e_cnt & 1);
             ++e_cnt;
             tc_fence_after();
             if (store_leader) TRACE(2 + g, 8);
@@ -1171,7 +1189,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         }
         while (true) {
             const int slot = qs;
-            mbar_wait(&q_full[slot], qph);            // the unit's header and entry table are published
+            FWAIT(3, &q_full[slot], qph);            // the unit's header and entry table are published
             const int4 h4 = hdr[slot];
             if (h4.x < 0) break;
             const TUnit un{h4.x, h4.y, h4.z, h4.w};
@@ -1200,7 +1218,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 const uint32_t mk[4] = {m4.x, m4.y, m4.z, m4.w};
                 uint32_t live = (bits >> (4 * quad)) & 0xFu;
                 const uint32_t need = live & ~(bits >> (16 + 4 * quad));
-                mbar_wait(s_full, s_cnt & 1);
+                FWAIT(0, s_full, s_cnt & 1);
                 ++s_cnt;
                 tc_fence_after();
                 if (store_leader) TRACE(2 + g, 2);
@@ -1256,7 +1274,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 }
                 if (s_cnt > 1) {
                     // PV of this group's previous entry: complete before O is rescaled or P rewritten
-                    mbar_wait(pv_done, (s_cnt - 2) & 1);
+                    FWAIT(1, pv_done, (s_cnt - 2) & 1);
                     tc_fence_after();
                 }
                 if (store_leader) TRACE(2 + g, 14);
@@ -1300,6 +1318,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
+#ifdef SPLAT_FUSED_PROF
+    if (blockIdx.x == 0 && lane == 0) g_fprof[warp][15] = clock64() - t_start;
+#endif
     // the last CTA to finish resets the work counter for the next launch on this handle (every
     // grab of every CTA happened before its increment of the done counter)
     if (threadIdx.x == 0) {
@@ -1409,6 +1430,14 @@ extern "C" int splat_debug_hang(unsigned long long *out)
     (void)out;
     return 0;
 #endif
+}
+
+extern "C" int splat_debug_fused_prof(unsigned long long *out)
+{
+    cudaMemcpyFromSymbol(out, g_fprof, sizeof(g_fprof));
+    static const unsigned long long z[12 * 16] = {};
+    cudaMemcpyToSymbol(g_fprof, z, sizeof(z));
+    return 0;
 }
 
 extern "C" int splat_debug_trace(unsigned long long *out, int *counts)
