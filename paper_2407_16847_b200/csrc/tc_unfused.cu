@@ -189,6 +189,9 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevAcsr &A = prm.A;
     const int n_units = A.n_qt * prm.BH;
+#ifdef SPLAT_UNF_PROF
+    const unsigned long long t_start = clock64();
+#endif
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::QS; ++i) { mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); }
@@ -209,7 +212,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
             unit_tile(A, u, bh, t);
-            if (qc >= C::QS) mbar_wait(&q_empty[qi], qph ^ 1);
+            if (qc >= C::QS) PWAIT(0, &q_empty[qi], qph ^ 1);
             if (lane == 0) {
                 mbar_expect_tx(&q_full[qi], C::kTileBytes);
 #pragma unroll
@@ -220,7 +223,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             if (++qi == C::QS) { qi = 0; qph ^= 1; }
             for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
                 const int kv = A.kv[e] & kKvMask;
-                if (kc >= C::KS) mbar_wait(&k_empty[ki], kph ^ 1);
+                if (kc >= C::KS) PWAIT(1, &k_empty[ki], kph ^ 1);
                 if (lane == 0) {
                     mbar_expect_tx(&k_full[ki], C::kTileBytes);
 #pragma unroll
@@ -241,12 +244,12 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
             unit_tile(A, u, bh, t);
-            mbar_wait(&q_full[qi], qph);
+            PWAIT(2, &q_full[qi], qph);
             const uint32_t qb = sQ + qi * C::kTileBytes;
             for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
                 const int sb = ns % kNWG;
-                mbar_wait(&k_full[ki], kph);
-                if (ns >= kNWG) mbar_wait(&s_empty[sb], ((ns / kNWG) - 1) & 1);
+                PWAIT(3, &k_full[ki], kph);
+                if (ns >= kNWG) PWAIT(4, &s_empty[sb], ((ns / kNWG) - 1) & 1);
                 tc_fence_after();
                 const uint32_t kb = sK + ki * C::kTileBytes;
                 if (lane == 0) {
@@ -314,7 +317,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 dst[2] = make_int2(rel + p2, (int)m4.z);
                 dst[3] = make_int2(rel + p3, (int)m4.w);
                 wg_sync(1 + eg);
-                mbar_wait(&s_full[eg], k & 1);
+                PWAIT(5, &s_full[eg], k & 1);
                 tc_fence_after();
                 float *const base = Sg + tbase[tb];
 #pragma unroll 1
@@ -338,6 +341,9 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             }
         }
     }
+#ifdef SPLAT_UNF_PROF
+    if (blockIdx.x == 0 && lane == 0) g_unf_prof[warp][7] = clock64() - t_start;
+#endif
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
