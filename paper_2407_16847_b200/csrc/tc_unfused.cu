@@ -334,7 +334,8 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     for (int j = 0; j < 32; ++j) {
                         const int2 q = tq[(tb * 128 + 32 * c + j) * 4 + quad];
                         const uint32_t mw = (uint32_t)q.y;
-                        st_pred_f32(base + q.x + __popc(mw & below), scale * v[j], (mw >> lane) & 1u);
+                        // unsigned 32-bit element offset from the tile base (no sign extension)
+                        st_pred_f32(base + ((uint32_t)q.x + (uint32_t)__popc(mw & below)), scale * v[j], (mw >> lane) & 1u);
                     }
                 }
                 ++k;
