@@ -278,7 +278,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         int2 *tq = reinterpret_cast<int2 *>(smem + C::OFF_TQ) + eg * 2 * 128 * 4;
         long long *tbase = reinterpret_cast<long long *>(smem + C::OFF_TBASE) + eg * 2;
-        const uint32_t below = (1u << lane) - 1u;
+        const uint32_t below = (1u << lane) - 1u, lanebit = 1u << lane;
         float *const Sg = prm.S;
         const float scale = prm.scale;
         uint32_t i = 0, k = 0;   // i: CTA tile counter, k: this group's tile counter
@@ -319,7 +319,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 wg_sync(1 + eg);
                 PWAIT(5, &s_full[eg], k & 1);
                 tc_fence_after();
-                float *const base = Sg + tbase[tb];
+                const unsigned long long baddr = reinterpret_cast<unsigned long long>(Sg + tbase[tb]);
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     float v[32];
@@ -334,8 +334,9 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                     for (int j = 0; j < 32; ++j) {
                         const int2 q = tq[(tb * 128 + 32 * c + j) * 4 + quad];
                         const uint32_t mw = (uint32_t)q.y;
-                        // unsigned 32-bit element offset from the tile base (no sign extension)
-                        st_pred_f32(base + ((uint32_t)q.x + (uint32_t)__popc(mw & below)), scale * v[j], (mw >> lane) & 1u);
+                        // unsigned 32-bit element offset from the tile base: one IMAD.WIDE.U32 per address
+                        const uint32_t eo = (uint32_t)q.x + (uint32_t)__popc(mw & below);
+                        st_pred_f32(reinterpret_cast<float *>(baddr + (unsigned long long)eo * 4ull), scale * v[j], mw & lanebit);
                     }
                 }
                 ++k;
