@@ -324,7 +324,11 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 {
     using C = Cfg<D>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // No static shared memory precedes the dynamic buffer, so it starts 1024-byte aligned (checked;
+    // the launch still reserves 1 KB of slack).  Using smem_raw itself -- not an integer align-up --
+    // keeps the shared state space visible to the compiler (LDS/STS, constant offsets).
+    uint8_t *smem = smem_raw;
+    if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0u) __trap();
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
     uint64_t *q_full = bars;                     // [2][QS]
     uint64_t *q_empty = q_full + 2 * C::QS;      // [2][QS]
@@ -901,7 +905,11 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     using C = SCfg;
     constexpr int D = 64;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // No static shared memory precedes the dynamic buffer, so it starts 1024-byte aligned (checked;
+    // the launch still reserves 1 KB of slack).  Using smem_raw itself -- not an integer align-up --
+    // keeps the shared state space visible to the compiler (LDS/STS, constant offsets).
+    uint8_t *smem = smem_raw;
+    if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0u) __trap();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // group of this warp: producers 0 / 3, MMA 1 / 2, softmax 4-7 / 8-11
     const int g = warp >= 4 ? (warp - 4) >> 2 : (warp == 0 || warp == 1 ? 0 : 1);
