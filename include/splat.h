@@ -246,6 +246,61 @@ splat_status splat_sparse_mhsa_host(splat_acsr a, const void *Qh, const void *Kh
                                     splat_dtype dt, int32_t B, int32_t H, int32_t d, float scale,
                                     void *Oh, void *dQ, void *dK, void *dV, void *dO, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Thread-block tiling analysis of the R-SDDMM point set (
+ * paper Sec. 7.2-7.3, App. A-C).  Host-only: no device,
+ * no stream, synchronous, thread-safe (no shared state).
+ *
+ * P = {(x, y) : query row y attends key column x} of the descriptor's mask.
+ * A thread block of m x n threads with anchor (x, y) and stretch s computes
+ * Comp = {(x + c s, y + r s) : r < m, c < n} -- m thread ROWS (y extent), n
+ * thread COLUMNS (x extent), reading T-1 -- and covers Comp ∩ P
+ * (Def. 2).  Every arrangement here uses one stretch for all of
+ * its blocks.
+ *
+ *   splat_poset_tile   poset tiling (Def. 5, Alg. 1):
+ *                      each iteration anchors one block at every minimal
+ *                      uncovered point (the set ⊤), until P is covered.
+ *                      stretch > 0 forces s; stretch == 0 selects it
+ *                      (Sec. 7.3.1): 1 for polygonal masks (every
+ *                      row contiguous, App. A), the cheapest divisor of the
+ *                      row stride X for strided masks (App. B), else the
+ *                      cheapest s in [1, min(N, 64)]; ties -> fewer blocks.
+ *   splat_naive_tile   App. C Def. 8: m-row patches from row
+ *                      0, each tiled left to right with unit-stretch blocks
+ *                      from its leftmost to its rightmost non-zero column.
+ *   splat_tiling_cost_eval  the cost report of a caller-given arrangement.
+ *
+ *   anchors  host int32 [cap][2] = (x, y) per block in placement order (Alg. 1:
+ *            iteration, then ascending y); the first min(cap, lambda) are
+ *            written; may be NULL when cap == 0 (cost->lambda gives the size).
+ *   cost     required: lambda, |P|, phi_TD = |(∪ Comp) \ P| (Comp points
+ *            outside the N x N mask count), phi_R = lambda m n - |P| - phi_TD,
+ *            phi_RU = |P| / (lambda m n), phi_CMR = mean of 1/Str = 1/s
+ *            (Def. 3), cost = lambda / phi_CMR (Def. 4).
+ * Errors: INVALID_ARG (null pointers, m or n outside [1, 4096], stretch
+ * outside [0 (poset) or 1 (eval), N], negative anchors, or -- eval only -- an
+ * arrangement whose covers miss a point of P, named in splat_last_error),
+ * UNSUPPORTED (seq_len > 8192: the analysis keeps P as an N x N bitset).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int64_t lambda;     /* number of thread blocks */
+    int64_t points;     /* |P| */
+    int64_t phi_td;     /* collective thread divergence */
+    int64_t phi_r;      /* redundant compute */
+    double phi_ru;      /* reuse */
+    double phi_cmr;     /* coalesced memory requests */
+    double cost;        /* lambda / phi_cmr */
+    int32_t stretch, m, n, reserved;
+} splat_tiling_cost;
+
+splat_status splat_poset_tile(const splat_pattern *p, int32_t m, int32_t n, int32_t stretch,
+                              int32_t *anchors, int64_t cap, splat_tiling_cost *cost);
+splat_status splat_naive_tile(const splat_pattern *p, int32_t m, int32_t n, int32_t *anchors,
+                              int64_t cap, splat_tiling_cost *cost);
+splat_status splat_tiling_cost_eval(const splat_pattern *p, int32_t m, int32_t n, int32_t stretch,
+                                    const int32_t *anchors, int64_t n_blocks, splat_tiling_cost *cost);
+
 /* Algorithmic FLOPs of one fused call: 4 * nnz * d * B * H (QK^T and PV at
  * 2*nnz*d each; the softmax is not counted; SURVEY reading A-14). */
 double splat_flops(splat_acsr a, int32_t B, int32_t H, int32_t d);

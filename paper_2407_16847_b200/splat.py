@@ -25,14 +25,25 @@ KINDS = {"window": 0, "blocked": 1, "strided": 2, "dilated": 3, "global_local": 
 # every symbol include/splat.h declares (tests check the library exports them all)
 EXPORTS = ("splat_acsr_build", "splat_acsr_info", "splat_acsr_copy_meta", "splat_plan_info",
            "splat_plan_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
-           "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_flops", "splat_last_launch_count",
-           "splat_last_error")
+           "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_poset_tile", "splat_naive_tile",
+           "splat_tiling_cost_eval", "splat_flops", "splat_last_launch_count", "splat_last_error")
 
 
 class SplatError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+class splat_tiling_cost(C.Structure):
+    _fields_ = [("lambda_", C.c_int64), ("points", C.c_int64), ("phi_td", C.c_int64), ("phi_r", C.c_int64),
+                ("phi_ru", C.c_double), ("phi_cmr", C.c_double), ("cost", C.c_double), ("stretch", C.c_int32),
+                ("m", C.c_int32), ("n", C.c_int32), ("reserved", C.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {"lambda": self.lambda_, "points": self.points, "phi_td": self.phi_td, "phi_r": self.phi_r,
+                "phi_ru": self.phi_ru, "phi_cmr": self.phi_cmr, "cost": self.cost, "stretch": self.stretch,
+                "m": self.m, "n": self.n}
 
 
 class splat_pattern(C.Structure):
@@ -65,6 +76,9 @@ def lib():
         L.splat_sparse_mhsa.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp]
         L.splat_sparse_mhsa_host.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp, vp, vp, vp,
                                              vp]
+        L.splat_poset_tile.argtypes = [P(splat_pattern), i32, i32, i32, vp, i64, P(splat_tiling_cost)]
+        L.splat_naive_tile.argtypes = [P(splat_pattern), i32, i32, vp, i64, P(splat_tiling_cost)]
+        L.splat_tiling_cost_eval.argtypes = [P(splat_pattern), i32, i32, i32, vp, i64, P(splat_tiling_cost)]
         L.splat_flops.argtypes = [vp, i32, i32, i32]
         L.splat_flops.restype = C.c_double
         L.splat_last_launch_count.restype = i32
@@ -219,6 +233,35 @@ def splat_sparse_mhsa_host(a: Acsr, Qh, Kh, Vh, Oh, scale: float, dQ, dK, dV, dO
                                         scale, Oh.data_ptr(), dQ.data_ptr(), dK.data_ptr(), dV.data_ptr(),
                                         dO.data_ptr(), C.c_void_p(_stream(stream))))
     return Oh
+
+
+def _tiling(fn, pattern, m: int, n: int, *pre):
+    cost = splat_tiling_cost()
+    pat = to_c_pattern(pattern)
+    _check(fn(C.byref(pat), m, n, *pre, None, 0, C.byref(cost)))
+    anchors = torch.zeros((max(cost.lambda_, 1), 2), dtype=torch.int32)
+    _check(fn(C.byref(pat), m, n, *pre, anchors.data_ptr(), cost.lambda_, C.byref(cost)))
+    return anchors[:cost.lambda_], cost.as_dict()
+
+
+def splat_poset_tile(pattern, m: int, n: int, stretch: int = 0):
+    """Poset tiling (Alg. 1) of the pattern's point set: (anchors [lambda,2] int32 (x, y), cost dict).
+    Host-only analysis; stretch 0 = Sec. 7.3.1 selection."""
+    return _tiling(lib().splat_poset_tile, pattern, m, n, stretch)
+
+
+def splat_naive_tile(pattern, m: int, n: int):
+    """App. C naive tiling: (anchors [lambda,2] int32 (x, y), cost dict)."""
+    return _tiling(lib().splat_naive_tile, pattern, m, n)
+
+
+def splat_tiling_cost_eval(pattern, m: int, n: int, stretch: int, anchors) -> dict:
+    """Def. 3/4 cost report of a given uniform-stretch arrangement (anchors: [k,2] (x, y))."""
+    a = torch.as_tensor(anchors, dtype=torch.int32).reshape(-1, 2).contiguous()
+    cost = splat_tiling_cost()
+    _check(lib().splat_tiling_cost_eval(C.byref(to_c_pattern(pattern)), m, n, stretch, a.data_ptr(), a.shape[0],
+                                        C.byref(cost)))
+    return cost.as_dict()
 
 
 def last_launch_count() -> int:
