@@ -301,6 +301,37 @@ splat_status splat_naive_tile(const splat_pattern *p, int32_t m, int32_t n, int3
 splat_status splat_tiling_cost_eval(const splat_pattern *p, int32_t m, int32_t n, int32_t stretch,
                                     const int32_t *anchors, int64_t n_blocks, splat_tiling_cost *cost);
 
+/* ---------------------------------------------------------------------------
+ * splat_acsr_from_mask -- ACSR build from an EXPLICIT bit mask (SURVEY §8(f)
+ * NEXT #2): the paper's analysis pass as written, checkRegularity(Mask) +
+ * generateACSRMetadata(Mask) (Listing 4, Sec. 5.1).
+ *
+ * Each row's non-zero columns are split into canonical greedy runs (reading
+ * R-4: 2x2 solve on the first two unconsumed columns, extended while
+ * the next column passes P:219, restarted at the first failing column) by a
+ * GPU kernel, one warp per row; then row_ptr is scanned and the tile plan is
+ * built exactly as for splat_acsr_build.  The handle works with every compute
+ * call (no strided-row decomposition: there is no descriptor).
+ *
+ *   mask      n rows of ceil(n/32) uint32 words, row-major, column j of row i
+ *             at bit (j % 32) of word i * ceil(n/32) + j / 32 (LSB first);
+ *             bits >= n in a row's last word are ignored.  A DEVICE pointer
+ *             on `device` (read only during the call), or a HOST pointer when
+ *             device == -1 (inspection handle, computed on the host).
+ *   n         1 <= n <= 131072 (the mask is n^2/8 bytes)
+ *   max_runs  1..SPLAT_MAX_SEGS: 1 is Def. 1's regularity; 4
+ *             admits the multi-run rows of reading R-3
+ *   out       receives the handle (caller owns it; free with _destroy)
+ *   bad_row, bad_col  (may be NULL) -1, or on NOT_REGULAR the first offending
+ *             point in row-major order: the first row needing more than
+ *             max_runs runs and the column that would start run max_runs+1
+ *             (for max_runs = 1 the first column breaking the
+ *             row's affine fit, e.g. column 5 of {0, 2, 4, 5}).
+ * Synchronous.  Errors: INVALID_ARG, NOT_REGULAR (no handle), OOM, CUDA.
+ * ------------------------------------------------------------------------- */
+splat_status splat_acsr_from_mask(const uint32_t *mask, int32_t n, int32_t max_runs, int device, void *stream,
+                                  splat_acsr *out, int32_t *bad_row, int32_t *bad_col);
+
 /* Algorithmic FLOPs of one fused call: 4 * nnz * d * B * H (QK^T and PV at
  * 2*nnz*d each; the softmax is not counted; SURVEY reading A-14). */
 double splat_flops(splat_acsr a, int32_t B, int32_t H, int32_t d);

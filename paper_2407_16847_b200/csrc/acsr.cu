@@ -10,6 +10,7 @@
 // ~2 MB (Mistral N = 32768: 2.1 MB): the build is latency-bound.
 #include <cuda_runtime.h>
 
+#include "kernels.h"
 #include "splat_internal.h"
 
 namespace splat {
@@ -41,41 +42,62 @@ __global__ void acsr_rows_kernel(splat_pattern p, int4 *__restrict__ seg, uint8_
     if (i == 0) row_ptr[0] = 0;
 }
 
-// In-place inclusive scan of row_ptr[1..N] with one 1024-thread CTA: each
-// thread scans a contiguous chunk, the chunk totals are scanned with warp
-// shuffles, then each chunk adds its prefix.  Exact int64 arithmetic.
+// In-place inclusive scan of row_ptr[1..N] with one 1024-thread CTA, in tiles of 8192 counts:
+// thread t owns 8 consecutive counts of a tile, scans them, and the 1024 thread totals are
+// scanned with warp shuffles; a running carry joins the tiles, and the next tile's loads are
+// issued before the current tile is scanned.  Exact int64 arithmetic.
 __global__ void __launch_bounds__(1024) acsr_scan_kernel(int64_t *__restrict__ row_ptr, int n)
 {
+    constexpr int PER = 8, TILE = 1024 * PER;
     __shared__ int64_t warp_tot[32];
-    const int t = threadIdx.x, nt = blockDim.x;
-    const int chunk = (n + nt - 1) / nt;
-    const int b = 1 + t * chunk, e = min(n + 1, b + chunk);
-    int64_t sum = 0;
-    for (int i = b; i < e; ++i) sum += row_ptr[i];
-    // exclusive scan of per-thread sums
-    int64_t x = sum;
-    const int lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    int64_t *x = row_ptr + 1;   // x[0..n-1] = counts of rows 0..n-1
+    int64_t carry = 0;
+    int64_t cur[PER], nxt[PER];
+    auto load = [&](int base, int64_t (&v)[PER]) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) warp_tot[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        int64_t v = lane < (nt >> 5) ? warp_tot[lane] : 0;
+        for (int k = 0; k < PER; ++k) {
+            const int i = base + t * PER + k;
+            v[k] = i < n ? x[i] : 0;
+        }
+    };
+    load(0, cur);
+    for (int base = 0; base < n; base += TILE) {
+        if (base + TILE < n) load(base + TILE, nxt);
+        int64_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            sum += cur[k];
+            cur[k] = sum;
+        }
+        int64_t inc = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int64_t y = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += y;
+            const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
         }
-        warp_tot[lane] = v;   // inclusive over warps
-    }
-    __syncthreads();
-    int64_t prefix = x - sum + (w > 0 ? warp_tot[w - 1] : 0);
-    for (int i = b; i < e; ++i) {
-        prefix += row_ptr[i];
-        row_ptr[i] = prefix;
+        if (lane == 31) warp_tot[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            int64_t v = warp_tot[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += y;
+            }
+            warp_tot[lane] = v;   // inclusive over warps
+        }
+        __syncthreads();
+        const int64_t prefix = carry + inc - sum + (w > 0 ? warp_tot[w - 1] : 0);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = base + t * PER + k;
+            if (i < n) x[i] = prefix + cur[k];
+        }
+        carry += warp_tot[31];
+        __syncthreads();      // warp_tot is rewritten by the next tile
+#pragma unroll
+        for (int k = 0; k < PER; ++k) cur[k] = nxt[k];
     }
 }
 
@@ -84,6 +106,11 @@ cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, 
 {
     const int n = p.seq_len;
     acsr_rows_kernel<<<(n + 255) / 256, 256, 0, st>>>(p, seg, nseg, row_ptr);
+    return launch_acsr_scan(row_ptr, n, st);
+}
+
+cudaError_t launch_acsr_scan(int64_t *row_ptr, int n, cudaStream_t st)
+{
     acsr_scan_kernel<<<1, 1024, 0, st>>>(row_ptr, n);
     return cudaGetLastError();
 }

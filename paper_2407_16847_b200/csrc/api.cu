@@ -213,63 +213,13 @@ using namespace splat;
 
 namespace {
 
-// The whole handle build (metadata + plan, device copies); `internal` patterns (the residue
-// decomposition's sub-patterns) skip the public descriptor validation.
-splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_acsr *out, bool internal)
+// Device metadata is in a->d_seg / d_nseg / d_row_ptr (queued on cs): copy it to the host,
+// build the tile plan and upload it.  Frees `a` on failure.
+splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *out)
 {
-    clear_error();
-    if (!p || !out) return set_error(SPLAT_ERR_INVALID_ARG, "null pattern or out pointer");
-    *out = nullptr;
-    splat_status st = internal ? SPLAT_OK : validate_pattern(*p);
-    if (st != SPLAT_OK) return st;
-    splat_acsr_s *a = new (std::nothrow) splat_acsr_s();
-    if (!a) return set_error(SPLAT_ERR_OOM, "host allocation failed");
-    a->pat = *p;
-    a->n = p->seq_len;
     const int N = a->n;
-    a->seg_h.assign((size_t)N * 16, 0);
-    a->nseg_h.assign(N, 0);
-    a->row_ptr_h.assign((size_t)N + 1, 0);
-    if (device < 0) {
-        // host INSPECTION handle: same closed form, evaluated on the host
-        for (int i = 0; i < N; ++i) {
-            Seg s[4];
-            const int n = row_segments(*p, i, s);
-            int off = 0;
-            for (int k = 0; k < n; ++k) {
-                int32_t *g = &a->seg_h[(size_t)i * 16 + 4 * k];
-                g[0] = s[k].start; g[1] = s[k].step; g[2] = s[k].count; g[3] = off;
-                off += s[k].count;
-            }
-            for (int k = n; k < 4; ++k) a->seg_h[(size_t)i * 16 + 4 * k + 3] = off;
-            a->nseg_h[i] = (uint8_t)n;
-            a->row_ptr_h[i + 1] = a->row_ptr_h[i] + off;
-        }
-        finish_host_meta(a);
-        build_plan(*a);
-        *out = a;
-        return SPLAT_OK;
-    }
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
-        delete a;
-        cudaGetLastError();
-        return set_error(SPLAT_ERR_INVALID_ARG, "device %d not available (%d devices)", device, ndev);
-    }
-    a->device = device;
-    DeviceGuard g(device);
-    cudaStream_t cs = (cudaStream_t)stream;
-    cudaError_t e;
-    if ((e = cudaMalloc(&a->d_seg, sizeof(int32_t) * 16 * (size_t)N)) != cudaSuccess ||
-        (e = cudaMalloc(&a->d_nseg, (size_t)N)) != cudaSuccess ||
-        (e = cudaMalloc(&a->d_row_ptr, sizeof(int64_t) * ((size_t)N + 1))) != cudaSuccess) {
-        free_device(a);
-        delete a;
-        return cuda_fail(e, "acsr allocation");
-    }
-    e = launch_acsr_build(*p, reinterpret_cast<int4 *>(a->d_seg), a->d_nseg, a->d_row_ptr, cs);
-    if (e == cudaSuccess)
-        e = cudaMemcpyAsync(a->seg_h.data(), a->d_seg, sizeof(int32_t) * 16 * (size_t)N, cudaMemcpyDeviceToHost, cs);
+    cudaError_t e = cudaMemcpyAsync(a->seg_h.data(), a->d_seg, sizeof(int32_t) * 16 * (size_t)N,
+                                    cudaMemcpyDeviceToHost, cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(a->nseg_h.data(), a->d_nseg, (size_t)N, cudaMemcpyDeviceToHost, cs);
     if (e == cudaSuccess)
@@ -326,6 +276,112 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
     return SPLAT_OK;
 }
 
+// Host INSPECTION variant of the mask ingest (mask_ingest.cu): the same greedy runs, column by
+// column.  Returns false with the first offending column if row i needs more than max_runs runs.
+bool host_mask_row(const uint32_t *row, int N, int max_runs, int32_t *seg, uint8_t *nseg, int64_t *cnt,
+                   int32_t *bad_col)
+{
+    auto bit = [&](int x) { return (row[x >> 5] >> (x & 31)) & 1u; };
+    int nr = 0, off = 0, x = 0;
+    while (true) {
+        while (x < N && !bit(x)) ++x;
+        if (x >= N) break;
+        if (nr == max_runs) {
+            *bad_col = x;
+            return false;
+        }
+        int c0 = x, step = 1, n = 1;
+        int c1 = c0 + 1;
+        while (c1 < N && !bit(c1)) ++c1;
+        if (c1 < N) {
+            step = c1 - c0;
+            n = 2;
+            int last = c1;
+            while (true) {
+                int nx = last + 1;
+                while (nx < N && !bit(nx)) ++nx;
+                if (nx >= N || nx - last != step) break;
+                last = nx;
+                ++n;
+            }
+            x = last + 1;
+        } else {
+            x = N;
+        }
+        int32_t *g = seg + 4 * nr;
+        g[0] = c0; g[1] = step; g[2] = n; g[3] = off;
+        off += n;
+        ++nr;
+    }
+    for (int k = nr; k < 4; ++k) seg[4 * k + 3] = off;
+    *nseg = (uint8_t)nr;
+    *cnt = off;
+    return true;
+}
+
+// The whole handle build (metadata + plan, device copies); `internal` patterns (the residue
+// decomposition's sub-patterns) skip the public descriptor validation.
+splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_acsr *out, bool internal)
+{
+    clear_error();
+    if (!p || !out) return set_error(SPLAT_ERR_INVALID_ARG, "null pattern or out pointer");
+    *out = nullptr;
+    splat_status st = internal ? SPLAT_OK : validate_pattern(*p);
+    if (st != SPLAT_OK) return st;
+    splat_acsr_s *a = new (std::nothrow) splat_acsr_s();
+    if (!a) return set_error(SPLAT_ERR_OOM, "host allocation failed");
+    a->pat = *p;
+    a->n = p->seq_len;
+    const int N = a->n;
+    a->seg_h.assign((size_t)N * 16, 0);
+    a->nseg_h.assign(N, 0);
+    a->row_ptr_h.assign((size_t)N + 1, 0);
+    if (device < 0) {
+        // host INSPECTION handle: same closed form, evaluated on the host
+        for (int i = 0; i < N; ++i) {
+            Seg s[4];
+            const int n = row_segments(*p, i, s);
+            int off = 0;
+            for (int k = 0; k < n; ++k) {
+                int32_t *g = &a->seg_h[(size_t)i * 16 + 4 * k];
+                g[0] = s[k].start; g[1] = s[k].step; g[2] = s[k].count; g[3] = off;
+                off += s[k].count;
+            }
+            for (int k = n; k < 4; ++k) a->seg_h[(size_t)i * 16 + 4 * k + 3] = off;
+            a->nseg_h[i] = (uint8_t)n;
+            a->row_ptr_h[i + 1] = a->row_ptr_h[i] + off;
+        }
+        finish_host_meta(a);
+        build_plan(*a);
+        *out = a;
+        return SPLAT_OK;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
+        delete a;
+        cudaGetLastError();
+        return set_error(SPLAT_ERR_INVALID_ARG, "device %d not available (%d devices)", device, ndev);
+    }
+    a->device = device;
+    DeviceGuard g(device);
+    cudaStream_t cs = (cudaStream_t)stream;
+    cudaError_t e;
+    if ((e = cudaMalloc(&a->d_seg, sizeof(int32_t) * 16 * (size_t)N)) != cudaSuccess ||
+        (e = cudaMalloc(&a->d_nseg, (size_t)N)) != cudaSuccess ||
+        (e = cudaMalloc(&a->d_row_ptr, sizeof(int64_t) * ((size_t)N + 1))) != cudaSuccess) {
+        free_device(a);
+        delete a;
+        return cuda_fail(e, "acsr allocation");
+    }
+    e = launch_acsr_build(*p, reinterpret_cast<int4 *>(a->d_seg), a->d_nseg, a->d_row_ptr, cs);
+    if (e != cudaSuccess) {
+        free_device(a);
+        delete a;
+        return cuda_fail(e, "acsr build");
+    }
+    return finish_device_build(a, cs, out);
+}
+
 // Residue decomposition of STRIDED_LOCAL(l) (see splat_acsr_s::sub_band): applicable when the
 // residue classes tile the sequence exactly (N % l == 0) and whole classes fill a 128-row tile
 // (nk = N / l divides 128, nk >= 2).
@@ -369,6 +425,88 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
     splat_status st = build_impl(p, device, stream, out, false);
     if (st == SPLAT_OK) build_residue_split(*out, stream);
     return st;
+}
+
+splat_status splat_acsr_from_mask(const uint32_t *mask, int32_t n, int32_t max_runs, int device, void *stream,
+                                  splat_acsr *out, int32_t *bad_row, int32_t *bad_col)
+{
+    clear_error();
+    if (bad_row) *bad_row = -1;
+    if (bad_col) *bad_col = -1;
+    if (!mask || !out) return set_error(SPLAT_ERR_INVALID_ARG, "null mask or out pointer");
+    *out = nullptr;
+    if (n < 1 || n > kMaxMaskN) return set_error(SPLAT_ERR_INVALID_ARG, "n = %d outside [1, %d]", n, kMaxMaskN);
+    if (max_runs < 1 || max_runs > SPLAT_MAX_SEGS)
+        return set_error(SPLAT_ERR_INVALID_ARG, "max_runs = %d outside [1, %d]", max_runs, SPLAT_MAX_SEGS);
+    splat_acsr_s *a = new (std::nothrow) splat_acsr_s();
+    if (!a) return set_error(SPLAT_ERR_OOM, "host allocation failed");
+    a->pat = splat_pattern{};
+    a->pat.kind = kKindMask;
+    a->pat.seq_len = n;
+    a->n = n;
+    a->seg_h.assign((size_t)n * 16, 0);
+    a->nseg_h.assign(n, 0);
+    a->row_ptr_h.assign((size_t)n + 1, 0);
+    auto not_regular = [&](long long r, long long c) {
+        if (bad_row) *bad_row = (int32_t)r;
+        if (bad_col) *bad_col = (int32_t)c;
+        return set_error(SPLAT_ERR_NOT_REGULAR, "row %lld needs more than %d affine runs (column %lld)", r,
+                         max_runs, c);
+    };
+    const int W = (n + 31) / 32;
+    if (device < 0) {
+        for (int i = 0; i < n; ++i) {
+            int64_t cnt = 0;
+            int32_t bc = -1;
+            if (!host_mask_row(mask + (size_t)i * W, n, max_runs, &a->seg_h[(size_t)i * 16], &a->nseg_h[i], &cnt,
+                               &bc)) {
+                delete a;
+                return not_regular(i, bc);
+            }
+            a->row_ptr_h[i + 1] = a->row_ptr_h[i] + cnt;
+        }
+        finish_host_meta(a);
+        build_plan(*a);
+        *out = a;
+        return SPLAT_OK;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
+        delete a;
+        cudaGetLastError();
+        return set_error(SPLAT_ERR_INVALID_ARG, "device %d not available (%d devices)", device, ndev);
+    }
+    a->device = device;
+    DeviceGuard g(device);
+    cudaStream_t cs = (cudaStream_t)stream;
+    cudaError_t e;
+    unsigned long long *d_bad = nullptr, bad = 0;
+    if ((e = cudaMalloc(&a->d_seg, sizeof(int32_t) * 16 * (size_t)n)) != cudaSuccess ||
+        (e = cudaMalloc(&a->d_nseg, (size_t)n)) != cudaSuccess ||
+        (e = cudaMalloc(&a->d_row_ptr, sizeof(int64_t) * ((size_t)n + 1))) != cudaSuccess ||
+        (e = cudaMalloc(&d_bad, sizeof(unsigned long long))) != cudaSuccess) {
+        cudaFree(d_bad);
+        free_device(a);
+        delete a;
+        return cuda_fail(e, "acsr allocation");
+    }
+    e = launch_acsr_from_mask(mask, n, max_runs, reinterpret_cast<int4 *>(a->d_seg), a->d_nseg, a->d_row_ptr,
+                              d_bad, cs);
+    note_launches(2);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    cudaFree(d_bad);
+    if (e != cudaSuccess) {
+        free_device(a);
+        delete a;
+        return cuda_fail(e, "mask ingest");
+    }
+    if (bad != ~0ull) {
+        free_device(a);
+        delete a;
+        return not_regular((long long)(bad >> 32), (long long)(bad & 0xffffffffull));
+    }
+    return finish_device_build(a, cs, out);
 }
 
 splat_status splat_acsr_info(splat_acsr a, int32_t *n, int64_t *nnz, int32_t *max_segs, double *density)

@@ -36,6 +36,11 @@ struct DevAcsr {
 
 cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, int64_t *row_ptr,
                               cudaStream_t st);
+cudaError_t launch_acsr_scan(int64_t *row_ptr, int n, cudaStream_t st);
+// explicit bit mask (row stride ceil(n/32) words, LSB first) -> greedy runs; *bad = min over
+// irregular rows of (row << 32 | first column of run max_runs + 1), all ones if none
+cudaError_t launch_acsr_from_mask(const uint32_t *mask, int n, int max_runs, int4 *seg, uint8_t *nseg,
+                                  int64_t *row_ptr, unsigned long long *bad, cudaStream_t st);
 
 // SIMT kernels (fp32 path; any d <= 256)
 cudaError_t launch_rsddmm_simt(const DevAcsr &A, const void *Q, const void *K, bool bf16, int BH, int d,

@@ -30,6 +30,9 @@ struct Seg {
 // r = rho * nk + k is natural row rho + l k, and it attends permuted keys rho * nk + m, m < k
 // (natural keys j = rho + l m = i - l (k - m)): one affine run (rho nk, 1, k) per row.
 constexpr int32_t kKindResiduePrev = 100;
+// handles built from an explicit bit mask (splat_acsr_from_mask): no descriptor, metadata only
+constexpr int32_t kKindMask = 101;
+constexpr int32_t kMaxMaskN = 1 << 17;
 
 SPLAT_HD int imin(int a, int b) { return a < b ? a : b; }
 SPLAT_HD int imax(int a, int b) { return a > b ? a : b; }

@@ -25,7 +25,7 @@ KINDS = {"window": 0, "blocked": 1, "strided": 2, "dilated": 3, "global_local": 
 # every symbol include/splat.h declares (tests check the library exports them all)
 EXPORTS = ("splat_acsr_build", "splat_acsr_info", "splat_acsr_copy_meta", "splat_plan_info",
            "splat_plan_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
-           "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_poset_tile", "splat_naive_tile",
+           "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_acsr_from_mask", "splat_poset_tile", "splat_naive_tile",
            "splat_tiling_cost_eval", "splat_flops", "splat_last_launch_count", "splat_last_error")
 
 
@@ -76,6 +76,7 @@ def lib():
         L.splat_sparse_mhsa.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp]
         L.splat_sparse_mhsa_host.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp, vp, vp, vp,
                                              vp]
+        L.splat_acsr_from_mask.argtypes = [vp, i32, i32, C.c_int, vp, P(vp), P(i32), P(i32)]
         L.splat_poset_tile.argtypes = [P(splat_pattern), i32, i32, i32, vp, i64, P(splat_tiling_cost)]
         L.splat_naive_tile.argtypes = [P(splat_pattern), i32, i32, vp, i64, P(splat_tiling_cost)]
         L.splat_tiling_cost_eval.argtypes = [P(splat_pattern), i32, i32, i32, vp, i64, P(splat_tiling_cost)]
@@ -116,14 +117,17 @@ def _dt(t: torch.Tensor) -> int:
 
 
 class Acsr:
-    """Owning wrapper of a ``splat_acsr`` handle (splat_acsr_build / _destroy)."""
+    """Owning wrapper of a ``splat_acsr`` handle (splat_acsr_build / _from_mask / _destroy)."""
 
-    def __init__(self, pattern, device: int = 0, stream=None):
+    def __init__(self, pattern, device: int = 0, stream=None, _handle=None):
         self.pattern = pattern
         self.device = device
         h = C.c_void_p()
-        st = 0 if device < 0 else _stream(stream) if torch.cuda.is_available() else 0
-        _check(lib().splat_acsr_build(C.byref(to_c_pattern(pattern)), device, C.c_void_p(st), C.byref(h)))
+        if _handle is not None:
+            h = _handle
+        else:
+            st = 0 if device < 0 else _stream(stream) if torch.cuda.is_available() else 0
+            _check(lib().splat_acsr_build(C.byref(to_c_pattern(pattern)), device, C.c_void_p(st), C.byref(h)))
         self.handle = h
         n, nnz, ms, dens = C.c_int32(), C.c_int64(), C.c_int32(), C.c_double()
         _check(lib().splat_acsr_info(h, C.byref(n), C.byref(nnz), C.byref(ms), C.byref(dens)))
@@ -167,6 +171,42 @@ class Acsr:
 
 def splat_acsr_build(pattern, device: int = 0, stream=None) -> Acsr:
     return Acsr(pattern, device, stream)
+
+
+class NotRegular(SplatError):
+    def __init__(self, status: int, msg: str, row: int, col: int):
+        super().__init__(status, msg)
+        self.row, self.col = row, col
+
+
+def pack_mask(mask: torch.Tensor) -> torch.Tensor:
+    """[n, n] bool -> [n, ceil(n/32)] int32 words, column j at bit j % 32 (LSB first).  Marshalling
+    of the caller's mask into the ABI's layout (the metadata itself is computed by the library)."""
+    n = mask.shape[0]
+    W = (n + 31) // 32
+    m = torch.zeros((n, W * 32), dtype=torch.int64, device=mask.device)
+    m[:, :n] = mask.to(torch.int64)
+    w = (m.view(n, W, 32) << torch.arange(32, device=mask.device, dtype=torch.int64)).sum(-1)
+    return torch.where(w >= 2 ** 31, w - 2 ** 32, w).to(torch.int32).contiguous()
+
+
+def splat_acsr_from_mask(words: torch.Tensor, n: int, max_runs: int = SPLAT_MAX_SEGS, device: int = 0,
+                         stream=None) -> Acsr:
+    """ACSR handle from a packed bit mask (see pack_mask): CUDA tensor -> GPU ingest on `device`;
+    CPU tensor with device=-1 -> host inspection handle.  Raises NotRegular with (row, col)."""
+    if not words.is_contiguous() or words.dtype != torch.int32 or words.numel() != n * ((n + 31) // 32):
+        raise SplatError(1, "words must be contiguous int32 [n, ceil(n/32)]")
+    if (device >= 0) != words.is_cuda:
+        raise SplatError(1, "device >= 0 needs a CUDA mask, device -1 a CPU mask")
+    h = C.c_void_p()
+    br, bc = C.c_int32(), C.c_int32()
+    st = _stream(stream) if device >= 0 else 0
+    rc = lib().splat_acsr_from_mask(words.data_ptr(), n, max_runs, device, C.c_void_p(st), C.byref(h),
+                                    C.byref(br), C.byref(bc))
+    if rc == 2:
+        raise NotRegular(rc, lib().splat_last_error().decode(), br.value, bc.value)
+    _check(rc)
+    return Acsr(None, device, _handle=h)
 
 
 def _bhnd(x: torch.Tensor):
