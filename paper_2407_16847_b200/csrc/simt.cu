@@ -93,6 +93,36 @@ __device__ __forceinline__ float ex2f(float x)
     return y;
 }
 
+// Short rows (mean row length <= 256): the same three passes with LPR = 8 (mean <= 64) or 16 lanes
+// per row and 32 / LPR rows per warp, so that a warp has several rows' loads in flight (a warp per row leaves the launch latency-bound: at
+// N = 1024 and 0.4 % density it takes ~14 waves of ~4 dependent memory trips each).  No early
+// exit: every lane reaches the shuffles; lanes of rows past the end just have no work.
+template <typename TP, int LPR>
+__global__ void __launch_bounds__(kWarps * 32)
+softmax_short_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P, int BH)
+{
+    constexpr float L2E = 1.4426950408889634f;
+    const int lane = threadIdx.x & 31, sl = lane & (LPR - 1);
+    const long long g = ((long long)blockIdx.x * kWarps + (threadIdx.x >> 5)) * (32 / LPR) + lane / LPR;
+    const bool ok = g < (long long)BH * A.n;
+    const int bh = ok ? (int)(g / A.n) : 0, i = ok ? (int)(g % A.n) : 0;
+    const long long b = A.row_ptr[i];
+    const int len = ok ? (int)(A.row_ptr[i + 1] - b) : 0;
+    const long long e0 = (long long)bh * A.nnz + b;
+    const float *s = S + e0;
+    TP *p = P + e0;
+    float m = -INFINITY, l = 0.f;
+    for (int x = sl; x < len; x += LPR) m = fmaxf(m, s[x]);
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float mL = m * L2E;
+    for (int x = sl; x < len; x += LPR) l += ex2f(fmaf(s[x], L2E, -mL));
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    const float inv = 1.f / l;
+    for (int x = sl; x < len; x += LPR) p[x] = from_f<TP>(ex2f(fmaf(s[x], L2E, -mL)) * inv);
+}
+
 // Row softmax over the ACSR row (the softmax of each input row of the ACSR, which
 // stores only the non-zeros; reading R-1).  Warp per row, three streaming passes over the row --
 // max, sum of exp, write -- with 16-byte loads of S on the aligned body of the row (the second and
@@ -335,6 +365,20 @@ cudaError_t launch_rsddmm_simt(const DevAcsr &A, const void *Q, const void *K, b
 
 cudaError_t launch_softmax(const DevAcsr &A, const float *S, void *P, bool p_bf16, int BH, cudaStream_t st)
 {
+    if (A.nnz <= 256ll * A.n) {
+        const bool r8 = A.nnz <= 64ll * A.n;
+        const long long rows = (long long)BH * A.n, per_cta = kWarps * (r8 ? 4 : 2);
+        const unsigned grid = (unsigned)((rows + per_cta - 1) / per_cta);
+        if (p_bf16 && r8)
+            softmax_short_kernel<__nv_bfloat16, 8><<<grid, kWarps * 32, 0, st>>>(A, S, (__nv_bfloat16 *)P, BH);
+        else if (p_bf16)
+            softmax_short_kernel<__nv_bfloat16, 16><<<grid, kWarps * 32, 0, st>>>(A, S, (__nv_bfloat16 *)P, BH);
+        else if (r8)
+            softmax_short_kernel<float, 8><<<grid, kWarps * 32, 0, st>>>(A, S, (float *)P, BH);
+        else
+            softmax_short_kernel<float, 16><<<grid, kWarps * 32, 0, st>>>(A, S, (float *)P, BH);
+        return cudaGetLastError();
+    }
     if (p_bf16)
         softmax_kernel<__nv_bfloat16><<<grid_rows(A, BH), kWarps * 32, 0, st>>>(A, S, (__nv_bfloat16 *)P);
     else

@@ -115,6 +115,28 @@ def test_tiny_config_fp32_all_primitives():
     assert maxabs(Of.view(256, 64).cpu(), o) <= TOL_FP32
 
 
+@pytest.mark.parametrize("p,BH", [(Pattern("window", 101, lo=3, hi=3), 3), (Pattern("blocked", 77, block=5), 5),
+                                   (Pattern("strided", 130, stride=9), 1), (Pattern("window", 300, lo=90, hi=60), 3)],
+                         ids=["win", "blk", "str", "win16"])
+def test_softmax_short_rows(p, BH):
+    # mean row length <= 64 (<= 256) takes the 8 (16) lanes-per-row softmax; BH * N not a multiple
+    # of the rows per CTA leaves a ragged last CTA
+    q, k, v = (make_random((BH, p.seq_len, 16), 300 + t, torch.float32) for t in range(3))
+    a = S.Acsr(p, device=DEV)
+    assert a.nnz <= 256 * p.seq_len
+    Q, K, V = (dev(t.view(1, BH, p.seq_len, 16)) for t in (q, k, v))
+    Sd = torch.empty(BH * a.nnz, dtype=torch.float32, device=DEV)
+    S.splat_rsddmm(a, Q, K, Sd, 0.5)
+    refs = oracle_heads(p, q, k, v, 0.5, range(BH), want_sp=True)
+    for pdt in (torch.float32, torch.bfloat16):
+        Pd = torch.empty(BH * a.nnz, dtype=pdt, device=DEV)
+        S.splat_sparse_softmax(a, Sd, Pd, 1, BH)
+        torch.cuda.synchronize()
+        Pd = Pd.view(BH, a.nnz)
+        for bh, (_, _, pref) in enumerate(refs):
+            assert maxabs(Pd[bh].float().cpu(), pref) <= (TOL_FP32 if pdt == torch.float32 else 4e-3)
+
+
 def paper_grid():
     # SPEC criterion 6: 3 paper patterns x densities x N x d
     for N in (64, 128, 256):
