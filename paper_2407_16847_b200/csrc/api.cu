@@ -105,13 +105,13 @@ void free_device(splat_acsr_s *a)
 {
     if (a->device < 0) return;
     DeviceGuard g(a->device);
-    for (splat_acsr_s *sub : {a->sub_band, a->sub_str}) {
+    for (splat_acsr_s *sub : {a->sub_band, a->sub_str, a->sub_perm}) {
         if (sub) {
             free_device(sub);
             delete sub;
         }
     }
-    a->sub_band = a->sub_str = nullptr;
+    a->sub_band = a->sub_str = a->sub_perm = nullptr;
     cudaFree(a->d_lse);
     a->d_lse = nullptr;
     for (int i = 0; i < 3; ++i)
@@ -204,6 +204,15 @@ bool use_residue_split(const splat_acsr_s *a)
         return v && atoi(v) != 0;
     }();
     return a->sub_band != nullptr && !off;
+}
+
+bool use_perm()
+{
+    static const bool off = [] {
+        const char *v = getenv("SPLAT_NO_RESIDUE_SPLIT");
+        return v && atoi(v) != 0;
+    }();
+    return !off;
 }
 
 }  // namespace
@@ -388,6 +397,23 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
 void build_residue_split(splat_acsr_s *a, void *stream)
 {
     const splat_pattern &p = a->pat;
+    if (p.kind == SPLAT_STRIDED && a->device >= 0) {
+        const int N = a->n, X = p.stride;
+        if (X < 2 || N % X != 0) return;
+        const int nk = N / X;
+        if (nk < 2 || (nk <= 128 ? 128 % nk != 0 : nk % 128 != 0)) return;
+        splat_pattern blk{};
+        blk.kind = SPLAT_BLOCKED;
+        blk.seq_len = N;
+        blk.block = nk;
+        splat_acsr hp = nullptr;
+        if (build_impl(&blk, a->device, stream, &hp, true) != SPLAT_OK) { clear_error(); return; }
+        a->sub_perm = hp;
+        a->rv_l = X;
+        a->rv_nk = nk;
+        a->rv_R = nk <= 128 ? 128 / nk : 1;
+        return;
+    }
     if (p.kind != SPLAT_STRIDED_LOCAL || a->device < 0) return;
     const int N = a->n, l = p.stride;
     if (l < 2 || N % l != 0) return;
@@ -648,6 +674,9 @@ splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const
         }
         e = launch_mhsa_tc_residue(dev_view(a->sub_band), dev_view(a->sub_str), a->rv_l, a->rv_nk, a->rv_R, a->d_lse,
                                    Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
+    } else if (dt == SPLAT_BF16 && a->sub_perm && use_perm()) {
+        e = launch_mhsa_tc_permuted(dev_view(a->sub_perm), a->rv_l, a->rv_nk, a->rv_R, Q, K, V, B * H, d, scale, O,
+                                    (cudaStream_t)stream, &nl);
     } else if (dt == SPLAT_BF16)
         e = launch_mhsa_tc(dev_view(a), Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
     else

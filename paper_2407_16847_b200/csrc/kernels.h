@@ -37,6 +37,11 @@ struct DevAcsr {
 cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, int64_t *row_ptr,
                               cudaStream_t st);
 cudaError_t launch_acsr_scan(int64_t *row_ptr, int n, cudaStream_t st);
+// fused bf16 MHSA of plain STRIDED(l) on residue-major views: `perm` is the BLOCKED(nk) handle of the
+// permuted mask (N = l nk; nk | 128 with R = 128 / nk, or 128 | nk with R = 1); d = 64 or 128
+cudaError_t launch_mhsa_tc_permuted(const DevAcsr &perm, int l, int nk, int R, const void *Q, const void *K,
+                                    const void *V, int BH, int d, float scale, void *O, cudaStream_t st,
+                                    int *n_launch);
 // explicit bit mask (row stride ceil(n/32) words, LSB first) -> greedy runs; *bad = min over
 // irregular rows of (row << 32 | first column of run max_runs + 1), all ones if none
 cudaError_t launch_acsr_from_mask(const uint32_t *mask, int n, int max_runs, int4 *seg, uint8_t *nseg,

@@ -370,7 +370,8 @@ inline bool make_map_residue(CUtensorMap *m, const void *base, int BH, int N, in
     if (!enc) return false;
     cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)nk, (cuuint64_t)l, (cuuint64_t)BH};
     cuuint64_t strides[3] = {(cuuint64_t)l * d * 2, (cuuint64_t)d * 2, (cuuint64_t)N * d * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)nk, (cuuint32_t)R, 1};
+    // a 128-row tile is R whole classes (nk | 128) or 128 rows of one class (128 | nk, R = 1)
+    cuuint32_t box[4] = {64, (cuuint32_t)(nk < 128 ? nk : 128), (cuuint32_t)R, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

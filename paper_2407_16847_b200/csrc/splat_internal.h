@@ -195,6 +195,11 @@ struct splat_acsr_s {
     // strided part on residue-major views of Q/K/V/O (4-D tensor maps) and merges the two
     // partial softmaxes in the band pass's epilogue.  Null when not applicable.
     splat_acsr_s *sub_band = nullptr, *sub_str = nullptr;
+    // Plain STRIDED(X) with N = X nk, nk | 128 or 128 | nk: rows and keys permuted residue-major
+    // (r' = (i mod X) nk + i div X) make the mask block diagonal, BLOCKED(nk) -- the residue
+    // classes of the paper's stretched thread blocks (Sec. 7.3.1, App. B).  The fused bf16 path
+    // runs this handle on residue-major views of Q/K/V/O; the other paths use the natural one.
+    splat_acsr_s *sub_perm = nullptr;
     int32_t rv_l = 0, rv_nk = 0, rv_R = 0;   // stride, rows per residue (N / l), residues per 128-row tile
     float *d_lse = nullptr;                   // [B*H*N] log2-sum-exp of the strided pass (grown on demand)
     size_t lse_cap = 0;

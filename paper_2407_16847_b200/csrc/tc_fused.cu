@@ -78,6 +78,7 @@ struct Params {
     //   pass 1 (view = 1): tiles are residue-major (4-D maps, R residues x nk rows); the epilogue
     //                      stores O_s / l_s to the natural rows of O and lse2 = m + log2(l) to lse
     //   pass 2 (merge = 1): natural band tiles; the epilogue merges with O_s (read from O) and lse
+    //   plain STRIDED (view = 1, lse = null): the only pass; the epilogue stores O / l directly
     int view, merge, rv_R, rv_nk, rv_l;
     float *lse;
     unsigned long long *sched;   // split kernel: [work counter, done counter], zero between launches
@@ -408,7 +409,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         for (int c = 0; c < C::kChunks; ++c)
                             if (prm.view)
                                 tma_load_4d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
-                                            &q_full[slot], 64 * c, 0, t * prm.rv_R, bh);
+                                            &q_full[slot], 64 * c, (t * 128) % prm.rv_nk, (t * 128) / prm.rv_nk, bh);
                             else
                                 tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
                                             &q_full[slot], 64 * c, t * 128, bh);
@@ -429,8 +430,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
                         if (prm.view)
-                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, 0,
-                                        kv * prm.rv_R, bh);
+                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c,
+                                        (kv * 128) % prm.rv_nk, (kv * 128) / prm.rv_nk, bh);
                         else
                             tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * 128, bh);
                 }
@@ -592,10 +593,11 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             if (store_leader) TRACE(2 + g, 8);
             float inv = l > 0.f ? 1.f / l : 0.f;
             // residue decomposition: natural row of this thread's tile row
-            const int nat = prm.view ? (t * prm.rv_R + r / prm.rv_nk) + prm.rv_l * (r % prm.rv_nk) : t * 128 + r;
+            // permuted row p = 128 t + r is residue class p / nk, position p % nk: natural p / nk + l (p % nk)
+            const int nat = prm.view ? (t * 128 + r) / prm.rv_nk + prm.rv_l * ((t * 128 + r) % prm.rv_nk) : t * 128 + r;
             const bool in_range = nat < prm.N;
             float a_s = 0.f;                      // merge weight of the strided partial (pass 2)
-            if (prm.view && in_range)
+            if (prm.view && prm.lse && in_range)
                 prm.lse[(size_t)bh * prm.N + nat] = l > 0.f ? m + __log2f(l) : -INFINITY;
             if (prm.merge) {
                 // O = (O_b 2^(m_b - M) + O_s 2^(lse_s - M)) / (l_b 2^(m_b - M) + 2^(lse_s - M))
@@ -640,7 +642,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 fence_proxy_async_smem();
                 named_bar(1 + g, 128);
                 if (store_leader) {
-                    if (prm.view) tma_store_4d(&tmO, ostage, 64 * c, 0, t * prm.rv_R, bh);
+                    if (prm.view)
+                        tma_store_4d(&tmO, ostage, 64 * c, (t * 128) % prm.rv_nk, (t * 128) / prm.rv_nk, bh);
                     else tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
                     bulk_commit();
                 }
@@ -1475,6 +1478,21 @@ cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int 
     r2.merge = 1;
     r2.lse = lse;
     return launch_d<128>(band, Q, K, V, BH, scale, O, st, r2);           // pass 2: causal band + merge
+}
+
+cudaError_t launch_mhsa_tc_permuted(const DevAcsr &perm, int l, int nk, int R, const void *Q, const void *K,
+                                    const void *V, int BH, int d, float scale, void *O, cudaStream_t st,
+                                    int *n_launch)
+{
+    *n_launch = 1;
+    ResidueArgs r;            // residue-major views, no lse: the epilogue writes O / l directly
+    r.view = 1;
+    r.R = R;
+    r.nk = nk;
+    r.l = l;
+    if (d == 64) return launch_d<64>(perm, Q, K, V, BH, scale, O, st, r);
+    if (d == 128) return launch_d<128>(perm, Q, K, V, BH, scale, O, st, r);
+    return cudaErrorNotSupported;
 }
 
 cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, int d,

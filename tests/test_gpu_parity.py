@@ -180,6 +180,15 @@ SMALL_BF16 = [
     Config("dil_d128", Pattern("dilated", 900, stride=3, radius=50), 1, 2, 128, "bf16", 207),
     Config("strided_d64", Pattern("strided", 600, stride=7), 1, 2, 64, "bf16", 208),
     Config("blocked_d64", Pattern("blocked", 640, block=96), 2, 1, 64, "bf16", 209),
+    # plain STRIDED with N = X nk, nk | 128 or 128 | nk: the residue-major (permuted, block-
+    # diagonal) fused path
+    Config("strided_perm_d64", Pattern("strided", 1024, stride=16), 1, 2, 64, "bf16", 220),
+    Config("strided_perm_d128", Pattern("strided", 768, stride=12), 1, 2, 128, "bf16", 221),
+    Config("strided_perm_ragged", Pattern("strided", 1000, stride=125), 1, 2, 64, "bf16", 222),
+    Config("strided_perm_nk128", Pattern("strided", 1024, stride=8), 1, 2, 64, "bf16", 223),
+    Config("strided_perm_nk2", Pattern("strided", 512, stride=256), 1, 2, 128, "bf16", 224),
+    Config("strided_perm_nk256", Pattern("strided", 1024, stride=4), 1, 2, 64, "bf16", 225),
+    Config("strided_perm_nk384", Pattern("strided", 768, stride=2), 1, 2, 128, "bf16", 226),
     Config("tiny_n", Pattern("window", 5, lo=1, hi=1), 1, 1, 64, "bf16", 210),
     # STRIDED_LOCAL with N % l == 0 and N/l | 128: residue decomposition (strided pass on
     # residue-major views + band pass with the merge), R = 2, 1, 4, 16 residues per tile
@@ -191,6 +200,7 @@ SMALL_BF16 = [
     Config("st_res_d64", Pattern("strided_local", 1024, stride=16, causal=1), 1, 2, 64, "bf16", 215),
 ]
 RESIDUE = [c for c in SMALL_BF16 if c.name.startswith("st_res")]
+PERM = [c for c in SMALL_BF16 if c.name.startswith("strided_perm")]
 
 
 @pytest.mark.parametrize("cfg", SMALL_BF16, ids=lambda c: c.name)
@@ -211,7 +221,7 @@ def test_bf16_fused_and_unfused_small(cfg):
         assert maxabs(Pd[bh].float().cpu(), p) <= TOL_BF16
 
 
-@pytest.mark.parametrize("cfg", SMALL_BF16[:5] + RESIDUE, ids=lambda c: c.name)
+@pytest.mark.parametrize("cfg", SMALL_BF16[:5] + RESIDUE + PERM, ids=lambda c: c.name)
 def test_bf16_uniform_attention_pin(cfg):
     # Q = 0 -> p_ij = 1/nnz_i; V one-hot (V[j,t] = [t == j mod d]) -> O_i[t] = #{j: j = t mod d}/nnz_i
     N, d = cfg.N, cfg.d
