@@ -604,6 +604,9 @@ splat_status splat_rsddmm(splat_acsr a, const void *Q, const void *K, splat_dtyp
     if (dt == SPLAT_BF16 && use_residue_split(a))
         e = launch_unfused_residue(true, dev_view(a->sub_band), dev_view(a->sub_str), dev_view(a), a->rv_l, a->rv_nk,
                                    a->rv_R, Q, K, B * H, d, scale, S, (cudaStream_t)stream, &nl);
+    else if (dt == SPLAT_BF16 && a->sub_perm && use_perm())
+        e = launch_unfused_permuted(true, dev_view(a->sub_perm), dev_view(a), a->rv_l, a->rv_nk, a->rv_R, Q, K, B * H,
+                                    d, scale, S, (cudaStream_t)stream, &nl);
     else
         e = dt == SPLAT_BF16 ? launch_rsddmm_tc(dev_view(a), Q, K, B * H, d, scale, S, (cudaStream_t)stream)
                              : launch_rsddmm_simt(dev_view(a), Q, K, false, B * H, d, scale, S, (cudaStream_t)stream);
@@ -641,6 +644,9 @@ splat_status splat_rspmm(splat_acsr a, const void *P, const void *V, splat_dtype
     if (dt == SPLAT_BF16 && use_residue_split(a))
         e = launch_unfused_residue(false, dev_view(a->sub_band), dev_view(a->sub_str), dev_view(a), a->rv_l, a->rv_nk,
                                    a->rv_R, P, V, B * H, d, 0.f, O, (cudaStream_t)stream, &nl);
+    else if (dt == SPLAT_BF16 && a->sub_perm && use_perm())
+        e = launch_unfused_permuted(false, dev_view(a->sub_perm), dev_view(a), a->rv_l, a->rv_nk, a->rv_R, P, V,
+                                    B * H, d, 0.f, O, (cudaStream_t)stream, &nl);
     else
         e = dt == SPLAT_BF16 ? launch_rspmm_tc(dev_view(a), P, V, B * H, d, O, (cudaStream_t)stream)
                              : launch_rspmm_simt(dev_view(a), P, V, false, B * H, d, O, (cudaStream_t)stream);

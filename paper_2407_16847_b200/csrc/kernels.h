@@ -37,6 +37,11 @@ struct DevAcsr {
 cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, int64_t *row_ptr,
                               cudaStream_t st);
 cudaError_t launch_acsr_scan(int64_t *row_ptr, int n, cudaStream_t st);
+// unfused R-SDDMM (sddmm) / R-SpMM of plain STRIDED(l) on the permuted BLOCKED(nk) handle; S / P stay in
+// the natural ACSR order of `nat`
+cudaError_t launch_unfused_permuted(bool sddmm, const DevAcsr &perm, const DevAcsr &nat, int l, int nk, int R,
+                                    const void *X, const void *Y, int BH, int d, float scale, void *out,
+                                    cudaStream_t st, int *n_launch);
 // fused bf16 MHSA of plain STRIDED(l) on residue-major views: `perm` is the BLOCKED(nk) handle of the
 // permuted mask (N = l nk; nk | 128 with R = 128 / nk, or 128 | nk with R = 1); d = 64 or 128
 cudaError_t launch_mhsa_tc_permuted(const DevAcsr &perm, int l, int nk, int R, const void *Q, const void *K,

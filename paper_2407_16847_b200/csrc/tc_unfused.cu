@@ -85,17 +85,19 @@ __device__ __forceinline__ void st_pred_f32(float *addr, float v, uint32_t pred)
                  : "memory");
 }
 
-// natural row of tile row r (pass 1: residue-major tile)
+// natural row of tile row r (pass 1: residue-major tile; permuted row p = 128 t + r is residue
+// class p / nk, position p % nk, natural row p / nk + l (p % nk))
 __device__ __forceinline__ int nat_row(const ParamsU &prm, int t, int r)
 {
-    return prm.pass == 1 ? (t * prm.rv_R + r / prm.rv_nk) + prm.rv_l * (r % prm.rv_nk) : t * 128 + r;
+    const int p = t * 128 + r;
+    return prm.pass == 1 ? p / prm.rv_nk + prm.rv_l * (p % prm.rv_nk) : p;
 }
 
 // 3-D (natural) or 4-D (residue-major, pass 1) tile load of 128 rows starting at tile `tile`
 __device__ __forceinline__ void load_tile_rows(const ParamsU &prm, void *dst, const CUtensorMap *m, uint64_t *bar,
                                                int c0, int tile, int bh)
 {
-    if (prm.pass == 1) tma_load_4d(dst, m, bar, c0, 0, tile * prm.rv_R, bh);
+    if (prm.pass == 1) tma_load_4d(dst, m, bar, c0, (tile * 128) % prm.rv_nk, (tile * 128) / prm.rv_nk, bh);
     else tma_load_3d(dst, m, bar, c0, tile * 128, bh);
 }
 
@@ -772,6 +774,32 @@ cudaError_t launch_unfused_residue(bool sddmm, const DevAcsr &band, const DevAcs
             if ((e = launch_spmm_pass<128>(str, p1, X, Y, BH, out, st)) != cudaSuccess) return e;
             return launch_spmm_pass<128>(band, p2, X, Y, BH, out, st);
         }
+    }
+    return cudaErrorNotSupported;
+}
+
+// Plain STRIDED(l): only the residue-major pass, on the BLOCKED(nk) handle of the permuted mask.  The
+// natural ACSR row of i holds exactly its stride keys, in the order m of the permuted block row, so
+// pass 1's addressing (natural row base + rank within the sub-pattern row) is the whole S / P.
+cudaError_t launch_unfused_permuted(bool sddmm, const DevAcsr &perm, const DevAcsr &nat, int l, int nk, int R,
+                                    const void *X, const void *Y, int BH, int d, float scale, void *out,
+                                    cudaStream_t st, int *n_launch)
+{
+    *n_launch = 1;
+    UPass p1;
+    p1.pass = 1;
+    p1.l = l;
+    p1.nk = nk;
+    p1.R = R;
+    p1.nat_row_ptr = nat.row_ptr;
+    p1.nat_nnz = nat.nnz;
+    if (sddmm) {
+        float *S = reinterpret_cast<float *>(out);
+        if (d == 64) return launch_sddmm_pass<64>(perm, p1, X, Y, BH, scale, S, st);
+        if (d == 128) return launch_sddmm_pass<128>(perm, p1, X, Y, BH, scale, S, st);
+    } else {
+        if (d == 64) return launch_spmm_pass<64>(perm, p1, X, Y, BH, out, st);
+        if (d == 128) return launch_spmm_pass<128>(perm, p1, X, Y, BH, out, st);
     }
     return cudaErrorNotSupported;
 }
