@@ -204,13 +204,15 @@ def test_gpu_mask_handle_runs_the_fused_path():
 
 @pytest.mark.gpu
 @gpu
-@pytest.mark.parametrize("name", ["longformer", "mistral"])
+@pytest.mark.parametrize("name", ["longformer", "mistral", "win8192", "win12800"])
 def test_gpu_ingest_full_size(name):
-    # the bench configurations' masks, packed on the GPU (no N x N host array), ingested, and
+    # the bench configurations' masks (and two windows whose rows span 256 / 400 words, the other
+    # register-resident and streaming kernels), packed on the GPU (no N x N host array), ingested, and
     # compared with the descriptor build (itself bit-exact against the oracle) and with the oracle
     # on sampled rows
     from workloads import CONFIG_BY_NAME
-    p = CONFIG_BY_NAME[name].pattern
+    extra = {"win8192": Pattern("window", 8192, lo=300, hi=20), "win12800": Pattern("window", 12800, lo=5, hi=700)}
+    p = extra[name] if name in extra else CONFIG_BY_NAME[name].pattern
     n = p.seq_len
     W = (n + 31) // 32
     words = torch.zeros((n, W), dtype=torch.int32, device="cuda")
