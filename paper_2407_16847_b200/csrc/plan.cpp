@@ -11,6 +11,7 @@
 // (LPT) for the persistent kernels.  The planner works on O(rows) metadata
 // only, never on per-nnz data.
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "splat_internal.h"
@@ -21,6 +22,11 @@ void build_plan(splat_acsr_s &a)
 {
     Plan &P = a.plan;
     const int N = a.n, bm = P.bm, bn = P.bn;
+    // Ablation knob for the span-specialisation study (the paper's Fig. 13):
+    // SPLAT_PLAN_ABLATE=1 drops the FULL flags (every tile masked), =2 also drops the span (every
+    // query tile visits every key tile, as if rows spanned the whole sequence).  Unset: the plan.
+    const char *ab = getenv("SPLAT_PLAN_ABLATE");
+    const int ablate = ab ? atoi(ab) : 0;
     P.n_qt = (N + bm - 1) / bm;
     P.n_kt = (N + bn - 1) / bn;
     P.qt_ptr.assign(P.n_qt + 1, 0);
@@ -56,9 +62,11 @@ void build_plan(splat_acsr_s &a)
                 }
             }
         }
+        if (ablate >= 2)
+            for (int j = 0; j < P.n_kt; ++j) touch(j);
         std::sort(touched.begin(), touched.end());
         for (int j : touched) {
-            const bool full = (j + 1) * bn <= N && fullc[j] == nrows;
+            const bool full = ablate == 0 && (j + 1) * bn <= N && fullc[j] == nrows;
             P.kv.push_back(j | (full ? 0 : kPartialBit));
         }
         P.qt_ptr[t + 1] = (int32_t)P.kv.size();
@@ -192,8 +200,8 @@ void build_plan(splat_acsr_s &a)
                             any |= m[4 * r + w] != 0u;
                             all &= m[4 * r + w] == ~0u;
                         }
-                        if (any) bits |= 1u << (4 * q + w);
-                        if (all) bits |= 1u << (16 + 4 * q + w);
+                        if (any || ablate >= 2) bits |= 1u << (4 * q + w);   // ablation 2: no dead-chunk skip
+                        if (all && ablate == 0) bits |= 1u << (16 + 4 * q + w);   // ablation >= 1: always mask
                     }
                 P.qt_bits[qent_of_pair_ent[g][e]] = bits;
             }

@@ -64,7 +64,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01h_paper_grid.json"))
+    ap.add_argument("--ablate", type=int, default=0,
+                    help="span-specialisation ablation (SPLAT_PLAN_ABLATE): 1 = no FULL tiles / chunks, "
+                         "2 = also no span (every key tile, every chunk)")
+    ap.add_argument("--patterns", default="window,blocked,strided")
     a = ap.parse_args()
+    if a.ablate:
+        os.environ["SPLAT_PLAN_ABLATE"] = str(a.ablate)
     dev = 0
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -75,10 +81,12 @@ def main():
     O_ = torch.empty_like(Q)
     dense_ms = run(lambda: torch.nn.functional.scaled_dot_product_attention(Q, K, V, scale=scale))
     mm_ms = run(lambda: torch.matmul(Q, K.transpose(-1, -2)))
-    doc = {"N": N, "B": B, "H": H, "d": D, "dtype": "bf16", "iters": a.iters,
+    doc = {"N": N, "B": B, "H": H, "d": D, "dtype": "bf16", "iters": a.iters, "ablate": a.ablate,
            "dense_sdpa_ms": dense_ms, "dense_qkT_matmul_ms": mm_ms, "points": []}
     print(f"dense SDPA {dense_ms * 1e3:.1f} us, QK^T matmul {mm_ms * 1e3:.1f} us")
     for kind, param, p in grid():
+        if kind not in a.patterns.split(","):
+            continue
         h = S.Acsr(p, device=dev)
         nnz = h.nnz
         Sb = torch.empty(B * H * nnz, dtype=torch.float32, device=dev)
