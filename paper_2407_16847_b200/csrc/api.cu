@@ -518,7 +518,7 @@ splat_status splat_acsr_from_mask(const uint32_t *mask, int32_t n, int32_t max_r
     }
     e = launch_acsr_from_mask(mask, n, max_runs, reinterpret_cast<int4 *>(a->d_seg), a->d_nseg, a->d_row_ptr,
                               d_bad, cs);
-    note_launches(2);
+    note_launches(n > 32 * 8192 ? 4 : 2);     // row kernel + row_ptr scan (multi-CTA above 32 tiles)
     if (e == cudaSuccess) e = cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     cudaFree(d_bad);

@@ -66,6 +66,28 @@ def test_acsr_bit_exact_configs(cfg):
     device_meta_equals_oracle(cfg.pattern)
 
 
+@pytest.mark.parametrize("p", [Pattern("window", 8193, lo=5, hi=2), Pattern("window", 50001, lo=7, hi=3000),
+                               Pattern("strided_local", 65536, stride=256, causal=1)], ids=["8193", "50001", "65536"])
+def test_acsr_bit_exact_multi_tile_scan(p):
+    # N > 8192: several scan tiles in one CTA
+    device_meta_equals_oracle(p)
+
+
+def test_acsr_multi_cta_scan_large_n():
+    # N > 32 * 8192: tile sums + scan of sums + per-tile apply.  The oracle's mask enumeration is
+    # O(N^2), so row_ptr is checked against the window's closed-form row counts
+    # min(N-1, i+hi) - max(0, i-lo) + 1 and sampled rows against the oracle
+    p = Pattern("window", 300001, lo=3, hi=40)
+    a = S.Acsr(p, device=DEV)
+    seg, nseg, row_ptr = a.copy_meta()
+    i = np.arange(p.seq_len, dtype=np.int64)
+    cnt = np.minimum(p.seq_len - 1, i + p.hi) - np.maximum(0, i - p.lo) + 1
+    assert np.array_equal(row_ptr.numpy(), np.concatenate([[0], np.cumsum(cnt)]))
+    for r in (0, 1, 2, 4, 150000, 262143, 262144, 300000):
+        runs = O.runs_from_cols(O.row_cols(p, r), max_seg=64)
+        assert [tuple(x) for x in seg[r, :int(nseg[r])].tolist()] == [tuple(x) for x in runs]
+
+
 @pytest.mark.parametrize("N", [1, 2, 7, 33, 64, 130])
 def test_acsr_bit_exact_exhaustive_small(N):
     pats = []
