@@ -42,32 +42,37 @@ __global__ void acsr_rows_kernel(splat_pattern p, int4 *__restrict__ seg, uint8_
     if (i == 0) row_ptr[0] = 0;
 }
 
-// In-place inclusive scan of row_ptr[1..N] with one 1024-thread CTA, in tiles of 8192 counts:
-// thread t owns 8 consecutive counts of a tile, scans them, and the 1024 thread totals are
-// scanned with warp shuffles; a running carry joins the tiles, and the next tile's loads are
-// issued before the current tile is scanned.  Exact int64 arithmetic.
+// In-place inclusive scan of row_ptr[1..N] with one 1024-thread CTA, in tiles of 4096 counts
+// staged through shared memory: coalesced global loads / stores (element base + 1024 k + t),
+// thread t scans its 4 consecutive counts from SMEM, the 1024 thread totals are scanned with warp
+// shuffles, and a running carry joins the tiles; the next tile's loads are issued before the
+// current tile is scanned.  Exact int64 arithmetic.
 __global__ void __launch_bounds__(1024) acsr_scan_kernel(int64_t *__restrict__ row_ptr, int n)
 {
-    constexpr int PER = 8, TILE = 1024 * PER;
+    constexpr int PER = 4, TILE = 1024 * PER;
+    __shared__ int64_t buf[TILE];
     __shared__ int64_t warp_tot[32];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     int64_t *x = row_ptr + 1;   // x[0..n-1] = counts of rows 0..n-1
     int64_t carry = 0;
-    int64_t cur[PER], nxt[PER];
-    auto load = [&](int base, int64_t (&v)[PER]) {
+    int64_t nxt[PER];
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int i = base + t * PER + k;
-            v[k] = i < n ? x[i] : 0;
-        }
-    };
-    load(0, cur);
+    for (int k = 0; k < PER; ++k) nxt[k] = k * 1024 + t < n ? x[k * 1024 + t] : 0;
     for (int base = 0; base < n; base += TILE) {
-        if (base + TILE < n) load(base + TILE, nxt);
-        int64_t sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) buf[k * 1024 + t] = nxt[k];
+        if (base + TILE < n) {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int i = base + TILE + k * 1024 + t;
+                nxt[k] = i < n ? x[i] : 0;
+            }
+        }
+        __syncthreads();
+        int64_t cur[PER], sum = 0;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            sum += cur[k];
+            sum += buf[PER * t + k];
             cur[k] = sum;
         }
         int64_t inc = sum;
@@ -90,14 +95,15 @@ __global__ void __launch_bounds__(1024) acsr_scan_kernel(int64_t *__restrict__ r
         __syncthreads();
         const int64_t prefix = carry + inc - sum + (w > 0 ? warp_tot[w - 1] : 0);
 #pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int i = base + t * PER + k;
-            if (i < n) x[i] = prefix + cur[k];
-        }
+        for (int k = 0; k < PER; ++k) buf[PER * t + k] = prefix + cur[k];
         carry += warp_tot[31];
-        __syncthreads();      // warp_tot is rewritten by the next tile
+        __syncthreads();
 #pragma unroll
-        for (int k = 0; k < PER; ++k) cur[k] = nxt[k];
+        for (int k = 0; k < PER; ++k) {
+            const int i = base + k * 1024 + t;
+            if (i < n) x[i] = buf[k * 1024 + t];
+        }
+        __syncthreads();      // buf and warp_tot are rewritten by the next tile
     }
 }
 
@@ -175,9 +181,8 @@ __global__ void __launch_bounds__(1024) acsr_tile_apply_kernel(int64_t *__restri
 
 cudaError_t launch_acsr_scan(int64_t *row_ptr, int n, cudaStream_t st)
 {
-    constexpr int TILE = 8192;
-    // the single CTA costs ~7 us per tile (strided 8-byte loads); the multi-CTA path adds a
-    // stream-ordered allocation, so it only pays beyond a few dozen tiles
+    constexpr int TILE = 8192;   // multi-CTA tile (acsr_tile_*_kernel); the single CTA stages 4096
+    // the multi-CTA path adds a stream-ordered allocation: it only pays beyond a few dozen tiles
     if (n <= 32 * TILE) {
         acsr_scan_kernel<<<1, 1024, 0, st>>>(row_ptr, n);
         return cudaGetLastError();
