@@ -401,7 +401,7 @@ void build_residue_split(splat_acsr_s *a, void *stream)
         const int N = a->n, X = p.stride;
         if (X < 2 || N % X != 0) return;
         const int nk = N / X;
-        if (nk < 2 || (nk <= 128 ? 128 % nk != 0 : nk % 128 != 0)) return;
+        if (nk < 2 || (nk & (nk - 1)) != 0) return;   // power of two: nk | 128 or 128 | nk
         splat_pattern blk{};
         blk.kind = SPLAT_BLOCKED;
         blk.seq_len = N;
@@ -680,7 +680,7 @@ splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const
         }
         e = launch_mhsa_tc_residue(dev_view(a->sub_band), dev_view(a->sub_str), a->rv_l, a->rv_nk, a->rv_R, a->d_lse,
                                    Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
-    } else if (dt == SPLAT_BF16 && a->sub_perm && use_perm()) {
+    } else if (dt == SPLAT_BF16 && a->sub_perm && a->rv_nk <= 128 && use_perm()) {
         e = launch_mhsa_tc_permuted(dev_view(a->sub_perm), a->rv_l, a->rv_nk, a->rv_R, Q, K, V, B * H, d, scale, O,
                                     (cudaStream_t)stream, &nl);
     } else if (dt == SPLAT_BF16)

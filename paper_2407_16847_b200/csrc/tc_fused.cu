@@ -409,7 +409,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         for (int c = 0; c < C::kChunks; ++c)
                             if (prm.view)
                                 tma_load_4d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
-                                            &q_full[slot], 64 * c, (t * 128) % prm.rv_nk, (t * 128) / prm.rv_nk, bh);
+                                            &q_full[slot], 64 * c, 0, t * prm.rv_R, bh);
                             else
                                 tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
                                             &q_full[slot], 64 * c, t * 128, bh);
@@ -430,8 +430,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
                         if (prm.view)
-                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c,
-                                        (kv * 128) % prm.rv_nk, (kv * 128) / prm.rv_nk, bh);
+                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, 0,
+                                        kv * prm.rv_R, bh);
                         else
                             tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * 128, bh);
                 }
@@ -593,8 +593,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             if (store_leader) TRACE(2 + g, 8);
             float inv = l > 0.f ? 1.f / l : 0.f;
             // residue decomposition: natural row of this thread's tile row
-            // permuted row p = 128 t + r is residue class p / nk, position p % nk: natural p / nk + l (p % nk)
-            const int nat = prm.view ? (t * 128 + r) / prm.rv_nk + prm.rv_l * ((t * 128 + r) % prm.rv_nk) : t * 128 + r;
+            const int nat = prm.view ? (t * prm.rv_R + r / prm.rv_nk) + prm.rv_l * (r % prm.rv_nk) : t * 128 + r;
             const bool in_range = nat < prm.N;
             float a_s = 0.f;                      // merge weight of the strided partial (pass 2)
             if (prm.view && prm.lse && in_range)
@@ -642,8 +641,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 fence_proxy_async_smem();
                 named_bar(1 + g, 128);
                 if (store_leader) {
-                    if (prm.view)
-                        tma_store_4d(&tmO, ostage, 64 * c, (t * 128) % prm.rv_nk, (t * 128) / prm.rv_nk, bh);
+                    if (prm.view) tma_store_4d(&tmO, ostage, 64 * c, 0, t * prm.rv_R, bh);
                     else tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
                     bulk_commit();
                 }
@@ -1480,12 +1478,15 @@ cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int 
     return launch_d<128>(band, Q, K, V, BH, scale, O, st, r2);           // pass 2: causal band + merge
 }
 
+// Plain STRIDED(l) with nk | 128: the BLOCKED(nk) handle of the permuted mask on residue-major
+// views (R whole classes per 128-row tile); no lse, the epilogue writes O / l directly.
 cudaError_t launch_mhsa_tc_permuted(const DevAcsr &perm, int l, int nk, int R, const void *Q, const void *K,
                                     const void *V, int BH, int d, float scale, void *O, cudaStream_t st,
                                     int *n_launch)
 {
     *n_launch = 1;
-    ResidueArgs r;            // residue-major views, no lse: the epilogue writes O / l directly
+    if (nk > 128) return cudaErrorNotSupported;
+    ResidueArgs r;
     r.view = 1;
     r.R = R;
     r.nk = nk;

@@ -58,6 +58,7 @@ struct ParamsU {
     // the first i / l entries of the natural row.  pass 2: causal band in natural order, after
     // the row's i / l stride entries; R-SpMM adds pass 1's O.
     int pass, rv_l, rv_nk, rv_R;
+    int rv_sh;                   // log2(rv_nk) (a power of two)
     const int64_t *nat_row_ptr;
     long long nat_nnz;
 };
@@ -90,14 +91,14 @@ __device__ __forceinline__ void st_pred_f32(float *addr, float v, uint32_t pred)
 __device__ __forceinline__ int nat_row(const ParamsU &prm, int t, int r)
 {
     const int p = t * 128 + r;
-    return prm.pass == 1 ? p / prm.rv_nk + prm.rv_l * (p % prm.rv_nk) : p;
+    return prm.pass == 1 ? (p >> prm.rv_sh) + prm.rv_l * (p & (prm.rv_nk - 1)) : p;
 }
 
 // 3-D (natural) or 4-D (residue-major, pass 1) tile load of 128 rows starting at tile `tile`
 __device__ __forceinline__ void load_tile_rows(const ParamsU &prm, void *dst, const CUtensorMap *m, uint64_t *bar,
                                                int c0, int tile, int bh)
 {
-    if (prm.pass == 1) tma_load_4d(dst, m, bar, c0, (tile * 128) % prm.rv_nk, (tile * 128) / prm.rv_nk, bh);
+    if (prm.pass == 1) tma_load_4d(dst, m, bar, c0, (tile << 7) & (prm.rv_nk - 1), (tile << 7) >> prm.rv_sh, bh);
     else tma_load_3d(dst, m, bar, c0, tile * 128, bh);
 }
 
@@ -693,6 +694,8 @@ void apply_pass(ParamsU &p, const UPass &ps)
     p.pass = ps.pass;
     p.rv_l = ps.l;
     p.rv_nk = ps.nk;
+    p.rv_sh = 0;
+    while ((1 << p.rv_sh) < ps.nk) ++p.rv_sh;
     p.rv_R = ps.R;
     p.nat_row_ptr = ps.nat_row_ptr;
     p.nat_nnz = ps.nat_nnz;

@@ -210,7 +210,7 @@ SMALL_BF16 = [
     Config("strided_perm_nk128", Pattern("strided", 1024, stride=8), 1, 2, 64, "bf16", 223),
     Config("strided_perm_nk2", Pattern("strided", 512, stride=256), 1, 2, 128, "bf16", 224),
     Config("strided_perm_nk256", Pattern("strided", 1024, stride=4), 1, 2, 64, "bf16", 225),
-    Config("strided_perm_nk384", Pattern("strided", 768, stride=2), 1, 2, 128, "bf16", 226),
+    Config("strided_perm_nk256_d128", Pattern("strided", 512, stride=2), 1, 2, 128, "bf16", 226),
     Config("tiny_n", Pattern("window", 5, lo=1, hi=1), 1, 1, 64, "bf16", 210),
     # STRIDED_LOCAL with N % l == 0 and N/l | 128: residue decomposition (strided pass on
     # residue-major views + band pass with the merge), R = 2, 1, 4, 16 residues per tile
