@@ -680,7 +680,7 @@ splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const
         }
         e = launch_mhsa_tc_residue(dev_view(a->sub_band), dev_view(a->sub_str), a->rv_l, a->rv_nk, a->rv_R, a->d_lse,
                                    Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
-    } else if (dt == SPLAT_BF16 && a->sub_perm && a->rv_nk <= 128 && use_perm()) {
+    } else if (dt == SPLAT_BF16 && a->sub_perm && use_perm()) {
         e = launch_mhsa_tc_permuted(dev_view(a->sub_perm), a->rv_l, a->rv_nk, a->rv_R, Q, K, V, B * H, d, scale, O,
                                     (cudaStream_t)stream, &nl);
     } else if (dt == SPLAT_BF16)

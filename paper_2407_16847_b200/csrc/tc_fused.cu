@@ -80,6 +80,7 @@ struct Params {
     //   pass 2 (merge = 1): natural band tiles; the epilogue merges with O_s (read from O) and lse
     //   plain STRIDED (view = 1, lse = null): the only pass; the epilogue stores O / l directly
     int view, merge, rv_R, rv_nk, rv_l;
+    int rv_sh;                   // log2(rv_nk) (a power of two: nk | 128 or 128 | nk)
     float *lse;
     unsigned long long *sched;   // split kernel: [work counter, done counter], zero between launches
 };
@@ -318,7 +319,9 @@ __device__ __forceinline__ void apply_mask(float *v, uint32_t m)
     for (int x = 0; x < 32; ++x) v[x] = ((m >> x) & 1u) ? v[x] : -INFINITY;
 }
 
-template <int D>
+// VIEW: residue-major 4-D views (strided-row residue pass, permuted plain STRIDED); a separate
+// instantiation so the natural-order kernel carries none of the view arithmetic.
+template <int D, bool VIEW>
 __global__ void __launch_bounds__(kThreads, 1)
 mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const Params prm)
@@ -407,9 +410,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         mbar_expect_tx(&q_full[slot], C::kTileBytes);
 #pragma unroll
                         for (int c = 0; c < C::kChunks; ++c)
-                            if (prm.view)
+                            if (VIEW)
                                 tma_load_4d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
-                                            &q_full[slot], 64 * c, 0, t * prm.rv_R, bh);
+                                            &q_full[slot], 64 * c, (t << 7) & (prm.rv_nk - 1), (t << 7) >> prm.rv_sh, bh);
                             else
                                 tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
                                             &q_full[slot], 64 * c, t * 128, bh);
@@ -429,9 +432,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     mbar_expect_tx(&full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
-                        if (prm.view)
-                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, 0,
-                                        kv * prm.rv_R, bh);
+                        if (VIEW)
+                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c,
+                                        (kv << 7) & (prm.rv_nk - 1), (kv << 7) >> prm.rv_sh, bh);
                         else
                             tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * 128, bh);
                 }
@@ -593,10 +596,12 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             if (store_leader) TRACE(2 + g, 8);
             float inv = l > 0.f ? 1.f / l : 0.f;
             // residue decomposition: natural row of this thread's tile row
-            const int nat = prm.view ? (t * prm.rv_R + r / prm.rv_nk) + prm.rv_l * (r % prm.rv_nk) : t * 128 + r;
+            // permuted row p = 128 t + r is residue class p / nk, position p % nk: natural p / nk + l (p % nk)
+            const int nat = VIEW ? ((t * 128 + r) >> prm.rv_sh) + prm.rv_l * ((t * 128 + r) & (prm.rv_nk - 1))
+                                 : t * 128 + r;
             const bool in_range = nat < prm.N;
             float a_s = 0.f;                      // merge weight of the strided partial (pass 2)
-            if (prm.view && prm.lse && in_range)
+            if (VIEW && prm.lse && in_range)
                 prm.lse[(size_t)bh * prm.N + nat] = l > 0.f ? m + __log2f(l) : -INFINITY;
             if (prm.merge) {
                 // O = (O_b 2^(m_b - M) + O_s 2^(lse_s - M)) / (l_b 2^(m_b - M) + 2^(lse_s - M))
@@ -641,7 +646,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 fence_proxy_async_smem();
                 named_bar(1 + g, 128);
                 if (store_leader) {
-                    if (prm.view) tma_store_4d(&tmO, ostage, 64 * c, 0, t * prm.rv_R, bh);
+                    if (VIEW)
+                        tma_store_4d(&tmO, ostage, 64 * c, (t << 7) & (prm.rv_nk - 1), (t << 7) >> prm.rv_sh, bh);
                     else tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
                     bulk_commit();
                 }
@@ -1362,13 +1368,15 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
                !make_map(&mo, O, BH, A.n, D)) {
         return cudaErrorInvalidValue;
     }
-    static bool attr_set[64] = {false};
+    static bool attr_set[2][64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!attr_set[dev & 63]) {
-        cudaError_t e = cudaFuncSetAttribute(mhsa_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM);
+    const int vw = ra.view ? 1 : 0;
+    if (!attr_set[vw][dev & 63]) {
+        cudaError_t e = ra.view ? cudaFuncSetAttribute(mhsa_tc_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM)
+                                : cudaFuncSetAttribute(mhsa_tc_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM);
         if (e != cudaSuccess) return e;
-        attr_set[dev & 63] = true;
+        attr_set[vw][dev & 63] = true;
     }
     Params p;
     p.A = A;
@@ -1385,11 +1393,16 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     p.merge = ra.merge;
     p.rv_R = ra.R;
     p.rv_nk = ra.nk;
+    p.rv_sh = 0;
+    while ((1 << p.rv_sh) < ra.nk) ++p.rv_sh;
     p.rv_l = ra.l;
     p.lse = ra.lse;
     const long long units = (long long)A.n_pairs * BH;
     const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
-    mhsa_tc_kernel<D><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, p);
+    if (ra.view)
+        mhsa_tc_kernel<D, true><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, p);
+    else
+        mhsa_tc_kernel<D, false><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, p);
     return cudaGetLastError();
 }
 
@@ -1478,14 +1491,14 @@ cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int 
     return launch_d<128>(band, Q, K, V, BH, scale, O, st, r2);           // pass 2: causal band + merge
 }
 
-// Plain STRIDED(l) with nk | 128: the BLOCKED(nk) handle of the permuted mask on residue-major
-// views (R whole classes per 128-row tile); no lse, the epilogue writes O / l directly.
+// Plain STRIDED(l) with nk | 128 (R whole classes per 128-row tile) or 128 | nk (a tile inside one
+// class): the BLOCKED(nk) handle of the permuted mask on residue-major views; no lse, the
+// epilogue writes O / l directly.
 cudaError_t launch_mhsa_tc_permuted(const DevAcsr &perm, int l, int nk, int R, const void *Q, const void *K,
                                     const void *V, int BH, int d, float scale, void *O, cudaStream_t st,
                                     int *n_launch)
 {
     *n_launch = 1;
-    if (nk > 128) return cudaErrorNotSupported;
     ResidueArgs r;
     r.view = 1;
     r.R = R;
