@@ -224,6 +224,11 @@ splat_status splat_rspmm(splat_acsr a, const void *P, const void *V, splat_dtype
  *                1.0 reproduces Eq. 1); else SPLAT_ERR_INVALID_ARG
  * SPLAT_BF16 runs the sm_100a tensor-core kernel (TMA + tcgen05 + TMEM,
  * online softmax, fp32 accumulation); SPLAT_FP32 runs the SIMT fp32 kernel.
+ * Strided masks are run on residue-major views of Q/K/V/O (rows grouped by
+ * i mod stride, the paper's row classes P:367-374): STRIDED_LOCAL (d = 128)
+ * as two passes merged by log-sum-exp, plain STRIDED (N = stride * nk, nk a
+ * power of two) as one block-diagonal pass; the result is the same Eq. 1 O
+ * in natural row order (§9c).
  * ------------------------------------------------------------------------- */
 splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const void *V,
                                splat_dtype dt, int32_t B, int32_t H, int32_t d, float scale,
