@@ -114,6 +114,8 @@ void free_device(splat_acsr_s *a)
     a->sub_band = a->sub_str = a->sub_perm = nullptr;
     cudaFree(a->d_lse);
     a->d_lse = nullptr;
+    for (int i = 0; i < kLaunchSlots; ++i)
+        if (a->slots[i].ev) cudaEventDestroy((cudaEvent_t)a->slots[i].ev);
     for (int i = 0; i < 3; ++i)
         if (a->hs[i]) cudaStreamDestroy((cudaStream_t)a->hs[i]);
     for (int i = 0; i < 2; ++i)
@@ -142,7 +144,7 @@ void finish_host_meta(splat_acsr_s *a)
     a->max_segs = mx;
 }
 
-DevAcsr dev_view(const splat_acsr_s *a)
+DevAcsr dev_view(const splat_acsr_s *a, int slot = 0)
 {
     DevAcsr A;
     A.seg = reinterpret_cast<const int4 *>(a->d_seg);
@@ -163,7 +165,7 @@ DevAcsr dev_view(const splat_acsr_s *a)
     A.n_buckets = a->plan.n_buckets;
     for (int b = 0; b <= a->plan.n_buckets && b <= kMaxBuckets; ++b) A.bucket_start[b] = a->plan.bucket_start[b];
     A.t_info = reinterpret_cast<const int4 *>(a->plan.d_t_info);
-    A.sched = a->plan.d_sched;
+    A.sched = a->plan.d_sched ? a->plan.d_sched + 2 * slot : nullptr;
     A.t_n_buckets = a->plan.t_n_buckets;
     for (int b = 0; b <= a->plan.t_n_buckets && b <= kMaxBuckets; ++b) A.t_bucket_start[b] = a->plan.t_bucket_start[b];
     return A;
@@ -195,23 +197,17 @@ splat_status check_d(splat_dtype dt, int d)
 
 bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
-// residue decomposition available and not disabled (SPLAT_NO_RESIDUE_SPLIT=1: diagnostics, the
-// single-pass natural-order plan)
+// residue decomposition available and not disabled (diagnostics build only: SPLAT_NO_RESIDUE_SPLIT=1
+// runs the single-pass natural-order plan)
 bool use_residue_split(const splat_acsr_s *a)
 {
-    static const bool off = [] {
-        const char *v = getenv("SPLAT_NO_RESIDUE_SPLIT");
-        return v && atoi(v) != 0;
-    }();
+    static const bool off = diag_env("SPLAT_NO_RESIDUE_SPLIT") != 0;
     return a->sub_band != nullptr && !off;
 }
 
 bool use_perm()
 {
-    static const bool off = [] {
-        const char *v = getenv("SPLAT_NO_RESIDUE_SPLIT");
-        return v && atoi(v) != 0;
-    }();
+    static const bool off = diag_env("SPLAT_NO_RESIDUE_SPLIT") != 0;
     return !off;
 }
 
@@ -252,7 +248,7 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
         (e = cudaMalloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_qt_bits, sizeof(uint32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
         (e = cudaMalloc(&P.d_t_info, sizeof(int32_t) * 4 * P.n_qt)) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_sched, 2 * sizeof(unsigned long long))) != cudaSuccess) {
+        (e = cudaMalloc(&P.d_sched, kLaunchSlots * 2 * sizeof(unsigned long long))) != cudaSuccess) {
         free_device(a);
         delete a;
         return cuda_fail(e, "plan allocation");
@@ -274,7 +270,7 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
         e = cudaMemcpyAsync(P.d_qt_bits, P.qt_bits.data(), sizeof(uint32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_t_info, P.t_info.data(), sizeof(int32_t) * 4 * P.n_qt, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess) e = cudaMemsetAsync(P.d_sched, 0, 2 * sizeof(unsigned long long), cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P.d_sched, 0, kLaunchSlots * 2 * sizeof(unsigned long long), cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) {
         free_device(a);
@@ -435,11 +431,119 @@ void build_residue_split(splat_acsr_s *a, void *stream)
         delete hb;
         return;
     }
+    float *lse = nullptr;
+    if (cudaMalloc(&lse, sizeof(float) * (size_t)kLaunchSlots * kLseHeads * N) != cudaSuccess) {
+        cudaGetLastError();
+        free_device(hb);
+        delete hb;
+        free_device(hs);
+        delete hs;
+        return;
+    }
+    a->d_lse = lse;
     a->sub_band = hb;
     a->sub_str = hs;
     a->rv_l = l;
     a->rv_nk = nk;
     a->rv_R = 128 / nk;
+}
+
+// Launch slots and the host pipeline's streams / events of a top-level device handle (build time,
+// so that compute calls never allocate).
+splat_status create_call_resources(splat_acsr_s *a)
+{
+    if (a->device < 0) return SPLAT_OK;
+    DeviceGuard g(a->device);
+    cudaError_t e = cudaSuccess;
+    for (int i = 0; i < kLaunchSlots && e == cudaSuccess; ++i)
+        e = cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t *>(&a->slots[i].ev), cudaEventDisableTiming);
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i)
+        e = cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t *>(&a->hs[i]), cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+        for (int c = 0; c < 16 && e == cudaSuccess; ++c)
+            e = cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t *>(&a->hev[i][c]), cudaEventDisableTiming);
+    return e == cudaSuccess ? SPLAT_OK : cuda_fail(e, "call resources");
+}
+
+// RAII use of a launch slot on `s`: waits for the slot's previous user, records the slot's event
+// after the work queued while held.  Under stream capture the event ordering is skipped (a captured
+// graph must not be replayed concurrently with another use of the same handle).
+struct SlotUse {
+    LaunchSlot *slot = nullptr;
+    int index = 0;
+    cudaStream_t s;
+    bool capturing = false;
+    SlotUse(splat_acsr_s *a, cudaStream_t st) : s(st)
+    {
+        index = (int)(a->next_slot.fetch_add(1u, std::memory_order_relaxed) % kLaunchSlots);
+        slot = &a->slots[index];
+        slot->mu.lock();
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        capturing = cap != cudaStreamCaptureStatusNone;
+        if (slot->used && !capturing) cudaStreamWaitEvent(s, (cudaEvent_t)slot->ev, 0);
+    }
+    ~SlotUse()
+    {
+        if (!capturing && cudaEventRecord((cudaEvent_t)slot->ev, s) == cudaSuccess) slot->used = true;
+        slot->mu.unlock();
+    }
+};
+
+}  // namespace
+
+namespace {
+
+constexpr int kHostChunks = 12;     // (b, h) chunks of the host pipeline (<= 15 events)
+
+// argument checks of splat_sparse_mhsa (also applied once to a whole host-path call)
+splat_status check_mhsa(splat_acsr a, const void *Q, const void *K, const void *V, splat_dtype dt, int B, int H,
+                        int d, float scale, const void *O)
+{
+    splat_status st = check_compute(a, B, H);
+    if (st == SPLAT_OK) st = check_d(dt, d);
+    if (st != SPLAT_OK) return st;
+    if (!Q || !K || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
+    if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O))
+        return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
+    if (!(scale > 0.f) || scale == INFINITY) return set_error(SPLAT_ERR_INVALID_ARG, "scale must be positive and finite");
+    return SPLAT_OK;
+}
+
+// dispatch of a validated fused call (sets the launch count); no allocation, no host sync
+cudaError_t launch_mhsa(splat_acsr a, const void *Q, const void *K, const void *V, splat_dtype dt, int BH, int d,
+                        float scale, void *O, cudaStream_t s)
+{
+    int nl = 1;
+    cudaError_t e;
+    if (dt == SPLAT_BF16 && d == 128 && use_residue_split(a)) {
+        // heads in chunks of kLseHeads: the slot's lse scratch holds one chunk
+        SlotUse su(a, s);
+        float *lse = a->d_lse + (size_t)su.index * kLseHeads * a->n;
+        const size_t slice = (size_t)a->n * d * 2;
+        e = cudaSuccess;
+        nl = 0;
+        for (int h0 = 0; h0 < BH && e == cudaSuccess; h0 += kLseHeads) {
+            const int nh = BH - h0 < kLseHeads ? BH - h0 : kLseHeads;
+            const size_t off = slice * h0;
+            int n1 = 0;
+            e = launch_mhsa_tc_residue(dev_view(a->sub_band), dev_view(a->sub_str), a->rv_l, a->rv_nk, a->rv_R, lse,
+                                       (const char *)Q + off, (const char *)K + off, (const char *)V + off, nh, d,
+                                       scale, (char *)O + off, s, &n1);
+            nl += n1;
+        }
+    } else if (dt == SPLAT_BF16 && a->sub_perm && use_perm())
+        e = launch_mhsa_tc_permuted(dev_view(a->sub_perm), a->rv_l, a->rv_nk, a->rv_R, Q, K, V, BH, d, scale, O, s,
+                                    &nl);
+    else if (dt == SPLAT_BF16 && d == 64) {
+        SlotUse su(a, s);                // the split kernel's work counter
+        e = launch_mhsa_tc(dev_view(a, su.index), Q, K, V, BH, d, scale, O, s, &nl);
+    } else if (dt == SPLAT_BF16)
+        e = launch_mhsa_tc(dev_view(a), Q, K, V, BH, d, scale, O, s, &nl);
+    else
+        e = launch_mhsa_simt(dev_view(a), Q, K, V, false, BH, d, scale, O, s);
+    note_launches(nl);
+    return e;
 }
 
 }  // namespace
@@ -450,6 +554,11 @@ splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, 
 {
     splat_status st = build_impl(p, device, stream, out, false);
     if (st == SPLAT_OK) build_residue_split(*out, stream);
+    if (st == SPLAT_OK && (st = create_call_resources(*out)) != SPLAT_OK) {
+        free_device(*out);
+        delete *out;
+        *out = nullptr;
+    }
     return st;
 }
 
@@ -532,7 +641,13 @@ splat_status splat_acsr_from_mask(const uint32_t *mask, int32_t n, int32_t max_r
         delete a;
         return not_regular((long long)(bad >> 32), (long long)(bad & 0xffffffffull));
     }
-    return finish_device_build(a, cs, out);
+    splat_status st = finish_device_build(a, cs, out);
+    if (st == SPLAT_OK && (st = create_call_resources(*out)) != SPLAT_OK) {
+        free_device(*out);
+        delete *out;
+        *out = nullptr;
+    }
+    return st;
 }
 
 splat_status splat_acsr_info(splat_acsr a, int32_t *n, int64_t *nnz, int32_t *max_segs, double *density)
@@ -658,37 +773,11 @@ splat_status splat_rspmm(splat_acsr a, const void *P, const void *V, splat_dtype
 splat_status splat_sparse_mhsa(splat_acsr a, const void *Q, const void *K, const void *V, splat_dtype dt,
                                int32_t B, int32_t H, int32_t d, float scale, void *O, void *stream)
 {
-    splat_status st = check_compute(a, B, H);
-    if (st == SPLAT_OK) st = check_d(dt, d);
+    splat_status st = check_mhsa(a, Q, K, V, dt, B, H, d, scale, O);
     if (st != SPLAT_OK) return st;
-    if (!Q || !K || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
-    if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O))
-        return set_error(SPLAT_ERR_INVALID_ARG, "tensors must be 16-byte aligned");
-    if (!(scale > 0.f) || scale == INFINITY) return set_error(SPLAT_ERR_INVALID_ARG, "scale must be positive and finite");
     DeviceGuard g(a->device);
-    cudaError_t e;
-    int nl = 1;
-    if (dt == SPLAT_BF16 && d == 128 && use_residue_split(a)) {
-        // residue decomposition: handle-owned lse scratch, grown on the first call with this B*H
-        const size_t need = (size_t)B * H * a->n;
-        if (a->lse_cap < need) {
-            cudaFree(a->d_lse);
-            a->d_lse = nullptr;
-            a->lse_cap = 0;
-            if ((e = cudaMalloc(&a->d_lse, need * sizeof(float))) != cudaSuccess) return cuda_fail(e, "lse scratch");
-            a->lse_cap = need;
-        }
-        e = launch_mhsa_tc_residue(dev_view(a->sub_band), dev_view(a->sub_str), a->rv_l, a->rv_nk, a->rv_R, a->d_lse,
-                                   Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
-    } else if (dt == SPLAT_BF16 && a->sub_perm && use_perm()) {
-        e = launch_mhsa_tc_permuted(dev_view(a->sub_perm), a->rv_l, a->rv_nk, a->rv_R, Q, K, V, B * H, d, scale, O,
-                                    (cudaStream_t)stream, &nl);
-    } else if (dt == SPLAT_BF16)
-        e = launch_mhsa_tc(dev_view(a), Q, K, V, B * H, d, scale, O, (cudaStream_t)stream, &nl);
-    else
-        e = launch_mhsa_simt(dev_view(a), Q, K, V, false, B * H, d, scale, O, (cudaStream_t)stream);
+    cudaError_t e = launch_mhsa(a, Q, K, V, dt, B * H, d, scale, O, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "splat_sparse_mhsa launch");
-    note_launches(nl);
     return SPLAT_OK;
 }
 
@@ -696,66 +785,61 @@ splat_status splat_sparse_mhsa_host(splat_acsr a, const void *Qh, const void *Kh
                                     int32_t B, int32_t H, int32_t d, float scale, void *Oh, void *dQ, void *dK,
                                     void *dV, void *dO, void *stream)
 {
-    splat_status st = check_compute(a, B, H);
-    if (st == SPLAT_OK) st = check_d(dt, d);
+    splat_status st = check_mhsa(a, dQ, dK, dV, dt, B, H, d, scale, dO);
     if (st != SPLAT_OK) return st;
     if (!Qh || !Kh || !Vh || !Oh) return set_error(SPLAT_ERR_INVALID_ARG, "null host pointer");
-    if (!dQ || !dK || !dV || !dO) return set_error(SPLAT_ERR_INVALID_ARG, "null device pointer");
+    if (!a->hs[0]) return set_error(SPLAT_ERR_INVALID_ARG, "handle has no host pipeline (internal sub-handle)");
     const int BH = B * H;
     const size_t slice = (size_t)a->n * d * (dt == SPLAT_BF16 ? 2 : 4);    // bytes per (b, h)
+    // chunk boundaries only at slice indices whose byte offset is 16-byte aligned (the kernels'
+    // alignment contract): multiples of `unit` slices
+    size_t gs = slice & 15u ? slice & 15u : 16u, g16 = 16;
+    while (gs) { const size_t t = g16 % gs; g16 = gs; gs = t; }          // gcd(slice mod 16, 16)
+    const int unit = (int)(16 / g16);
+    const int n_units = (BH + unit - 1) / unit;
+    const int nch = n_units >= kHostChunks ? kHostChunks : n_units;
     DeviceGuard g(a->device);
     cudaStream_t cs = (cudaStream_t)stream;
-    cudaError_t e = cudaSuccess;
-    // handle-owned pipeline streams / events, created on first use
-    for (int i = 0; i < 3 && e == cudaSuccess; ++i)
-        if (!a->hs[i]) e = cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t *>(&a->hs[i]), cudaStreamNonBlocking);
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
-        for (int c = 0; c < 16 && e == cudaSuccess; ++c)
-            if (!a->hev[i][c]) e = cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t *>(&a->hev[i][c]), cudaEventDisableTiming);
-    if (e != cudaSuccess) return cuda_fail(e, "pipeline streams");
     cudaStream_t s_in = (cudaStream_t)a->hs[0], s_k = (cudaStream_t)a->hs[1], s_out = (cudaStream_t)a->hs[2];
-    // chunks of (b, h) slices: enough to overlap, each still filling the GPU
-    static const int max_ch = [] {
-        const char *v = getenv("SPLAT_HOST_CHUNKS");      // tuning knob, <= 15
-        const int c = v ? atoi(v) : 12;
-        return c < 1 ? 1 : (c > 15 ? 15 : c);
-    }();
-    const int nch = BH >= max_ch ? max_ch : BH;
-    cudaEvent_t start = (cudaEvent_t)a->hev[0][15], done_k[15], done_in[15];
-    for (int c = 0; c < nch; ++c) {
-        done_in[c] = (cudaEvent_t)a->hev[0][c];
-        done_k[c] = (cudaEvent_t)a->hev[1][c];
-    }
+    cudaEvent_t start = (cudaEvent_t)a->hev[0][15], fin = (cudaEvent_t)a->hev[1][15];
     // everything the caller enqueued on `stream` before this call happens first
-    if ((e = cudaEventRecord(start, cs)) != cudaSuccess) return cuda_fail(e, "event");
+    cudaError_t e = cudaEventRecord(start, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "event");
     cudaStreamWaitEvent(s_in, start, 0);
     cudaStreamWaitEvent(s_k, start, 0);
     cudaStreamWaitEvent(s_out, start, 0);
     int nl = 0;
     for (int c = 0; c < nch && e == cudaSuccess; ++c) {
-        const int b0 = (int)((long long)BH * c / nch), b1 = (int)((long long)BH * (c + 1) / nch);
+        const int b0 = (int)std::min<long long>(BH, (long long)unit * ((long long)n_units * c / nch));
+        const int b1 = (int)std::min<long long>(BH, (long long)unit * ((long long)n_units * (c + 1) / nch));
+        if (b1 <= b0) continue;
         const size_t off = slice * b0, bytes = slice * (b1 - b0);
         auto hp = [&](const void *p) { return static_cast<const char *>(p) + off; };
         auto dp = [&](void *p) { return static_cast<char *>(p) + off; };
+        cudaEvent_t done_in = (cudaEvent_t)a->hev[0][c], done_k = (cudaEvent_t)a->hev[1][c];
         e = cudaMemcpyAsync(dp(dQ), hp(Qh), bytes, cudaMemcpyHostToDevice, s_in);
         if (e == cudaSuccess) e = cudaMemcpyAsync(dp(dK), hp(Kh), bytes, cudaMemcpyHostToDevice, s_in);
         if (e == cudaSuccess) e = cudaMemcpyAsync(dp(dV), hp(Vh), bytes, cudaMemcpyHostToDevice, s_in);
-        if (e == cudaSuccess) e = cudaEventRecord(done_in[c], s_in);
-        if (e != cudaSuccess) break;
-        cudaStreamWaitEvent(s_k, done_in[c], 0);
-        st = splat_sparse_mhsa(a, dp(dQ), dp(dK), dp(dV), dt, 1, b1 - b0, d, scale, dp(dO), s_k);
-        if (st != SPLAT_OK) return st;
+        if (e == cudaSuccess) e = cudaEventRecord(done_in, s_in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_k, done_in, 0);
+        if (e == cudaSuccess) e = launch_mhsa(a, dp(dQ), dp(dK), dp(dV), dt, b1 - b0, d, scale, dp(dO), s_k);
         nl += g_launches;
-        if ((e = cudaEventRecord(done_k[c], s_k)) != cudaSuccess) break;
-        cudaStreamWaitEvent(s_out, done_k[c], 0);
-        e = cudaMemcpyAsync(static_cast<char *>(Oh) + off, static_cast<char *>(dO) + off, bytes, cudaMemcpyDeviceToHost,
-                            s_out);
+        if (e == cudaSuccess) e = cudaEventRecord(done_k, s_k);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, done_k, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(static_cast<char *>(Oh) + off, static_cast<char *>(dO) + off, bytes,
+                                cudaMemcpyDeviceToHost, s_out);
     }
-    if (e != cudaSuccess) return cuda_fail(e, "pipelined host copies");
-    // the caller's stream waits for the last copy-out (and, through it, for everything else)
-    cudaEvent_t fin = (cudaEvent_t)a->hev[1][15];
-    if ((e = cudaEventRecord(fin, s_out)) != cudaSuccess || (e = cudaStreamWaitEvent(cs, fin, 0)) != cudaSuccess)
-        return cuda_fail(e, "pipeline join");
+    // the caller's stream waits for the last copy-out and, through it, for everything queued above --
+    // also after an error, so a caller that frees its buffers afterwards cannot race the copies
+    cudaEventRecord(fin, s_in);
+    cudaStreamWaitEvent(s_out, fin, 0);
+    cudaEventRecord(fin, s_k);
+    cudaStreamWaitEvent(s_out, fin, 0);
+    const cudaError_t ej = cudaEventRecord(fin, s_out);
+    const cudaError_t ew = ej == cudaSuccess ? cudaStreamWaitEvent(cs, fin, 0) : ej;
+    if (e != cudaSuccess) return cuda_fail(e, "splat_sparse_mhsa_host");
+    if (ew != cudaSuccess) return cuda_fail(ew, "pipeline join");
     note_launches(nl);
     return SPLAT_OK;
 }

@@ -64,6 +64,9 @@ cudaError_t launch_mhsa_simt(const DevAcsr &A, const void *Q, const void *K, con
 
 // sm_100a tensor-core kernels (bf16, d in {64, 128}); return cudaErrorNotSupported
 // when the configuration is outside what they implement.
+// d = 64 streaming fused kernel (tc_fused64.cu); A.sched = the call's launch-slot work counter
+cudaError_t launch_mhsa64(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, float scale,
+                          void *O, cudaStream_t st);
 cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, int d,
                            float scale, void *O, cudaStream_t st, int *n_launch);
 // Residue decomposition of STRIDED_LOCAL (splat_acsr_s::sub_band): pass 1 over the strided

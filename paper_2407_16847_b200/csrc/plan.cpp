@@ -22,11 +22,10 @@ void build_plan(splat_acsr_s &a)
 {
     Plan &P = a.plan;
     const int N = a.n, bm = P.bm, bn = P.bn;
-    // Ablation knob for the span-specialisation study (the paper's Fig. 13):
-    // SPLAT_PLAN_ABLATE=1 drops the FULL flags (every tile masked), =2 also drops the span (every
-    // query tile visits every key tile, as if rows spanned the whole sequence).  Unset: the plan.
-    const char *ab = getenv("SPLAT_PLAN_ABLATE");
-    const int ablate = ab ? atoi(ab) : 0;
+    // Ablation knob for the span-specialisation study (the paper's Fig. 13),
+    // diagnostics build only: SPLAT_PLAN_ABLATE=1 drops the FULL flags (every tile masked), =2 also
+    // drops the span (every query tile visits every key tile).  Product build: always 0.
+    const int ablate = diag_env("SPLAT_PLAN_ABLATE");
     P.n_qt = (N + bm - 1) / bm;
     P.n_kt = (N + bn - 1) / bn;
     P.qt_ptr.assign(P.n_qt + 1, 0);

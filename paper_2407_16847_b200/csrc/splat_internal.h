@@ -1,7 +1,10 @@
 // splat_internal.h -- internal types of the SPLAT B200 library (not part of the ABI).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
+#include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "splat.h"
@@ -33,6 +36,21 @@ constexpr int32_t kKindResiduePrev = 100;
 // handles built from an explicit bit mask (splat_acsr_from_mask): no descriptor, metadata only
 constexpr int32_t kKindMask = 101;
 constexpr int32_t kMaxMaskN = 1 << 17;
+
+// Diagnostics build (-DSPLAT_DIAG -> libsplat_diag.so, tools/ only): environment knobs that change
+// the plan or switch kernels off for profiling.  The product library (libsplat.so) is built
+// without SPLAT_DIAG: there every knob reads as 0 and no environment variable is consulted.
+#ifdef SPLAT_DIAG
+constexpr bool kDiag = true;
+inline int diag_env(const char *name)
+{
+    const char *e = getenv(name);
+    return e ? atoi(e) : 0;
+}
+#else
+constexpr bool kDiag = false;
+inline int diag_env(const char *) { return 0; }
+#endif
 
 SPLAT_HD int imin(int a, int b) { return a < b ? a : b; }
 SPLAT_HD int imax(int a, int b) { return a > b ? a : b; }
@@ -168,7 +186,22 @@ struct Plan {
     int32_t *d_kv_mask = nullptr;
     uint32_t *d_qt_bits = nullptr;
     int32_t *d_t_info = nullptr;
-    unsigned long long *d_sched = nullptr;   // [2] split-kernel work / done counters (zero between launches)
+    unsigned long long *d_sched = nullptr;   // [kLaunchSlots][2] split-kernel work / done counters
+};
+
+// Per-call device resources of a compute call (the split kernel's work counter, the residue
+// decomposition's lse scratch) come from one of kLaunchSlots slots, allocated at build time.  A
+// call takes the next slot round robin; the calling stream first waits for the slot's previous
+// user (an event), so two streams sharing one handle never share a slot's resources at the same
+// time -- correct by construction, with up to kLaunchSlots calls in flight concurrently.
+constexpr int kLaunchSlots = 8;
+// heads (b, h) per launch of the residue decomposition (lse scratch per slot: kLseHeads x N floats)
+constexpr int kLseHeads = 64;
+
+struct LaunchSlot {
+    std::mutex mu;
+    void *ev = nullptr;          // cudaEvent_t recorded after the slot's last use
+    bool used = false;
 };
 
 }  // namespace splat
@@ -201,9 +234,13 @@ struct splat_acsr_s {
     // runs this handle on residue-major views of Q/K/V/O; the other paths use the natural one.
     splat_acsr_s *sub_perm = nullptr;
     int32_t rv_l = 0, rv_nk = 0, rv_R = 0;   // stride, rows per residue (N / l), residues per 128-row tile
-    float *d_lse = nullptr;                   // [B*H*N] log2-sum-exp of the strided pass (grown on demand)
-    size_t lse_cap = 0;
-    // splat_sparse_mhsa_host pipeline: copy-in, compute and copy-out streams + per-chunk events
+    float *d_lse = nullptr;                   // [kLaunchSlots][kLseHeads * N] log2-sum-exp of the strided pass
+    // launch slots (top-level device handles only)
+    splat::LaunchSlot slots[splat::kLaunchSlots];
+    std::atomic<unsigned> next_slot{0};
+    // splat_sparse_mhsa_host pipeline: copy-in, compute and copy-out streams + per-chunk events,
+    // created at build time (top-level device handles only)
+    std::mutex host_mu;
     void *hs[3] = {nullptr, nullptr, nullptr};
     void *hev[2][16] = {};
 };

@@ -39,6 +39,7 @@
 
 #include "kernels.h"
 #include "sm100.cuh"
+#include "softmax_math.cuh"
 
 namespace splat {
 namespace {
@@ -85,14 +86,26 @@ struct Params {
     unsigned long long *sched;   // split kernel: [work counter, done counter], zero between launches
 };
 
+// Profiling knobs (SPLAT_TC_DEBUG) exist only in the diagnostics build (libsplat_diag.so); in the
+// product build DBG() is a compile-time 0.
+#define DBG(m) (kDiag && (prm.dbg & (m)))
+
+#if defined(SPLAT_TRACE) && !defined(SPLAT_DIAG)
+#error "SPLAT_TRACE needs the diagnostics build (-DSPLAT_DIAG)"
+#endif
+#if defined(SPLAT_FUSED_PROF) && !defined(SPLAT_DIAG)
+#error "SPLAT_FUSED_PROF needs the diagnostics build (-DSPLAT_DIAG)"
+#endif
+#ifdef SPLAT_DIAG
 // Profiling aid (SPLAT_TC_DEBUG & 4): clock64 timestamps of pipeline events in CTA 0.
 __device__ unsigned long long g_trace[6][2048];
 __device__ int g_trace_n[6];
+#endif
 #ifdef SPLAT_TRACE
 // per-role event counter lives in a register (tr_n, declared at the top of the kernel)
 #define TRACE(R, TAG)                                                                                    \
     do {                                                                                                 \
-        if ((prm.dbg & 4) && blockIdx.x == 0) {                                                          \
+        if (DBG(4) && blockIdx.x == 0) {                                                          \
             if (tr_n < 2048) g_trace[R][tr_n] = ((unsigned long long)(TAG) << 48) | (clock64() & 0xffffffffffffull); \
             ++tr_n;                                                                                      \
             g_trace_n[R] = tr_n;                                                                         \
@@ -203,121 +216,7 @@ __device__ __forceinline__ int ent_at(const DevAcsr &A, const UnitInfo &un, cons
     return A.pair_ent[e];
 }
 
-__device__ __forceinline__ float fmax3(float a, float b, float c)
-{
-    float d;
-    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-    return d;
-}
-
-__device__ __forceinline__ uint64_t pack2(float lo, float hi)
-{
-    uint64_t r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-    return r;
-}
-
-__device__ __forceinline__ void unpack2(uint64_t v, float &lo, float &hi)
-{
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c)
-{
-    uint64_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b)
-{
-    uint64_t d;
-    asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-
-__device__ __forceinline__ float max32(const float *v)
-{
-    float a0 = fmax3(v[0], v[1], v[2]), a1 = fmax3(v[3], v[4], v[5]);
-    float a2 = fmax3(v[6], v[7], v[8]), a3 = fmax3(v[9], v[10], v[11]);
-#pragma unroll
-    for (int x = 12; x < 32; x += 8) {
-        a0 = fmax3(a0, v[x + 0], v[x + 1]);
-        a1 = fmax3(a1, v[x + 2], v[x + 3]);
-        a2 = fmax3(a2, v[x + 4], v[x + 5]);
-        a3 = fmax3(a3, v[x + 6], v[x + 7]);
-    }
-    return fmax3(fmax3(a0, a1, a2), a3, -INFINITY);
-}
-
-// Number of the 32 exponentials of a chunk evaluated on the FMA pipe instead of MUFU (the MUFU
-// does 16 ex2/clk/SM against 8192 bf16 FLOP/clk on the tensor pipe: at d = 64 it is the
-// co-bottleneck).  Multiple of 4.
-#ifndef SPLAT_NEMU128
-#define SPLAT_NEMU128 4       // d = 128 (MUFU has more slack against the tensor pipe there)
-#endif
-#ifndef SPLAT_NEMU
-#define SPLAT_NEMU 8
-#endif
-
-__device__ __forceinline__ uint64_t fmax2_clamp(uint64_t z)
-{
-    float a, b;
-    unpack2(z, a, b);
-    return pack2(fmaxf(a, -126.f), fmaxf(b, -126.f));
-}
-
-// 2^x for a packed pair on the FMA pipe: x = j + f with j = rint(x) (1.5*2^23 magic-number
-// rounding), f in [-1/2, 1/2]; 2^f by a degree-3 polynomial (max relative error 7.5e-5, far
-// below bf16's 2^-9); the exponent j is added to the bits of 2^f.  x is clamped at -126 so
-// masked (-inf) scores give 2^-126 (below any bf16 P that matters; -127 would wrap the
-// exponent field of a p just under 1).
-__device__ __forceinline__ void exp2_emu2(uint64_t z, float &ra, float &rb)
-{
-    const uint64_t zc = fmax2_clamp(z);
-    const uint64_t t = fadd2(zc, pack2(12582912.f, 12582912.f));
-    const uint64_t jf = fadd2(t, pack2(-12582912.f, -12582912.f));
-    const uint64_t f = ffma2(jf, pack2(-1.f, -1.f), zc);
-    uint64_t p = ffma2(pack2(0.0551716648f, 0.0551716648f), f, pack2(0.2426111251f, 0.2426111251f));
-    p = ffma2(p, f, pack2(0.6932609677f, 0.6932609677f));
-    p = ffma2(p, f, pack2(0.9999280572f, 0.9999280572f));
-    float pa, pb, ta, tb;
-    unpack2(p, pa, pb);
-    unpack2(t, ta, tb);
-    ra = __int_as_float(__float_as_int(pa) + (__float_as_int(ta) << 23));
-    rb = __int_as_float(__float_as_int(pb) + (__float_as_int(tb) << 23));
-}
-
-// p = exp2(s*c - m) for 32 scores -> 16 packed bf16 pairs; row-sum partials in acc0/acc1.
-template <int NEMU = SPLAT_NEMU>
-__device__ __forceinline__ void exp32(const float *v, uint64_t cc, uint64_t mm, uint64_t &acc0, uint64_t &acc1,
-                                      uint32_t *pw)
-{
-#pragma unroll
-    for (int x = 0; x < 32; x += 4) {
-        const uint64_t z0 = ffma2(pack2(v[x], v[x + 1]), cc, mm);
-        const uint64_t z1 = ffma2(pack2(v[x + 2], v[x + 3]), cc, mm);
-        float a, b, c, d;
-        if (x < NEMU) {
-            exp2_emu2(z0, a, b);
-            exp2_emu2(z1, c, d);
-        } else {
-            unpack2(z0, a, b);
-            unpack2(z1, c, d);
-            a = ex2(a); b = ex2(b); c = ex2(c); d = ex2(d);
-        }
-        acc0 = fadd2(acc0, pack2(a, b));
-        acc1 = fadd2(acc1, pack2(c, d));
-        pw[x / 2] = pack_bf16(a, b);
-        pw[x / 2 + 1] = pack_bf16(c, d);
-    }
-}
-
-__device__ __forceinline__ void apply_mask(float *v, uint32_t m)
-{
-#pragma unroll
-    for (int x = 0; x < 32; ++x) v[x] = ((m >> x) & 1u) ? v[x] : -INFINITY;
-}
+using namespace smx;
 
 // VIEW: residue-major 4-D views (strided-row residue pass, permuted plain STRIDED); a separate
 // instantiation so the natural-order kernel carries none of the view arithmetic.
@@ -498,7 +397,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const uint32_t vbase = sV + pst * C::kTileBytes;                                                 \
         if (elect_one()) {                                                                               \
             _Pragma("unroll") for (int kk = 0; kk < 8; ++kk)                                             \
-                if (!(prm.dbg & 1))                                                                      \
+                if (!(DBG(1)))                                                                      \
                     mma_bf16_ts(o_tm, p_tm + kk * 8, sdesc_sw128(vbase + kk * 2048, kTileBytes64, 1024), \
                                 idO, (first && kk == 0) ? 0u : 1u);                                      \
             mma_commit(&v_empty[pst]);                                                                   \
@@ -544,7 +443,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t off = (kk >> 2) * kTileBytes64 + (kk & 3) * 32;
-                        if (!(prm.dbg & 1))
+                        if (!(DBG(1)))
                             mma_bf16_ss(s_tm, sdesc_sw128(qb + off, 16, 1024), sdesc_sw128(kbase + off, 16, 1024),
                                         idS, kk > 0 ? 1u : 0u);
                     }
@@ -741,7 +640,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 const float mref = m_run == -INFINITY ? 0.f : m_run;
                 const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
                 uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
-                if (prm.dbg & 2) live = 0;
+                if DBG(2) live = 0;
                 // exponentials first (registers): SEP -- the previous PV has long finished when O is
                 // rescaled and P rewritten; non-SEP -- P overwrites S's columns (all of S is in
                 // registers already) and S(j) was computed after PV(j-1), so O is final here
@@ -815,10 +714,10 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
     }
 }
 
+#ifdef SPLAT_FUSED_PROF
 // Profiling aid (SPLAT_FUSED_PROF build): cycles each warp of CTA 0 spends in each barrier wait
 // of the split kernel (by call site) and in total; read with splat_debug_fused_prof.
 __device__ unsigned long long g_fprof[12][16];
-#ifdef SPLAT_FUSED_PROF
 #define FWAIT(SITE, BAR, PH)                                                                    \
     do {                                                                                        \
         const unsigned long long t0_ = clock64();                                               \
@@ -971,7 +870,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         auto load_v = [&]() {
             if (vc >= C::KS) FWAIT(10, &v_empty[vi], vph ^ 1);
             if (lane == 0) {
-                if (prm.dbg & 16) {          // profiling aid: no TMA traffic (garbage K/V)
+                if DBG(16) {          // profiling aid: no TMA traffic (garbage K/V)
                     mbar_arrive(&v_full[vi]);
                 } else {
                     mbar_expect_tx(&v_full[vi], C::TB);
@@ -1024,7 +923,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 if (kc >= C::KS) FWAIT(9, &k_empty[ki], kph ^ 1);
                 TRACE(g == 0 ? 0 : 5, 31);
                 if (lane == 0) {
-                    if (prm.dbg & 16) {
+                    if DBG(16) {
                         mbar_arrive(&k_full[ki]);
                     } else {
                         mbar_expect_tx(&k_full[ki], C::TB);
@@ -1059,7 +958,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         constexpr uint32_t idO = idesc_bf16(128, D, true);
         const uint32_t sQ = smem_u32(gsu + C::OFF_Q), sK = smem_u32(gsu + C::OFF_K), sV = smem_u32(gsu + C::OFF_V);
         const uint32_t s_tm = tmu + gu * 128, o_tm = tmu + 256 + gu * D, p_tm = tmu + 384 + gu * 64;
-        const bool no_mma = (prm.dbg & 1) != 0;
+        const bool no_mma = (DBG(1)) != 0;
         int qi = 0;
         uint32_t qph = 0, pcnt = 0, scnt = 0, gent = 0;
         // the pending PV (entry whose P the softmax is computing)
@@ -1271,7 +1170,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 const float mref = m_run == -INFINITY ? 0.f : m_run;
                 const uint64_t cc = pack2(c2, c2), mm = pack2(-mref, -mref);
                 uint64_t acc0 = pack2(0.f, 0.f), acc1 = acc0;
-                if (prm.dbg & 2) live = 0;
+                if DBG(2) live = 0;
                 uint32_t pw[64];
 #pragma unroll
                 for (int w = 0; w < 4; ++w) {
@@ -1384,10 +1283,7 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     p.N = A.n;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.O = reinterpret_cast<__nv_bfloat16 *>(O);
-    static const int dbg = [] {
-        const char *e = getenv("SPLAT_TC_DEBUG");
-        return e ? atoi(e) : 0;
-    }();
+    static const int dbg = diag_env("SPLAT_TC_DEBUG");
     p.dbg = dbg;
     p.view = ra.view;
     p.merge = ra.merge;
@@ -1427,10 +1323,7 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
     p.N = A.n;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.O = reinterpret_cast<__nv_bfloat16 *>(O);
-    static const int dbg = [] {
-        const char *e = getenv("SPLAT_TC_DEBUG");
-        return e ? atoi(e) : 0;
-    }();
+    static const int dbg = diag_env("SPLAT_TC_DEBUG");
     p.dbg = dbg;
     p.sched = A.sched;
     if (!p.sched) return cudaErrorInvalidValue;
@@ -1443,6 +1336,7 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
 
 }  // namespace
 
+#ifdef SPLAT_DIAG
 extern "C" int splat_debug_hang(unsigned long long *out)
 {
 #ifdef SPLAT_HANG_DEBUG
@@ -1456,10 +1350,15 @@ extern "C" int splat_debug_hang(unsigned long long *out)
 
 extern "C" int splat_debug_fused_prof(unsigned long long *out)
 {
+#ifdef SPLAT_FUSED_PROF
     cudaMemcpyFromSymbol(out, g_fprof, sizeof(g_fprof));
     static const unsigned long long z[12 * 16] = {};
     cudaMemcpyToSymbol(g_fprof, z, sizeof(z));
     return 0;
+#else
+    (void)out;
+    return 1;
+#endif
 }
 
 extern "C" int splat_debug_trace(unsigned long long *out, int *counts)
@@ -1470,6 +1369,7 @@ extern "C" int splat_debug_trace(unsigned long long *out, int *counts)
     cudaMemcpyToSymbol(g_trace_n, z, sizeof(z));
     return 0;
 }
+#endif  // SPLAT_DIAG
 
 cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int l, int nk, int R, float *lse,
                                    const void *Q, const void *K, const void *V, int BH, int d, float scale, void *O,
@@ -1513,11 +1413,11 @@ cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const
                            float scale, void *O, cudaStream_t st, int *n_launch)
 {
     *n_launch = 1;
-    static const bool paired64 = [] {
-        const char *e = getenv("SPLAT_TC_PAIRED64");     // diagnostics: the paired kernel at d = 64
-        return e && atoi(e) != 0;
-    }();
-    if (d == 64 && !paired64) return launch_split64(A, Q, K, V, BH, scale, O, st);
+    // diagnostics build only: SPLAT_TC_PAIRED64=1 runs the paired kernel at d = 64, =2 the round-1
+    // split-group kernel; product: the streaming d = 64 kernel (tc_fused64.cu)
+    static const int alt64 = diag_env("SPLAT_TC_PAIRED64");
+    if (d == 64 && alt64 == 0) return launch_mhsa64(A, Q, K, V, BH, scale, O, st);
+    if (d == 64 && alt64 == 2) return launch_split64(A, Q, K, V, BH, scale, O, st);
     if (d == 64) return launch_d<64>(A, Q, K, V, BH, scale, O, st);
     if (d == 128) return launch_d<128>(A, Q, K, V, BH, scale, O, st);
     return cudaErrorNotSupported;

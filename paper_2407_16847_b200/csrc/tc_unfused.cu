@@ -63,10 +63,13 @@ struct ParamsU {
     long long nat_nnz;
 };
 
+#if defined(SPLAT_UNF_PROF) && !defined(SPLAT_DIAG)
+#error "SPLAT_UNF_PROF needs the diagnostics build (-DSPLAT_DIAG)"
+#endif
+#ifdef SPLAT_UNF_PROF
 // Profiling aid (SPLAT_UNF_PROF build): cycles each warp of CTA 0 spends in barrier waits, by
 // call site, and in total; read with splat_debug_unf_prof.
 __device__ unsigned long long g_unf_prof[32][8];
-#ifdef SPLAT_UNF_PROF
 #define PWAIT(SITE, BAR, PH)                                                                    \
     do {                                                                                        \
         const unsigned long long t0_ = clock64();                                               \
@@ -824,6 +827,7 @@ cudaError_t launch_rspmm_tc(const DevAcsr &A, const void *P, const void *V, int 
 
 }  // namespace splat
 
+#ifdef SPLAT_UNF_PROF
 extern "C" int splat_debug_unf_prof(unsigned long long *out)
 {
     cudaMemcpyFromSymbol(out, splat::g_unf_prof, sizeof(splat::g_unf_prof));
@@ -831,3 +835,4 @@ extern "C" int splat_debug_unf_prof(unsigned long long *out)
     cudaMemcpyToSymbol(splat::g_unf_prof, z, sizeof(z));
     return 0;
 }
+#endif

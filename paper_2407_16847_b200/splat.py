@@ -13,7 +13,10 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
+# SPLAT_LIB=diag selects the diagnostics build (profiling / ablation knobs; tools/ only -- bench.py
+# refuses to run with any SPLAT_* variable set).  Default: the product library.
 LIB_PATH = os.path.join(_PKG, "libsplat.so")
+DIAG_LIB_PATH = os.path.join(_PKG, "libsplat_diag.so")
 
 SPLAT_MAX_SEGS = 4
 STATUS = {0: "SPLAT_OK", 1: "SPLAT_ERR_INVALID_ARG", 2: "SPLAT_ERR_NOT_REGULAR", 3: "SPLAT_ERR_SHAPE",
@@ -59,9 +62,10 @@ def lib():
     """Load libsplat.so (raises if it is missing: no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} not built: run `python -m paper_2407_16847_b200.build`")
-        L = C.CDLL(LIB_PATH)
+        path = DIAG_LIB_PATH if os.environ.get("SPLAT_LIB") == "diag" else LIB_PATH
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} not built: run `python -m paper_2407_16847_b200.build`")
+        L = C.CDLL(path)
         vp, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
         P = C.POINTER
         L.splat_acsr_build.argtypes = [P(splat_pattern), C.c_int, vp, P(vp)]

@@ -1,6 +1,8 @@
 """Split-kernel wait profile (SPLAT_FUSED_PROF build): per warp of CTA 0, % of cycles per wait site."""
 import ctypes as C
 import os
+
+os.environ.setdefault("SPLAT_LIB", "diag")     # profiling hooks live in libsplat_diag.so
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

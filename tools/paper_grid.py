@@ -71,6 +71,7 @@ def main():
     a = ap.parse_args()
     if a.ablate:
         os.environ["SPLAT_PLAN_ABLATE"] = str(a.ablate)
+        os.environ["SPLAT_LIB"] = "diag"          # the ablation knob exists only in libsplat_diag.so
     dev = 0
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)

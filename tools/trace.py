@@ -1,6 +1,8 @@
 """Debug aid: pipeline timeline of CTA 0 of the fused kernel (SPLAT_TC_DEBUG=4)."""
 import ctypes as C
 import os
+
+os.environ.setdefault("SPLAT_LIB", "diag")     # profiling hooks live in libsplat_diag.so
 import sys
 
 os.environ["SPLAT_TC_DEBUG"] = str(4 | int(os.environ.get("SPLAT_TC_DEBUG_EXTRA", "0")))
