@@ -1413,11 +1413,11 @@ cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const
                            float scale, void *O, cudaStream_t st, int *n_launch)
 {
     *n_launch = 1;
-    // diagnostics build only: SPLAT_TC_PAIRED64=1 runs the paired kernel at d = 64, =2 the round-1
-    // split-group kernel; product: the streaming d = 64 kernel (tc_fused64.cu)
+    // d = 64: the split-group kernel.  Diagnostics build only: SPLAT_TC_PAIRED64=1 runs the paired
+    // kernel, =3 the half-row double-buffered kernel of tc_fused64.cu (experimental)
     static const int alt64 = diag_env("SPLAT_TC_PAIRED64");
-    if (d == 64 && alt64 == 0) return launch_mhsa64(A, Q, K, V, BH, scale, O, st);
-    if (d == 64 && alt64 == 2) return launch_split64(A, Q, K, V, BH, scale, O, st);
+    if (d == 64 && alt64 == 0) return launch_split64(A, Q, K, V, BH, scale, O, st);
+    if (d == 64 && alt64 == 3) return launch_mhsa64(A, Q, K, V, BH, scale, O, st);
     if (d == 64) return launch_d<64>(A, Q, K, V, BH, scale, O, st);
     if (d == 128) return launch_d<128>(A, Q, K, V, BH, scale, O, st);
     return cudaErrorNotSupported;
