@@ -2,39 +2,49 @@
 """Benchmark of the fused SPLAT sparse-MHSA hot path on B200 (one JSON line).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1)
 
 Metric (BASELINE.json): fused sparse-MHSA nnz-counted TFLOP/s (4*nnz*d per
 (b, h), SURVEY A-14) and its fraction of the B200 roofline.  A step is one
 splat_sparse_mhsa call (rows a1/a2 -- ACSR + plan -- are built once per
-pattern, outside the step, exactly as the paper's compile-once/launch-many
-workflow, Listing 4) over one batch of synthetic Q/K/V of the
-config's shape (workloads.py), resident in HBM.  L2 is flushed (a 256 MiB
-write) before every timed step, and each step is timed with CUDA events on
-the launching stream; ms_per_step is the mean over the K steps, max over
-ranks.  Multi-GPU: one process per GPU, every rank runs its own batch of
-independent (b, h) units (weak scaling, no collective on the data path;
-NCCL only for the barrier and the max-over-ranks time).
+pattern, outside the step, as the paper's compile-once/launch-many workflow,
+Listing 4) over one batch of synthetic Q/K/V of the config's shape
+(workloads.py), resident in HBM.  L2 is flushed (a 256 MiB write) before every
+timed step, and each step is timed with CUDA events on the launching stream;
+ms_per_step is the mean over the K steps, max over ranks.
+
+Multi-GPU: ``--gpus N`` launches N ranks (torch.distributed.run,
+one process per GPU, NCCL) when the script is not already running under a
+launcher.  The config's B*H (b, h) units are split into contiguous blocks of
+B*H/N per rank (strong scaling; ``--scaling weak`` gives every rank a full
+batch).  No collective on the data path; outside the timed region O is
+all-gathered over NCCL and every rank's first and last slices are compared
+BITWISE with a one-device recomputation, and sampled rows with the fp64 oracle.
 
 ``e2e`` is the same metric through splat_sparse_mhsa_host with pinned host
 buffers: H2D of Q, K, V, the kernel and D2H of O inside the timed region.
+``per_config`` (N = 1) measures the other BASELINE configs in the same run.
 ``cpu_baseline`` is the fp64 oracle (oracle/) timed on the host's cores on a
-bounded sample of the same workload (rank 0, N=1 only).
-``--impl reference`` times that oracle as the reference arm.
+bounded sample of the same workload (rank 0, N=1 only).  ``--impl reference``
+times that oracle as the reference arm.
+
+The library is the product build (libsplat.so): the script refuses to run when
+any SPLAT_* environment variable is set (those select diagnostics builds or
+knobs), and records that in the line.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
-
-import numpy as np
 import os
+import platform
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
 
+import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -46,14 +56,15 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                   "sm_max_mhz": 1965.0}
 DEFAULT_CONFIG = "longformer"          # BASELINE.json configs[1]
+METRIC = "fused sparse-MHSA nnz-counted TFLOP/s"
 
 
 def load_peaks():
     try:
         with open(PEAKS_PATH) as f:
-            return json.load(f), "measured"
+            return json.load(f), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return dict(FALLBACK_PEAKS), "fallback"
+        return dict(FALLBACK_PEAKS), "fallback (B200_PROFILING.md)"
 
 
 def dist_env():
@@ -61,6 +72,29 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def refuse_knobs():
+    bad = sorted(k for k in os.environ if k.startswith("SPLAT_"))
+    if bad:
+        sys.stderr.write(f"bench.py: refusing to run with {bad} set (diagnostics knobs / builds are not "
+                         "product runs); unset them\n")
+        sys.exit(2)
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(n: int) -> int:
+    """Re-run this script under torch.distributed.run with n ranks on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------
@@ -120,13 +154,23 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle (cpu_baseline / reference arm)
 # ---------------------------------------------------------------------------
-def oracle_sample(cfg, seconds_target: float = 15.0):
-    """Bounded sample of the workload for the oracle: the first H_s (b,h) slices
-    (all rows), plus rows [0, R) of one more slice, sized so the fp64 oracle
-    needs about ``seconds_target`` s at ~1 GFLOP/s per thread (measured rate of
-    the oracle on the GPU box).  Returns (full_heads, extra_rows, flops, threads)."""
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
+
+
+def oracle_sample(cfg, seconds_target: float = 15.0, threads: int | None = None):
+    """Bounded sample of the workload for the oracle: the first H_s (b,h) slices (all rows),
+    plus rows [0, R) of one more slice, sized so the fp64 oracle needs about ``seconds_target`` s
+    at ~1 GFLOP/s per thread.  Returns (full_heads, extra_rows, flops, threads)."""
     from oracle import oracle as O
-    threads = O.default_threads()
+    threads = threads or O.default_threads()
     budget = seconds_target * 1.0e9 * threads
     if cfg.N <= 8192:
         row_ptr = O.acsr(cfg.pattern)[2]
@@ -169,6 +213,16 @@ def sample_text(cfg, full, rows, threads):
     return s + f"; fp64 oracle, {threads} threads"
 
 
+def cpu_baseline(cfg, seconds: float) -> dict:
+    full, rows, oflops, threads = oracle_sample(cfg, seconds_target=seconds)
+    ts = time_oracle(cfg, full, rows, threads, reps=1)
+    tiny = CONFIG_BY_NAME["tiny"]
+    t1 = time_oracle(tiny, 1, 0, 1, reps=1)[0]             # single-thread tiny time
+    return {"value": oflops / ts[0] / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": sample_text(cfg, full, rows, threads) + f"; {ts[0]:.1f} s",
+            "cpu_model": cpu_model(), "tiny_single_thread_s": t1}
+
+
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -180,12 +234,13 @@ def run_reference(args, cfg):
     value = flops / sec / 1e12
     sample = sample_text(cfg, full, rows, threads)
     line = {
-        "impl": "reference", "metric": "fused sparse-MHSA nnz-counted TFLOP/s", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "B": cfg.B, "H": cfg.H, "N": cfg.N, "d": cfg.d,
                    "pattern": cfg.pattern.__dict__, "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -196,7 +251,7 @@ def run_reference(args, cfg):
 # GPU arm
 # ---------------------------------------------------------------------------
 def load_traffic(cfg_name: str):
-    """dram bytes per launch of the fused kernel from the committed ncu summary (or None)."""
+    """DRAM bytes per launch of the fused kernel from the committed ncu --set full summary (or None)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
@@ -206,9 +261,105 @@ def load_traffic(cfg_name: str):
         return None
 
 
+def roofline(cfg, nnz: int, nbh: int, ms: float, peaks: dict, peak_src: str) -> dict:
+    """Dominant-kernel roofline for one launch over nbh (b,h) slices taking ms milliseconds."""
+    kernel_tflops = 4.0 * nnz * cfg.d * nbh / (ms * 1e-3) / 1e12
+    if cfg.dtype == "bf16":
+        ai = 4.0 * nnz * cfg.d / (4.0 * cfg.N * cfg.d * 2)       # FLOP per compulsory byte (Q, K, V, O once)
+        ridge = peaks["bf16_tflops"] * 1e3 / peaks["hbm_gbs"]
+        if ai >= ridge:
+            r = {"bound": "tensor", "achieved": kernel_tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s"}
+        else:
+            gbs = 4.0 * cfg.N * cfg.d * 2 * nbh / (ms * 1e-3) / 1e9
+            r = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+        r["arith_intensity"] = ai
+    else:
+        alu_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12   # SIMT fp32 FFMA (DESIGN §6)
+        r = {"bound": "alu", "achieved": kernel_tflops, "peak": alu_peak, "unit": "TFLOP/s"}
+    r["frac"] = r["achieved"] / r["peak"]
+    r["peak_source"] = peak_src
+    return r
+
+
+def time_steps(step, stream, steps: int, warmup: int, flush, dev: int, sync_ranks=None):
+    """CUDA-event time of `steps` calls of step() after `warmup`, L2 flushed before each timed call."""
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if sync_ranks:
+        sync_ranks()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        for i in range(steps):
+            if flush is not None:
+                flush.fill_(float(i))                       # evict L2 (256 MiB > 126 MB)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if sync_ranks:
+        sync_ranks()
+    ms = [a.elapsed_time(b) for a, b in ev]
+    return sum(ms) / len(ms), clk.result()
+
+
+def device_inputs(cfg, nbh: int, dev, seed: int):
+    """Seeded uniform [-1, 1) Q, K, V generated on the device (per_config timing only)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    out = []
+    for _ in range(3):
+        x = torch.rand((1, nbh, cfg.N, cfg.d), generator=g, device=dev, dtype=torch.float32) * 2 - 1
+        out.append(x.to(cfg.torch_dtype))
+    return out
+
+
+def plan_stats(acsr) -> dict:
+    bm, bn, nq, ne = acsr.plan_info()
+    return {"tile": [bm, bn], "query_tiles": nq, "entries_per_head": ne,
+            "tile_efficiency": acsr.nnz / float(max(1, ne) * bm * bn)}
+
+
+def per_config_line(S, cfg, dev, stream, flush, peaks, peak_src, steps: int) -> dict:
+    """One BASELINE config on this GPU (all B*H slices, device-generated inputs)."""
+    acsr = S.Acsr(cfg.pattern, device=dev)
+    Q, K, V = device_inputs(cfg, cfg.BH, dev, 7 + cfg.index)
+    O = torch.empty_like(Q)
+
+    def step():
+        S.splat_sparse_mhsa(acsr, Q, K, V, O, cfg.scale, stream)
+
+    ms, clk = time_steps(step, stream, steps, 3, flush, dev)
+    launches = S.last_launch_count()
+    ok = bool(torch.isfinite(O.float()).all())
+    flops = acsr.flops(1, cfg.BH, cfg.d)
+    line = {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms, "steps": steps,
+            "B": cfg.B, "H": cfg.H, "N": cfg.N, "d": cfg.d, "dtype": cfg.dtype, "nnz_per_head": acsr.nnz,
+            "density": acsr.density, "plan": plan_stats(acsr), "launches_per_step": launches,
+            "roofline": roofline(cfg, acsr.nnz, cfg.BH, ms, peaks, peak_src), "clocks": clk, "finite": ok,
+            "data": "synthetic, device-generated uniform [-1, 1)"}
+    acsr.destroy()
+    del Q, K, V, O
+    torch.cuda.empty_cache()
+    return line
+
+
+def oracle_rows_check(cfg, host, O_host, bh_global, n_slices: int = 2, rows: int = 64) -> float:
+    """Max-abs error of the first `rows` rows of `n_slices` slices against the fp64 oracle."""
+    from oracle import oracle as O
+    err = 0.0
+    for i in range(min(n_slices, O_host.shape[1])):
+        ref = O.attention(cfg.pattern, host[0][0, i], host[1][0, i], host[2][0, i], cfg.scale, rows=(0, rows))
+        got = O_host[0, i, :rows].float().numpy()
+        err = max(err, float(np.max(np.abs(got - ref))))
+    return err
+
+
 def run_ours(args, cfg):
     import torch.distributed as dist
     from paper_2407_16847_b200 import splat as S
+    from paper_2407_16847_b200.shard import bh_range, gather_and_check
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -217,10 +368,11 @@ def run_ours(args, cfg):
     dev = torch.cuda.current_device()
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
+    sync_ranks = dist.barrier if ws > 1 else None
 
-    from paper_2407_16847_b200.shard import bh_range
     B, H = cfg.B, cfg.H
-    bh = bh_range(B * H, rank, ws, args.scaling if ws > 1 else "weak")
+    scaling = args.scaling if ws > 1 else "strong"
+    bh = bh_range(B * H, rank, ws, scaling)
     nbh = len(bh)
     dt = cfg.torch_dtype
     host = [make_tensor(cfg.index, t, 1, 1, cfg.N, cfg.d, dt, bh).view(1, nbh, cfg.N, cfg.d).pin_memory()
@@ -234,46 +386,19 @@ def run_ours(args, cfg):
     def step():
         S.splat_sparse_mhsa(acsr, Q, K, V, O, cfg.scale, stream)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
+    ms_step, clocks = time_steps(step, stream, args.steps, args.warmup, None if args.no_flush else flush, dev,
+                                 sync_ranks)
     launches_per_step = S.last_launch_count()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(dev) as clk:
-        for i in range(args.steps):
-            if not args.no_flush:
-                flush.fill_(float(i))                       # evict L2 (256 MiB > 126 MB)
-            ev[i][0].record(stream)
-            step()
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    ms = [a.elapsed_time(b) for a, b in ev]
-    ms_step = sum(ms) / len(ms)
     if not torch.isfinite(O.float()).all():
         raise RuntimeError("non-finite output")
 
     # e2e through the C ABI with pinned host buffers (H2D + kernel + D2H per step)
     Oh = torch.empty_like(host[0]).pin_memory()
-    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
 
     def e2e_step():
         S.splat_sparse_mhsa_host(acsr, host[0], host[1], host[2], Oh, cfg.scale, Q, K, V, O, stream)
 
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
-    torch.cuda.synchronize()
-    for i in range(args.steps):
-        e2e_ev[i][0].record(stream)
-        e2e_step()
-        e2e_ev[i][1].record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev) / args.steps
+    e2e_ms, _ = time_steps(e2e_step, stream, args.steps, max(1, args.warmup), None, dev, sync_ranks)
     h2d = sum(h.numel() * h.element_size() for h in host)
     d2h = Oh.numel() * Oh.element_size()
 
@@ -284,49 +409,65 @@ def run_ours(args, cfg):
     total_flops = flops * ws
     value = total_flops / (ms_step * 1e-3) / 1e12
 
+    # ---- validation (outside the timed region)
+    S.splat_sparse_mhsa(acsr, Q, K, V, O, cfg.scale, stream)
+    torch.cuda.synchronize()
+    validation = {}
+    if ws > 1 and scaling == "strong":
+        def recompute(idx):
+            qkv = [make_tensor(cfg.index, t, 1, 1, cfg.N, cfg.d, dt, idx).view(1, len(idx), cfg.N, cfg.d).to(dev)
+                   for t in (0, 1, 2)]
+            o = torch.empty_like(qkv[0])
+            S.splat_sparse_mhsa(acsr, qkv[0], qkv[1], qkv[2], o, cfg.scale, stream)
+            torch.cuda.synchronize()
+            return o[0]
+        validation.update(gather_and_check(O[0], recompute))
+    validation["oracle_rows_maxabs"] = oracle_rows_check(cfg, host, O.cpu(), bh)
+    validation["oracle_rows_checked"] = "rows [0, 64) of this rank's first 2 slices"
+    validation["tolerance"] = 2e-2 if cfg.dtype == "bf16" else 1e-5
+    validation["ok"] = validation["oracle_rows_maxabs"] <= validation["tolerance"] and \
+        validation.get("bitwise_equal_to_one_device", True)
+
     peaks, peak_src = load_peaks()
-    kernel_tflops = flops / (ms_step * 1e-3) / 1e12          # per-GPU, per launch
-    if cfg.dtype == "bf16":
-        ai = 4.0 * acsr.nnz * cfg.d / (4.0 * cfg.N * cfg.d * 2)  # FLOP per compulsory byte
-        ridge = peaks["bf16_tflops"] * 1e3 / peaks["hbm_gbs"]
-        if ai >= ridge:
-            roof = {"bound": "tensor", "achieved": kernel_tflops, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s"}
-        else:
-            gbs = 4.0 * cfg.N * cfg.d * 2 * nbh / (ms_step * 1e-3) / 1e9
-            roof = {"bound": "hbm", "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
-    else:
-        alu_peak = 148 * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12   # SIMT fp32 FFMA
-        roof = {"bound": "alu", "achieved": kernel_tflops, "peak": alu_peak, "unit": "TFLOP/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["peak_source"] = peak_src
+    roof = roofline(cfg, acsr.nnz, nbh, ms_step, peaks, peak_src)
     roof["traffic"] = load_traffic(cfg.name)
+    roof["traffic_source"] = "profiles/ncu_summary.json (ncu --set full, dram read+write per launch)"
 
     line = {
-        "metric": "fused sparse-MHSA nnz-counted TFLOP/s", "value": value, "unit": "TFLOP/s",
+        "metric": METRIC, "value": value, "unit": "TFLOP/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak" if args.scaling == "weak" or ws == 1 else "strong",
+        "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": cfg.dtype if cfg.dtype != "fp32" else "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "B": B, "H": H, "N": cfg.N, "d": cfg.d, "bh_per_rank": nbh,
                    "pattern": cfg.pattern.__dict__, "nnz_per_head": acsr.nnz, "density": acsr.density,
-                   "l2": "warm (diagnostic --no-flush)" if args.no_flush else "flushed before every timed step (256 MiB write)", "parallelism": f"bh-shard x{ws}"},
+                   "plan": plan_stats(acsr),
+                   "l2": "warm (diagnostic --no-flush)" if args.no_flush else "flushed before every timed step (256 MiB write)",
+                   "parallelism": f"(b,h)-shard x{ws} ({scaling})"},
         "roofline": roof,
         "e2e": {"value": total_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.result(),
+        "clocks": clocks,
+        "validation": validation,
+        "library": {"so": os.path.basename(S.LIB_PATH), "knobs": "none (SPLAT_* refused)"},
     }
+    acsr.destroy()
+    del Q, K, V, O
+    torch.cuda.empty_cache()
+    if ws == 1 and not args.no_per_config:
+        line["per_config"] = {}
+        for c in CONFIGS:
+            if c.name == cfg.name:
+                continue
+            line["per_config"][c.name] = per_config_line(S, c, dev, stream, flush, peaks, peak_src,
+                                                         5 if c.name == "mistral" else 20)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        full, rows, oflops, threads = oracle_sample(cfg, seconds_target=args.cpu_seconds)
-        ts = time_oracle(cfg, full, rows, threads, reps=1)
-        line["cpu_baseline"] = {
-            "value": oflops / ts[0] / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-            "sample": sample_text(cfg, full, rows, threads) + f"; {ts[0]:.1f} s"}
+        line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
-    acsr.destroy()
-    return 0
+    return 0 if validation["ok"] else 1
 
 
 def main():
@@ -336,13 +477,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=[c.name for c in CONFIGS])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostics only: keep L2 warm between steps")
     args = ap.parse_args()
+    refuse_knobs()
     if args.warmup < 3:
         args.warmup = 3
+    ws, _, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args.gpus)
+    if ws != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+        return 2
+    if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")            # communicator logs: rank count on stderr
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     cfg = CONFIG_BY_NAME[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)

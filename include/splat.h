@@ -345,6 +345,11 @@ double splat_flops(splat_acsr a, int32_t B, int32_t H, int32_t d);
  * issued (instrumentation for the bench's gpu_launches count). */
 int32_t splat_last_launch_count(void);
 
+/* Number of device allocations the library has made in this process (all of
+ * them at handle build time: compute calls never allocate, SURVEY §8(b)
+ * "Ownership"; the tests check the count does not move across compute calls). */
+int64_t splat_device_alloc_count(void);
+
 /* Thread-local message describing the last error on this thread ("" if none). */
 const char *splat_last_error(void);
 

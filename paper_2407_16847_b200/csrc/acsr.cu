@@ -189,7 +189,7 @@ cudaError_t launch_acsr_scan(int64_t *row_ptr, int n, cudaStream_t st)
     }
     const int nb = (n + TILE - 1) / TILE;
     int64_t *sums = nullptr;
-    cudaError_t e = cudaMallocAsync(&sums, sizeof(int64_t) * (size_t)nb, st);
+    cudaError_t e = dev_alloc_async(reinterpret_cast<void **>(&sums), sizeof(int64_t) * (size_t)nb, st);
     if (e != cudaSuccess) return e;
     acsr_tile_sum_kernel<<<nb, 1024, 0, st>>>(row_ptr, n, sums);
     acsr_scan_kernel<<<1, 1024, 0, st>>>(sums - 1, nb);     // inclusive scan of sums[0..nb-1]

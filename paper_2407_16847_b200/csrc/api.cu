@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <new>
 
 #include "kernels.h"
@@ -16,6 +17,20 @@
 namespace splat {
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_allocs{0};
+
+// Every device allocation of the library goes through here (build time only: compute calls never
+// allocate; splat_device_alloc_count lets the tests check that).
+cudaError_t dev_alloc_bytes(void **p, size_t bytes)
+{
+    g_allocs.fetch_add(1, std::memory_order_relaxed);
+    return cudaMalloc(p, bytes);
+}
+cudaError_t dev_alloc_async(void **p, size_t bytes, cudaStream_t st)
+{
+    g_allocs.fetch_add(1, std::memory_order_relaxed);
+    return cudaMallocAsync(p, bytes, st);
+}
 static thread_local int g_launches = 0;
 
 splat_status set_error(splat_status st, const char *fmt, ...)
@@ -239,16 +254,16 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
     finish_host_meta(a);
     build_plan(*a);
     Plan &P = a->plan;
-    if ((e = cudaMalloc(&P.d_qt_ptr, sizeof(int32_t) * (P.n_qt + 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_kv, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_order, sizeof(int32_t) * P.n_qt)) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_pair_ent, sizeof(int32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_pair_info, sizeof(int32_t) * 8 * P.n_pairs)) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_qt_bits, sizeof(uint32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_t_info, sizeof(int32_t) * 4 * P.n_qt)) != cudaSuccess ||
-        (e = cudaMalloc(&P.d_sched, kLaunchSlots * 2 * sizeof(unsigned long long))) != cudaSuccess) {
+    if ((e = dev_alloc(&P.d_qt_ptr, sizeof(int32_t) * (P.n_qt + 1))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_kv, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_order, sizeof(int32_t) * P.n_qt)) != cudaSuccess ||
+        (e = dev_alloc(&P.d_pair_ent, sizeof(int32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_pair_info, sizeof(int32_t) * 8 * P.n_pairs)) != cudaSuccess ||
+        (e = dev_alloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_qt_bits, sizeof(uint32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_t_info, sizeof(int32_t) * 4 * P.n_qt)) != cudaSuccess ||
+        (e = dev_alloc(&P.d_sched, kLaunchSlots * 2 * sizeof(unsigned long long))) != cudaSuccess) {
         free_device(a);
         delete a;
         return cuda_fail(e, "plan allocation");
@@ -371,9 +386,9 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
     DeviceGuard g(device);
     cudaStream_t cs = (cudaStream_t)stream;
     cudaError_t e;
-    if ((e = cudaMalloc(&a->d_seg, sizeof(int32_t) * 16 * (size_t)N)) != cudaSuccess ||
-        (e = cudaMalloc(&a->d_nseg, (size_t)N)) != cudaSuccess ||
-        (e = cudaMalloc(&a->d_row_ptr, sizeof(int64_t) * ((size_t)N + 1))) != cudaSuccess) {
+    if ((e = dev_alloc(&a->d_seg, sizeof(int32_t) * 16 * (size_t)N)) != cudaSuccess ||
+        (e = dev_alloc(&a->d_nseg, (size_t)N)) != cudaSuccess ||
+        (e = dev_alloc(&a->d_row_ptr, sizeof(int64_t) * ((size_t)N + 1))) != cudaSuccess) {
         free_device(a);
         delete a;
         return cuda_fail(e, "acsr allocation");
@@ -432,7 +447,7 @@ void build_residue_split(splat_acsr_s *a, void *stream)
         return;
     }
     float *lse = nullptr;
-    if (cudaMalloc(&lse, sizeof(float) * (size_t)kLaunchSlots * kLseHeads * N) != cudaSuccess) {
+    if (dev_alloc(&lse, sizeof(float) * (size_t)kLaunchSlots * kLseHeads * N) != cudaSuccess) {
         cudaGetLastError();
         free_device(hb);
         delete hb;
@@ -616,10 +631,10 @@ splat_status splat_acsr_from_mask(const uint32_t *mask, int32_t n, int32_t max_r
     cudaStream_t cs = (cudaStream_t)stream;
     cudaError_t e;
     unsigned long long *d_bad = nullptr, bad = 0;
-    if ((e = cudaMalloc(&a->d_seg, sizeof(int32_t) * 16 * (size_t)n)) != cudaSuccess ||
-        (e = cudaMalloc(&a->d_nseg, (size_t)n)) != cudaSuccess ||
-        (e = cudaMalloc(&a->d_row_ptr, sizeof(int64_t) * ((size_t)n + 1))) != cudaSuccess ||
-        (e = cudaMalloc(&d_bad, sizeof(unsigned long long))) != cudaSuccess) {
+    if ((e = dev_alloc(&a->d_seg, sizeof(int32_t) * 16 * (size_t)n)) != cudaSuccess ||
+        (e = dev_alloc(&a->d_nseg, (size_t)n)) != cudaSuccess ||
+        (e = dev_alloc(&a->d_row_ptr, sizeof(int64_t) * ((size_t)n + 1))) != cudaSuccess ||
+        (e = dev_alloc(&d_bad, sizeof(unsigned long long))) != cudaSuccess) {
         cudaFree(d_bad);
         free_device(a);
         delete a;
@@ -851,6 +866,8 @@ double splat_flops(splat_acsr a, int32_t B, int32_t H, int32_t d)
 }
 
 int32_t splat_last_launch_count(void) { return g_launches; }
+
+int64_t splat_device_alloc_count(void) { return g_allocs.load(); }
 
 const char *splat_last_error(void) { return g_err; }
 

@@ -30,11 +30,12 @@ struct RowId {
     int bh, i;
 };
 
+template <int W = kWarps>
 __device__ __forceinline__ RowId row_of_warp(int n)
 {
-    const int nrb = (n + kWarps - 1) / kWarps;
+    const int nrb = (n + W - 1) / W;
     const int rb = blockIdx.x;
-    return {rb / nrb, (rb % nrb) * kWarps + (int)(threadIdx.x >> 5)};
+    return {rb / nrb, (rb % nrb) * W + (int)(threadIdx.x >> 5)};
 }
 
 __device__ __forceinline__ int col_of(const int4 *g, int ns, int x)
@@ -277,13 +278,18 @@ rspmm_simt_kernel(DevAcsr A, const T *__restrict__ P, const T *__restrict__ V, i
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kWarps * 32)
+// Fused fp32 / SIMT path: one warp per (b, h, row), W warps (rows) per CTA -- W = 1 spreads a
+// small problem (the tiny config: 256 rows) over 256 CTAs instead of 32.  Per 32-key chunk: lane x
+// computes <q, k_x> (q staged in shared memory), warp-shuffle max / sum (online softmax), then
+// O += p V over the chunk with the V rows of 4 keys loaded before their FMAs (4 loads in flight
+// per lane instead of one dependent load per key).
+template <typename T, int W>
+__global__ void __launch_bounds__(W * 32)
 mhsa_simt_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K, const T *__restrict__ V,
                  int d, float scale, T *__restrict__ O)
 {
     extern __shared__ float qs[];
-    const RowId r = row_of_warp(A.n);
+    const RowId r = row_of_warp<W>(A.n);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (r.i >= A.n) return;
     float *qw = qs + w * d;
@@ -297,6 +303,7 @@ mhsa_simt_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K, co
     const int len = (int)(A.row_ptr[r.i + 1] - A.row_ptr[r.i]);
     const T *Kb = K + (size_t)r.bh * A.n * d;
     const T *Vb = V + (size_t)r.bh * A.n * d;
+    const int nu = (d + 31) >> 5;          // output columns per lane: lane + 32 u, u < nu <= 8
     float m = -INFINITY, l = 0.f, acc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] = 0.f;
@@ -323,15 +330,25 @@ mhsa_simt_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K, co
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc[u] *= alpha;
         const int cnt = min(32, len - e0);
-        for (int j = 0; j < cnt; ++j) {
-            const float pj = __shfl_sync(0xffffffffu, p, j);
-            const int cj = __shfl_sync(0xffffffffu, col, j);
-            const T *vr = Vb + (size_t)cj * d;
+        for (int j0 = 0; j0 < cnt; j0 += 4) {
+            float pj[4], vv[4][8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int t = lane + 32 * u;
-                if (t < d) acc[u] = fmaf(pj, to_f(vr[t]), acc[u]);
+            for (int jj = 0; jj < 4; ++jj) {
+                const int j = min(j0 + jj, 31);
+                pj[jj] = __shfl_sync(0xffffffffu, p, j);
+                const int cj = __shfl_sync(0xffffffffu, col, j);
+                if (j0 + jj >= cnt) pj[jj] = 0.f;            // p of an invalid lane is 0 already
+                const T *vr = Vb + (size_t)cj * d;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int t = lane + 32 * u;
+                    vv[jj][u] = (u < nu && t < d) ? to_f(vr[t]) : 0.f;
+                }
             }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc[u] = fmaf(pj[jj], vv[jj][u], acc[u]);
         }
     }
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -401,14 +418,26 @@ cudaError_t launch_rspmm_simt(const DevAcsr &A, const void *P, const void *V, bo
 cudaError_t launch_mhsa_simt(const DevAcsr &A, const void *Q, const void *K, const void *V, bool bf16,
                              int BH, int d, float scale, void *O, cudaStream_t st)
 {
-    const size_t sm = (size_t)kWarps * d * sizeof(float);
-    if (bf16)
-        mhsa_simt_kernel<__nv_bfloat16><<<grid_rows(A, BH), kWarps * 32, sm, st>>>(
-            A, (const __nv_bfloat16 *)Q, (const __nv_bfloat16 *)K, (const __nv_bfloat16 *)V, d, scale,
-            (__nv_bfloat16 *)O);
-    else
-        mhsa_simt_kernel<float><<<grid_rows(A, BH), kWarps * 32, sm, st>>>(
-            A, (const float *)Q, (const float *)K, (const float *)V, d, scale, (float *)O);
+    // few rows (fewer than 8 per SM): one warp per CTA so every SM gets rows
+    const bool small = (long long)BH * A.n <= 148ll * 8;
+    const int W = small ? 1 : kWarps;
+    const size_t sm = (size_t)W * d * sizeof(float);
+    const dim3 grid((unsigned)(BH * ((A.n + W - 1) / W)));
+    if (bf16) {
+        if (small)
+            mhsa_simt_kernel<__nv_bfloat16, 1><<<grid, 32, sm, st>>>(A, (const __nv_bfloat16 *)Q,
+                (const __nv_bfloat16 *)K, (const __nv_bfloat16 *)V, d, scale, (__nv_bfloat16 *)O);
+        else
+            mhsa_simt_kernel<__nv_bfloat16, kWarps><<<grid, kWarps * 32, sm, st>>>(A, (const __nv_bfloat16 *)Q,
+                (const __nv_bfloat16 *)K, (const __nv_bfloat16 *)V, d, scale, (__nv_bfloat16 *)O);
+    } else {
+        if (small)
+            mhsa_simt_kernel<float, 1><<<grid, 32, sm, st>>>(A, (const float *)Q, (const float *)K,
+                                                              (const float *)V, d, scale, (float *)O);
+        else
+            mhsa_simt_kernel<float, kWarps><<<grid, kWarps * 32, sm, st>>>(A, (const float *)Q, (const float *)K,
+                                                                           (const float *)V, d, scale, (float *)O);
+    }
     return cudaGetLastError();
 }
 

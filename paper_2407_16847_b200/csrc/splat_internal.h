@@ -2,6 +2,7 @@
 #pragma once
 
 #include <atomic>
+#include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
 #include <mutex>
@@ -246,6 +247,10 @@ struct splat_acsr_s {
 };
 
 namespace splat {
+cudaError_t dev_alloc_bytes(void **p, size_t bytes);
+cudaError_t dev_alloc_async(void **p, size_t bytes, cudaStream_t st);
+template <typename T>
+inline cudaError_t dev_alloc(T **p, size_t bytes) { return dev_alloc_bytes(reinterpret_cast<void **>(p), bytes); }
 splat_status set_error(splat_status st, const char *fmt, ...);
 void clear_error();
 void note_launches(int n);

@@ -29,7 +29,8 @@ KINDS = {"window": 0, "blocked": 1, "strided": 2, "dilated": 3, "global_local": 
 EXPORTS = ("splat_acsr_build", "splat_acsr_info", "splat_acsr_copy_meta", "splat_plan_info",
            "splat_plan_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
            "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_acsr_from_mask", "splat_poset_tile", "splat_naive_tile",
-           "splat_tiling_cost_eval", "splat_flops", "splat_last_launch_count", "splat_last_error")
+           "splat_tiling_cost_eval", "splat_flops", "splat_last_launch_count", "splat_device_alloc_count",
+           "splat_last_error")
 
 
 class SplatError(RuntimeError):
@@ -306,6 +307,13 @@ def splat_tiling_cost_eval(pattern, m: int, n: int, stretch: int, anchors) -> di
     _check(lib().splat_tiling_cost_eval(C.byref(to_c_pattern(pattern)), m, n, stretch, a.data_ptr(), a.shape[0],
                                         C.byref(cost)))
     return cost.as_dict()
+
+
+def device_alloc_count() -> int:
+    """Device allocations the library has made so far (build time only)."""
+    L = lib()
+    L.splat_device_alloc_count.restype = C.c_int64
+    return int(L.splat_device_alloc_count())
 
 
 def last_launch_count() -> int:

@@ -149,3 +149,42 @@ def test_density_and_flops():
     a = S.Acsr(p, device=-1)
     assert abs(a.density - a.nnz / p.seq_len ** 2) < 1e-15
     assert a.flops(8, 12, 64) == 4.0 * a.nnz * 64 * 96
+
+
+# ---------------------------------------------------------------------------
+# product build hygiene: no environment knobs, no debug exports, every
+# device allocation through the counted wrapper (build time only)
+# ---------------------------------------------------------------------------
+CSRC = os.path.join(ROOT, "paper_2407_16847_b200", "csrc")
+
+
+def _sources():
+    return [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cpp", ".h", ".cuh"))]
+
+
+def test_no_getenv_outside_the_diagnostics_helper():
+    for f in _sources():
+        txt = open(f).read()
+        for m in re.finditer(r"\bgetenv\s*\(", txt):
+            pre = txt[:m.start()]
+            # the only getenv is diag_env's, compiled under #ifdef SPLAT_DIAG
+            assert os.path.basename(f) == "splat_internal.h", f
+            assert pre.rfind("#ifdef SPLAT_DIAG") > pre.rfind("#endif"), f
+
+
+def test_every_device_allocation_is_counted():
+    for f in _sources():
+        txt = open(f).read()
+        n = len(re.findall(r"\bcudaMalloc(Async)?\s*\(", txt))
+        if os.path.basename(f) == "api.cu":
+            assert n == 2, n          # the two wrappers themselves
+        else:
+            assert n == 0, f
+
+
+def test_product_library_has_no_debug_exports():
+    out = subprocess.check_output(["nm", "-D", "--defined-only", S.LIB_PATH]).decode()
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    for name in ("splat_debug_trace", "splat_debug_fused_prof", "splat_debug_hang", "splat_debug_prof64",
+                 "splat_debug_unf_prof"):
+        assert name not in exported, name
