@@ -842,6 +842,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         for (int gg = 0; gg < 2; ++gg) {
             uint64_t *b = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR) + gg * C::NB;
             for (int i = 0; i < 2 * C::QS + 4 * C::KS; ++i) mbar_init(&b[i], 1);
+            // q_empty: the unit's last PV (MMA commit) and the 4 softmax warps, done with the unit's
+            // header and entry table -- the producer rewrites both only after all five
+            for (int i = 0; i < C::QS; ++i) mbar_init(&b[C::QS + i], 5);
             const int o = 2 * C::QS + 4 * C::KS;
             mbar_init(&b[o + 0], 1);   // s_full  (MMA commit)
             mbar_init(&b[o + 1], 4);   // s_empty (4 softmax warps)
@@ -1121,6 +1124,8 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 SPLAT_NEXT_UNIT_PREFETCH();
                 if (pe_on) { epilogue(pe_l, pe_t, pe_bh); pe_on = false; }
                 epilogue(0.f, un.t, un.bh);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&q_empty[slot]);
                 continue;
             }
             for (int j = j0; j < j1; ++j) {
@@ -1219,6 +1224,8 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 first = false;
             }
 #undef SPLAT_NEXT_UNIT_PREFETCH
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&q_empty[slot]);   // header + entry table of this slot consumed
             pe_on = true;
             pe_l = l_run;
             pe_t = un.t;
