@@ -18,7 +18,7 @@ Q, K, V = q.cuda(), k.cuda(), v.cuda()
 O = torch.empty_like(Q)
 a = S.Acsr(cfg.pattern)
 L = S.lib()
-buf = (C.c_ulonglong * (12 * 16))()
+buf = (C.c_ulonglong * (20 * 16))()
 for it in range(3):
     L.splat_debug_prof64(buf)
     S.splat_sparse_mhsa(a, Q, K, V, O, cfg.scale)
@@ -30,11 +30,12 @@ names = {
     "softmax": {11: "metadata (m_full)", 0: "meta->s_full", 1: "s_full wait", 2: "S ld+wait", 3: "mask+max",
                 4: "max exchange", 5: "bump+exps", 6: "epilogue", 7: "pv_done wait", 8: "O rescale", 9: "P st+arrive"},
 }
-for w in range(12):
+for w in range(int(os.environ.get("NWARPS", "12"))):
     row = [buf[w * 16 + k] for k in range(16)]
     tot = row[15]
     if not tot:
         continue
-    role = "producer" if w == 0 else ("mma" if w == 1 else "softmax")
+    role = os.environ.get("ROLES", "p,m").split(",")[w] if w < len(os.environ.get("ROLES", "p,m").split(",")) else "s"
+    role = {"p": "producer", "m": "mma", "s": "softmax"}[role]
     parts = ", ".join(f"{n}={100 * row[k] / tot:.1f}%" for k, n in names[role].items() if row[k])
     print(f"warp {w:2d} {role:8s} total {tot / 1e6:8.1f} Mcyc: {parts}")
