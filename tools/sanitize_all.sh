@@ -5,7 +5,7 @@ OUT=gpurun_out/${TAG:-r02}_sanitizer.txt
 for tool in memcheck racecheck synccheck; do
   for c in tiny n512_d64 n512_d128 st_d128 str_d64; do
     echo "=== $tool $c" >> $OUT
-    timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_case.py $c >> $OUT 2>&1
+    timeout 300 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_case.py $c >> $OUT 2>&1
     echo "exit $?" >> $OUT
   done
 done
