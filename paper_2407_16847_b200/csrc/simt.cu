@@ -278,8 +278,7 @@ rspmm_simt_kernel(DevAcsr A, const T *__restrict__ P, const T *__restrict__ V, i
     }
 }
 
-// Fused fp32 / SIMT path: one warp per (b, h, row), W warps (rows) per CTA -- W = 1 spreads a
-// small problem (the tiny config: 256 rows) over 256 CTAs instead of 32.  Per 32-key chunk: lane x
+// Fused fp32 / SIMT path: one warp per (b, h, row), W warps (rows) per CTA.  Per 32-key chunk: lane x
 // computes <q, k_x> (q staged in shared memory), warp-shuffle max / sum (online softmax), then
 // O += p V over the chunk with the V rows of 4 keys loaded before their FMAs (4 loads in flight
 // per lane instead of one dependent load per key).
@@ -360,6 +359,94 @@ mhsa_simt_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K, co
     }
 }
 
+// Small problems (fewer than 8 rows per SM, e.g. the tiny config's 256 rows): one CTA of 128
+// threads per (b, h, row), so the row's memory trips are few and wide instead of one warp walking
+// its keys.  Per chunk of 128 keys: thread j computes s_j = scale <q, k_{c_j}> (q in shared
+// memory, the K row read with all loads in flight), block max / sum (online softmax over chunks);
+// then thread t accumulates O[t] (and O[t + 128]) over the chunk's keys, V rows coalesced across
+// threads.  fp32 arithmetic throughout (the paper's FP32).
+constexpr int kRowThreads = 128;
+
+template <typename T>
+__device__ __forceinline__ float dot_full(const float *q, const T *__restrict__ k, int d)
+{
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int t = 0;
+    for (; t + 4 <= d; t += 4) {
+        a0 = fmaf(q[t], to_f(k[t]), a0);
+        a1 = fmaf(q[t + 1], to_f(k[t + 1]), a1);
+        a2 = fmaf(q[t + 2], to_f(k[t + 2]), a2);
+        a3 = fmaf(q[t + 3], to_f(k[t + 3]), a3);
+    }
+    for (; t < d; ++t) a0 = fmaf(q[t], to_f(k[t]), a0);
+    return (a0 + a1) + (a2 + a3);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRowThreads)
+mhsa_simt_row_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K, const T *__restrict__ V, int d,
+                     float scale, T *__restrict__ O)
+{
+    __shared__ float qsh[256];
+    __shared__ float psh[kRowThreads];
+    __shared__ int csh[kRowThreads];
+    __shared__ float rmax[kRowThreads / 32], rsum[kRowThreads / 32];
+    const int bh = blockIdx.x / A.n, i = blockIdx.x % A.n;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const T *q = Q + ((size_t)bh * A.n + i) * d;
+    for (int t = tid; t < d; t += kRowThreads) qsh[t] = to_f(q[t]);
+    int4 g[4];
+    const int ns = A.nseg[i];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) g[s] = A.seg[(size_t)i * 4 + s];
+    const int len = (int)(A.row_ptr[i + 1] - A.row_ptr[i]);
+    const T *Kb = K + (size_t)bh * A.n * d;
+    const T *Vb = V + (size_t)bh * A.n * d;
+    __syncthreads();
+    float m = -INFINITY, l = 0.f, acc0 = 0.f, acc1 = 0.f;
+    for (int e0 = 0; e0 < len; e0 += kRowThreads) {
+        const int e = e0 + tid;
+        const bool valid = e < len;
+        const int col = valid ? col_of(g, ns, e) : 0;
+        const float s = valid ? scale * dot_full(qsh, Kb + (size_t)col * d, d) : -INFINITY;
+        float cm = s;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+        if (lane == 0) rmax[w] = cm;
+        __syncthreads();
+        cm = fmaxf(fmaxf(rmax[0], rmax[1]), fmaxf(rmax[2], rmax[3]));
+        const float mn = fmaxf(m, cm);
+        const float alpha = expf(m - mn);   // m = -inf on the first chunk -> 0
+        const float p = valid ? expf(s - mn) : 0.f;
+        psh[tid] = p;
+        csh[tid] = col;
+        float ps = p;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+        if (lane == 0) rsum[w] = ps;
+        __syncthreads();
+        l = l * alpha + ((rsum[0] + rsum[1]) + (rsum[2] + rsum[3]));
+        m = mn;
+        acc0 *= alpha;
+        acc1 *= alpha;
+        const int cnt = min(kRowThreads, len - e0);
+        if (tid < d) {
+            const bool two = tid + kRowThreads < d;
+#pragma unroll 8
+            for (int j = 0; j < cnt; ++j) {
+                const T *vr = Vb + (size_t)csh[j] * d;
+                acc0 = fmaf(psh[j], to_f(vr[tid]), acc0);
+                if (two) acc1 = fmaf(psh[j], to_f(vr[tid + kRowThreads]), acc1);
+            }
+        }
+        __syncthreads();     // psh / csh / rmax / rsum are rewritten by the next chunk
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    T *o = O + ((size_t)bh * A.n + i) * d;
+    if (tid < d) o[tid] = from_f<T>(acc0 * inv);
+    if (tid + kRowThreads < d) o[tid + kRowThreads] = from_f<T>(acc1 * inv);
+}
+
 inline dim3 grid_rows(const DevAcsr &A, int BH)
 {
     return dim3((unsigned)(BH * ((A.n + kWarps - 1) / kWarps)));
@@ -418,26 +505,26 @@ cudaError_t launch_rspmm_simt(const DevAcsr &A, const void *P, const void *V, bo
 cudaError_t launch_mhsa_simt(const DevAcsr &A, const void *Q, const void *K, const void *V, bool bf16,
                              int BH, int d, float scale, void *O, cudaStream_t st)
 {
-    // few rows (fewer than 8 per SM): one warp per CTA so every SM gets rows
-    const bool small = (long long)BH * A.n <= 148ll * 8;
-    const int W = small ? 1 : kWarps;
-    const size_t sm = (size_t)W * d * sizeof(float);
-    const dim3 grid((unsigned)(BH * ((A.n + W - 1) / W)));
-    if (bf16) {
-        if (small)
-            mhsa_simt_kernel<__nv_bfloat16, 1><<<grid, 32, sm, st>>>(A, (const __nv_bfloat16 *)Q,
+    // few rows (fewer than 8 per SM): one CTA per row so every SM gets work and each row's memory
+    // trips are few and wide
+    if ((long long)BH * A.n <= 148ll * 8 && d <= 256) {
+        const dim3 grid((unsigned)(BH * A.n));
+        if (bf16)
+            mhsa_simt_row_kernel<__nv_bfloat16><<<grid, kRowThreads, 0, st>>>(A, (const __nv_bfloat16 *)Q,
                 (const __nv_bfloat16 *)K, (const __nv_bfloat16 *)V, d, scale, (__nv_bfloat16 *)O);
         else
-            mhsa_simt_kernel<__nv_bfloat16, kWarps><<<grid, kWarps * 32, sm, st>>>(A, (const __nv_bfloat16 *)Q,
-                (const __nv_bfloat16 *)K, (const __nv_bfloat16 *)V, d, scale, (__nv_bfloat16 *)O);
-    } else {
-        if (small)
-            mhsa_simt_kernel<float, 1><<<grid, 32, sm, st>>>(A, (const float *)Q, (const float *)K,
-                                                              (const float *)V, d, scale, (float *)O);
-        else
-            mhsa_simt_kernel<float, kWarps><<<grid, kWarps * 32, sm, st>>>(A, (const float *)Q, (const float *)K,
-                                                                           (const float *)V, d, scale, (float *)O);
+            mhsa_simt_row_kernel<float><<<grid, kRowThreads, 0, st>>>(A, (const float *)Q, (const float *)K,
+                                                                      (const float *)V, d, scale, (float *)O);
+        return cudaGetLastError();
     }
+    const size_t sm = (size_t)kWarps * d * sizeof(float);
+    const dim3 grid((unsigned)(BH * ((A.n + kWarps - 1) / kWarps)));
+    if (bf16)
+        mhsa_simt_kernel<__nv_bfloat16, kWarps><<<grid, kWarps * 32, sm, st>>>(A, (const __nv_bfloat16 *)Q,
+            (const __nv_bfloat16 *)K, (const __nv_bfloat16 *)V, d, scale, (__nv_bfloat16 *)O);
+    else
+        mhsa_simt_kernel<float, kWarps><<<grid, kWarps * 32, sm, st>>>(A, (const float *)Q, (const float *)K,
+                                                                       (const float *)V, d, scale, (float *)O);
     return cudaGetLastError();
 }
 

@@ -11,14 +11,15 @@
 //             writes scale * S of the row's non-zeros with one coalesced store per row.  The
 //             position of (row i, column c) is row_ptr[i] + (runs of row i left of the tile,
 //             closed form) + (popcount of the pattern's row mask left of c).
-//   R-SpMM  : a warp reads each query row's ACSR segment of key tile j with lanes over columns
-//             (coalesced) and expands it into a dense bf16 P tile in 128B-swizzled SMEM (zeros
-//             off the mask); O += P V_j is an SS-MMA (V an MN-major operand), O accumulated in
-//             TMEM over the tile's key tiles and written once as bf16.
+//   R-SpMM  : a query row's non-zeros inside key tile j are one contiguous span of P (ACSR order),
+//             copied with one bulk copy per (row, tile) into an SMEM staging ring and expanded into
+//             a dense bf16 P tile in 128B-swizzled SMEM (zeros off the mask); O += P V_j is an
+//             SS-MMA (V an MN-major operand), O accumulated in TMEM over the tile's key tiles and
+//             written once as bf16.
 //
-// Both kernels run 4 epilogue / gather warpgroups that take the S / P tiles round robin, so
-// four tiles are in flight per SM.  Work units: (b*H+h, 128-row query tile), head-major,
-// query tiles in LPT order; persistent CTAs, one per SM.
+// R-SDDMM runs 4 epilogue warpgroups that take the S tiles round robin (four tiles in flight per
+// SM).  Work units: (b*H+h, 128-row query tile), head-major, query tiles in LPT order; persistent
+// CTAs, one per SM.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -36,14 +37,7 @@ using namespace sm100;
 #endif
 constexpr int kNWG = SPLAT_UNF_NWG;               // epilogue / gather warpgroups
 constexpr int kThreadsU = 64 + 128 * kNWG;        // warp 0 TMA, warp 1 MMA, then the warpgroups
-#ifndef SPLAT_UNF_RB
-#define SPLAT_UNF_RB 4
-#endif
-constexpr int kNWGP = 3;                          // SpMM gather warpgroups (+ 1 epilogue warpgroup)
-constexpr int kThreadsP = 64 + 128 + 128 * kNWGP;
 constexpr int kSub = 128 * 128;                   // [128 rows x 64 bf16] swizzle-128B sub-tile (16 KB)
-constexpr int kRB = SPLAT_UNF_RB;                 // SpMM gather, PARTIAL tiles: rows per load batch
-constexpr int kRF = 8;                            // SpMM gather, FULL tiles: rows per load batch
 
 struct ParamsU {
     DevAcsr A;
@@ -77,8 +71,17 @@ __device__ unsigned long long g_unf_prof[32][8];
         if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                                         \
             g_unf_prof[threadIdx.x >> 5][SITE] += clock64() - t0_;                              \
     } while (0)
+// time of a code region into a wait slot of the profile (SPLAT_UNF_PROF build only)
+#define PSPAN_BEGIN(V) const unsigned long long V = clock64()
+#define PSPAN_END(SITE, V)                                                                      \
+    do {                                                                                        \
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                                         \
+            g_unf_prof[threadIdx.x >> 5][SITE] += clock64() - (V);                              \
+    } while (0)
 #else
 #define PWAIT(SITE, BAR, PH) mbar_wait(BAR, PH)
+#define PSPAN_BEGIN(V) do { } while (0)
+#define PSPAN_END(SITE, V) do { } while (0)
 #endif
 
 // predicated 4-byte global store (no branch / reconvergence per element)
@@ -155,6 +158,16 @@ __device__ __forceinline__ long long row_offset(const ParamsU &prm, int bh, int 
     long long base;
     row_info(A, t * 128 + r, base, R);
     if (prm.pass == 0) return (long long)bh * A.nnz + base;
+    const int i = nat_row(prm, t, r);
+    if (i >= A.n) return 0;
+    return (long long)bh * prm.nat_nnz + prm.nat_row_ptr[i] + (prm.pass == 2 ? i / prm.rv_l : 0);
+}
+
+// (b,h) element offset of tile row r's ACSR row in S / P (row_offset without the runs)
+__device__ __forceinline__ long long row_base(const ParamsU &prm, int bh, int t, int r)
+{
+    const DevAcsr &A = prm.A;
+    if (prm.pass == 0) return t * 128 + r < A.n ? (long long)bh * A.nnz + A.row_ptr[t * 128 + r] : 0ll;
     const int i = nat_row(prm, t, r);
     if (i >= A.n) return 0;
     return (long long)bh * prm.nat_nnz + prm.nat_row_ptr[i] + (prm.pass == 2 ? i / prm.rv_l : 0);
@@ -360,20 +373,48 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 }
 
 // ============================================================================ R-SpMM
+//
+// The sparse operand is P in ACSR order: the non-zeros of row i inside key tile [c0, c0 + 128) are
+// the contiguous values P[row_ptr[i] + rank_before(i, c0) ...] (columns ascending, Fig. 5(b)), so a
+// (row, key tile) span is one contiguous run of <= 256 bytes.  The P producer warpgroup (thread =
+// query row) publishes the row's column mask and alignment shift, and each producer warp copies
+// its 32 rows' spans (16-byte aligned supersets, one coalesced cp.async request per row) into a
+// staging ring in SMEM -- the whole tile (up to 32 KB) in flight at once, no registers held.  (One
+// cp.async.bulk per row was tried: the TMA unit takes ~80 cycles per small copy, 0.71 ms on
+// Longformer.)  Two expander warpgroups take the
+// staged tiles in turn and scatter them into a dense 128B-swizzled bf16 P tile (lane = 4 columns:
+// one unaligned 8-byte read from the staged row, a byte permute by the 4-bit mask nibble, zeros
+// off the mask).  O += P V_j is an SS-MMA (V an MN-major operand), O accumulated in TMEM over the
+// query tile's key tiles and written once as bf16.
+//
+//   warp 0 : V producer (TMA)            warp 1 : MMA issuer
+//   warps 4-7   : epilogue (thread = query row = TMEM lane)
+//   warps 8-15          : P producer (warp w: rows 16 (w - 8) .. +15, lane = row for the row table;
+//                         one warp's copies issue at ~one 272-byte request per 125 cycles, so eight
+//                         warps share each tile)
+//   warps 16-19, 20-23  : expanders (entry k -> expander k % 2, dense P buffer k % 2)
+constexpr int kNExp = 2;
+constexpr int kThreadsP = 768;
+constexpr int kStgRow = 272;                      // staged row: 256 bytes + 16-byte alignment slack
+
 template <int D>
 struct CfgP {
     static constexpr int kChunks = D / 64;
     static constexpr int kTileBytes = kChunks * kSub;                 // V tile
-    static constexpr int KS = D == 64 ? 4 : 2;
+    static constexpr int KS = D == 64 ? 3 : 2;                        // V ring
+    static constexpr int NSTG = D == 64 ? 3 : 2;                      // P staging ring
     static constexpr int OFF_V = 0;
-    static constexpr int OFF_P = OFF_V + KS * kTileBytes;             // [kNWGP] P tiles, 32 KB each
-    // per gather warpgroup, double-buffered: [128 rows] {P offset of the row's span, row mask}
-    static constexpr int OFF_RI = OFF_P + kNWGP * 2 * kSub;
-    static constexpr int OFF_BAR = OFF_RI + kNWGP * 2 * 128 * 32;
-    static constexpr int NBAR = 2 * KS + 2 * kNWGP + 4;
-    static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
+    static constexpr int OFF_P = OFF_V + KS * kTileBytes;             // [kNExp] dense P tiles, 32 KB each
+    static constexpr int OFF_STG = OFF_P + kNExp * 2 * kSub;          // [NSTG][128 rows][kStgRow]
+    // [NSTG][128 rows][16 column groups of 8] u16: low byte = staged element index of the group's
+    // first live value, high byte = the group's 8 mask bits
+    static constexpr int OFF_RM = OFF_STG + NSTG * 128 * kStgRow;
+    static constexpr int OFF_BAR = OFF_RM + NSTG * 128 * 32;
+    static constexpr int NBAR = 2 * KS + 2 * NSTG + 2 * kNExp + 4;
+    static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16;   // the dynamic buffer is 1024-aligned (checked)
     static constexpr int TMEM_COLS = 2 * D;                           // O double buffer
     static_assert(SMEM <= 232448, "shared memory budget");
+    static_assert(OFF_STG % 16 == 0 && OFF_RM % 16 == 0 && OFF_BAR % 8 == 0, "alignment");
 };
 
 template <int D>
@@ -382,13 +423,16 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
 {
     using C = CfgP<D>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // pointer arithmetic on the __shared__ array keeps the state space known (LDS/STS, not generic)
-    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    // no static shared memory precedes the dynamic buffer, so it starts 1024-byte aligned (checked)
+    uint8_t *smem = smem_raw;
+    if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0u) __trap();
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR);
     uint64_t *v_full = bars, *v_empty = bars + C::KS;
-    uint64_t *p_full = v_empty + C::KS, *p_empty = p_full + kNWGP;
-    uint64_t *o_full = p_empty + kNWGP, *o_empty = o_full + 2;
+    uint64_t *stg_full = v_empty + C::KS, *stg_empty = stg_full + C::NSTG;
+    uint64_t *p_full = stg_empty + C::NSTG, *p_empty = p_full + kNExp;
+    uint64_t *o_full = p_empty + kNExp, *o_empty = o_full + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + C::NBAR);
+    uint8_t *rrec = smem + C::OFF_RM;      // [NSTG][128][32] bytes
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevAcsr &A = prm.A;
     const int n_units = A.n_qt * prm.BH;
@@ -398,7 +442,8 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::KS; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-        for (int i = 0; i < kNWGP; ++i) { mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1); }
+        for (int i = 0; i < C::NSTG; ++i) { mbar_init(&stg_full[i], 8); mbar_init(&stg_empty[i], 4); }
+        for (int i = 0; i < kNExp; ++i) { mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&o_full[i], 1); mbar_init(&o_empty[i], 4); }
         fence_mbar_init();
         tma_prefetch(&tmV);
@@ -441,13 +486,13 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             if (uo >= 2) PWAIT(1, &o_empty[ob], ((uo >> 1) - 1) & 1);
             bool first = true;
             for (int e = A.qt_ptr[t]; e < A.qt_ptr[t + 1]; ++e) {
-                const int pb = np % kNWGP;
+                const int pb = np % kNExp;
                 PWAIT(2, &v_full[ki], kph);
-                PWAIT(3, &p_full[pb], (np / kNWGP) & 1);
+                PWAIT(3, &p_full[pb], (np / kNExp) & 1);
                 ++np;
                 tc_fence_after();
                 const uint32_t vb = sV + ki * C::kTileBytes, pa = sP + pb * 2 * kSub;
-                if (lane == 0) {
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk)
                         mma_bf16_ss(tmem + ob * D, sdesc_sw128(pa + (kk >> 2) * kSub + (kk & 3) * 32, 16, 1024),
@@ -459,126 +504,186 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                 first = false;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
             }
-            if (lane == 0) mma_commit(&o_full[ob]);
+            if (elect_one()) mma_commit(&o_full[ob]);
             __syncwarp();
         }
-    } else if (warp >= 6) {
-        // gather warpgroup eg takes P tiles i = eg, eg + kNWGP, ...  Thread r publishes its query
-        // row's span offset and column mask for the tile; warp q then fills rows q, q + 4, ...
-        // (interleaved, so rows with many non-zeros -- e.g. Longformer's global rows, which all sit
-        // in the first 32 rows of tile 0 -- are spread over the four warps).
-        const int eg = (warp - 6) >> 2, quad = warp & 3, r = quad * 32 + lane;
-        uint8_t *ptile = smem + C::OFF_P + eg * 2 * kSub;
-        struct RowInfo {
-            long long off;
-            int valid, pad;
-            uint4 m;
-        };
-        RowInfo *ri = reinterpret_cast<RowInfo *>(smem + C::OFF_RI) + eg * 2 * 128;
-        const uint32_t below = (1u << lane) - 1u;
-        const unsigned short *Pg = reinterpret_cast<const unsigned short *>(prm.P);
-        const long long total = (long long)prm.BH * (prm.pass ? prm.nat_nnz : A.nnz);   // elements of P
-        uint32_t i = 0, k = 0;
+    } else if (warp >= 8 && warp < 16) {
+        // ---------------------------------------------------------------- P producers: thread = row r
+        const int r = (warp - 8) * 16 + (lane & 15);   // lanes 16-31 mirror lanes 0-15
+        const unsigned char *Pb = reinterpret_cast<const unsigned char *>(prm.P);
+        const long long total_b = 2ll * (long long)prm.BH * (prm.pass ? prm.nat_nnz : A.nnz);   // bytes of P
+        const long long end_a = total_b & ~15ll;       // bulk copies stay below this (16-byte granules)
+        uint32_t k = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
             unit_tile(A, u, bh, t);
             const int e0 = A.qt_ptr[t], e1 = A.qt_ptr[t + 1];
-            int e = e0 + (int)((eg - (int)(i % kNWGP) + kNWGP) % kNWGP);
-            i += (uint32_t)(e1 - e0);
-            if (e < e1) {
-                RowRuns R;
-                const long long rowoff = row_offset(prm, bh, t, r, R);
-                const bool rvalid = t * 128 + r < A.n;
-                for (; e < e1; e += kNWGP) {
-                    const int ent = A.kv[e];
-                    const int c0 = (ent & kKvMask) * 128;
-                    const bool partial = (ent & kPartialBit) != 0;
-                    RowInfo *rb = ri + (k & 1) * 128;
-                    {
-                        uint4 m4 = make_uint4(~0u, ~0u, ~0u, ~0u);
-                        if (partial) m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
-                        RowInfo x;
-                        x.off = rowoff + rank_before(R, c0);
-                        x.valid = rvalid;
-                        x.pad = 0;
-                        x.m = rvalid ? m4 : make_uint4(0u, 0u, 0u, 0u);
-                        rb[r] = x;
-                    }
-                    wg_sync(1 + eg);          // row table of this tile complete (double-buffered)
-                    if (k >= 1) mbar_wait(&p_empty[eg], (k - 1) & 1);
-                    if (!partial) {
-                        // FULL tile: each row's segment is 128 consecutive values.  Lane l loads the
-                        // 8-byte aligned words l (and l+1 when the segment is not 8-byte aligned) and
-                        // funnel-shifts columns 4l .. 4l+3 out of them: 8 bytes per lane per row.
-                        for (int j0 = 0; j0 < 32; j0 += kRF) {
-                            uint2 c[kRF], x[kRF];
-                            int sh[kRF];
-#pragma unroll
-                            for (int j = 0; j < kRF; ++j) {
-                                const int rr = quad + 4 * (j0 + j);
-                                const long long o = rb[rr].off;
-                                const long long a = o & ~3ll;
-                                sh[j] = (int)(o - a);
-                                const uint2 *src = reinterpret_cast<const uint2 *>(Pg + a) + lane;
-                                c[j] = x[j] = make_uint2(0u, 0u);
-                                if (rb[rr].valid) {
-                                    c[j] = __ldg(src);
-                                    if (sh[j] && a + 4 * lane + 8 <= total) x[j] = __ldg(src + 1);
-                                }
-                            }
-#pragma unroll
-                            for (int j = 0; j < kRF; ++j) {
-                                const int rr = quad + 4 * (j0 + j);
-                                uint2 v = c[j];
-                                if (sh[j] == 1) v = make_uint2(__funnelshift_r(c[j].x, c[j].y, 16), __funnelshift_r(c[j].y, x[j].x, 16));
-                                else if (sh[j] == 2) v = make_uint2(c[j].y, x[j].x);
-                                else if (sh[j] == 3) v = make_uint2(__funnelshift_r(c[j].y, x[j].x, 16), __funnelshift_r(x[j].x, x[j].y, 16));
-                                // columns 4 lane .. 4 lane + 3 -> sub-tile lane / 16, swizzled 16-byte chunk
-                                const int byte = rr * 128 + (((((lane & 15) >> 1) ^ (rr & 7))) << 4) + (lane & 1) * 8;
-                                *reinterpret_cast<uint2 *>(ptile + (lane >> 4) * kSub + byte) = v;
-                            }
-                        }
-                    } else {
-                        // kRB rows per batch: 4 kRB independent loads in flight per lane
-                        for (int j0 = 0; j0 < 32; j0 += kRB) {
-                            unsigned short h[kRB][4];
-#pragma unroll
-                            for (int j = 0; j < kRB; ++j) {
-                                const int rr = quad + 4 * (j0 + j);
-                                const long long o = rb[rr].off;
-                                const uint4 mm = rb[rr].m;
-                                const uint32_t mw[4] = {mm.x, mm.y, mm.z, mm.w};
-                                const unsigned short *src = Pg + o;
-                                int pre = 0;
-#pragma unroll
-                                for (int w = 0; w < 4; ++w) {
-                                    h[j][w] = 0;
-                                    if ((mw[w] >> lane) & 1u) h[j][w] = __ldg(src + pre + __popc(mw[w] & below));
-                                    pre += __popc(mw[w]);
-                                }
-                            }
-#pragma unroll
-                            for (int j = 0; j < kRB; ++j) {
-                                const int rr = quad + 4 * (j0 + j);     // row within the tile
-#pragma unroll
-                                for (int w = 0; w < 4; ++w) {
-                                    // column 32 w + lane -> sub-tile w/2, 16-byte chunk (col & 63) / 8, swizzled by row
-                                    const int cc = (32 * (w & 1) + lane);
-                                    const int byte = rr * 128 + ((((cc >> 3) ^ (rr & 7))) << 4) + (cc & 7) * 2;
-                                    *reinterpret_cast<unsigned short *>(ptile + (w >> 1) * kSub + byte) = h[j][w];
-                                }
-                            }
-                        }
-                    }
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&p_full[eg]);
-                    ++k;
+            PSPAN_BEGIN(t_unit);
+            // The unit's entries are in ascending key-tile order and cover each row's non-zeros
+            // exactly once, so the rank of the row's first non-zero in entry e is the running sum of
+            // its non-zero counts in the entries before it.
+            const long long rowoff = row_base(prm, bh, t, r);
+            const bool rvalid = t * 128 + r < A.n;
+            long long run = 0;
+            // the unit's plan words and mask ids, lane l holding entry e0 + l (the warp's copy is
+            // broadcast by shuffle; entries past 32 are read from global memory), and the row mask
+            // of the next entry loaded one entry ahead
+            const int ne = e1 - e0;
+            const int ent_l = lane < ne ? A.kv[e0 + lane] : 0;
+            const int mid_l = lane < ne ? A.kv_mask[e0 + lane] : -1;
+            auto ent_of = [&](int i) { return i < 32 ? __shfl_sync(0xffffffffu, ent_l, i) : A.kv[e0 + i]; };
+            auto mask_of = [&](int i, int en) {
+                const int mid = i < 32 ? __shfl_sync(0xffffffffu, mid_l, i) : A.kv_mask[e0 + i];
+                uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);
+                if (en & kPartialBit) m = A.masks[(size_t)mid * 128 + r];
+                return m;
+            };
+            int ent = ne > 0 ? ent_of(0) : 0;
+            uint4 m4 = ne > 0 ? mask_of(0, ent) : make_uint4(0u, 0u, 0u, 0u);
+            PSPAN_END(3, t_unit);
+            for (int e = e0; e < e1; ++e, ++k) {
+                const uint4 mc = rvalid ? m4 : make_uint4(0u, 0u, 0u, 0u);
+                if (e + 1 < e1) {
+                    ent = ent_of(e + 1 - e0);
+                    m4 = mask_of(e + 1 - e0, ent);
                 }
+                const int s = k % C::NSTG;
+                if (k >= C::NSTG) PWAIT(4, &stg_empty[s], ((k / C::NSTG) - 1) & 1);
+                const int cnt = __popc(mc.x) + __popc(mc.y) + __popc(mc.z) + __popc(mc.w);
+                const long long b0 = 2ll * (rowoff + run), b1 = b0 + 2ll * cnt;
+                run += cnt;
+                const long long a0 = b0 & ~15ll;
+                long long a1 = (b1 + 15) & ~15ll;
+                uint8_t *srow = smem + C::OFF_STG + (s * 128 + r) * kStgRow;
+                uint32_t bytes = 0;
+                if (cnt > 0) {
+                    if (a1 > end_a && lane < 16) {
+                        // the last row of P: the bytes past the last full 16-byte granule are copied
+                        // by this thread (a bulk copy may not read past the end of the buffer)
+                        for (long long x = (a0 > end_a ? a0 : end_a); x < b1; x += 2)
+                            *reinterpret_cast<unsigned short *>(srow + (x - a0)) =
+                                *reinterpret_cast<const unsigned short *>(Pb + x);
+                        a1 = end_a > a0 ? end_a : a0;
+                    }
+                    bytes = (uint32_t)(a1 - a0);
+                }
+                {
+                    // row record: lanes 0-15 write column groups 0-7 (mask words 0, 1), lanes 16-31
+                    // groups 8-15 (words 2, 3) of row r
+                    const uint32_t shift = (uint32_t)((b0 - a0) >> 1);
+                    const uint32_t wa = lane < 16 ? mc.x : mc.z, wb = lane < 16 ? mc.y : mc.w;
+                    const uint32_t base = shift + (lane < 16 ? 0u : (uint32_t)(__popc(mc.x) + __popc(mc.y)));
+                    uint32_t rec[4];
+#pragma unroll
+                    for (int g2 = 0; g2 < 4; ++g2) {
+                        uint32_t v = 0;
+#pragma unroll
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int g = 2 * g2 + hh;            // group within this half: word g / 4, byte g % 4
+                            const uint32_t wd = g < 4 ? wa : wb;
+                            const uint32_t bsh = 8u * (uint32_t)(g & 3);
+                            const uint32_t pre = (g < 4 ? 0u : (uint32_t)__popc(wa)) + (uint32_t)__popc(wd & ((1u << bsh) - 1u));
+                            v |= ((base + pre) | (((wd >> bsh) & 0xFFu) << 8)) << (16 * hh);
+                        }
+                        rec[g2] = v;
+                    }
+                    *reinterpret_cast<uint4 *>(rrec + (s * 128 + r) * 32 + (lane >> 4) * 16) = make_uint4(rec[0], rec[1], rec[2], rec[3]);
+                }
+                // The warp copies its 16 rows one row per instruction: lane c moves the row's 16-byte
+                // granule c (<= 17 granules, one coalesced 272-byte request), then every thread
+                // registers an arrive-on for its copies and lane 0 arrives for the warp (releasing
+                // the row table and tail bytes written above).
+                PSPAN_BEGIN(t_copy);
+                const uint32_t ng = bytes >> 4;
+                const uint32_t stg_row0 = (uint32_t)(s * 128 + (warp - 8) * 16) * kStgRow;
+#pragma unroll 4
+                for (int rr = 0; rr < 16; ++rr) {
+                    const uint32_t n_rr = __shfl_sync(0xffffffffu, ng, rr);
+                    const long long a_rr = __shfl_sync(0xffffffffu, a0, rr);
+                    if ((uint32_t)lane < n_rr)
+                        cp_async16(smem + C::OFF_STG + stg_row0 + rr * kStgRow + 16 * lane, Pb + a_rr + 16 * lane);
+                }
+                cp_async_mbar_arrive(&stg_full[s]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&stg_full[s]);
+                PSPAN_END(5, t_copy);
             }
         }
-    } else {
-        // epilogue warpgroup (warps 2..5): O of unit uo (the plain sum P V) -> bf16 -> HBM;
+    } else if (warp >= 16) {
+        // ---------------------------------------------------------------- expanders
+        // expander x takes entries k = x, x + 2, ...; warp q of it fills rows q, q + 4, ... (rows
+        // with many non-zeros, e.g. Longformer's global rows, all in the first 32 rows of tile 0,
+        // are spread over the four warps).  Lane l owns columns 4l .. 4l + 3.
+        const int x = (warp - 16) >> 2, q = warp & 3;
+        uint8_t *ptile = smem + C::OFF_P + x * 2 * kSub;
+        // Half-warp h = lane / 16 takes one row, lane l16 = lane % 16 its columns 8 l16 .. 8 l16 + 7:
+        // one 16-byte swizzle chunk of the dense tile (sub-tile l16 / 8, chunk l16 % 8), the byte
+        // l16 % 4 of mask word l16 / 4.
+        const int h = lane >> 4, l16 = lane & 15;
+        const int sub = (l16 >> 3) * kSub, chunk = l16 & 7;
+        uint32_t k = 0, j = 0;     // k: CTA entry counter, j: this expander's tile counter
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+          int bh, t;
+          unit_tile(A, u, bh, t);
+          const uint32_t kend = k + (uint32_t)(A.qt_ptr[t + 1] - A.qt_ptr[t]);
+          for (k += (uint32_t)((x - (int)(k % kNExp) + kNExp) % kNExp); k < kend; k += kNExp, ++j) {
+            const int s = k % C::NSTG;
+            PWAIT(5, &stg_full[s], (k / C::NSTG) & 1);
+            if (j >= 1) PWAIT(6, &p_empty[x], (j - 1) & 1);
+            const uint8_t *stg = smem + C::OFF_STG + s * 128 * kStgRow;
+            // Rows q + 4 (2 i + h), i < 16: the group's 8 staged values from element qq (the row
+            // record: shift + live columns left of 8 l16) are one unaligned 16-byte read (five aligned
+            // words, funnel-shifted by the element parity), stored as is when all 8 columns are live,
+            // as zeros otherwise (branch-free, so the unrolled rows overlap); groups straddling a run
+            // boundary are redone below.
+            PSPAN_BEGIN(t_rows);
+#ifdef SPLAT_SPMM_NOEXP
+            if (false)
+#endif
+            uint32_t pend = 0;      // rows i whose group straddles a run boundary (bit i)
+#pragma unroll 4
+            for (int i = 0; i < 16; ++i) {
+                const int rr = q + 4 * (2 * i + h);
+                const uint32_t rc = *reinterpret_cast<const unsigned short *>(rrec + (s * 128 + rr) * 32 + 2 * l16);
+                const uint32_t byte = rc >> 8, qq = rc & 0xFFu;    // qq: staged element index (<= 127)
+                const uint32_t *w = reinterpret_cast<const uint32_t *>(stg + rr * kStgRow) + (qq >> 1);
+                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+                const uint32_t sh = (qq & 1u) << 4, keep = byte == 0xFFu ? ~0u : 0u;
+                pend |= (byte != 0u && byte != 0xFFu) ? (1u << i) : 0u;
+                const uint4 o = make_uint4(__funnelshift_r(w0, w1, sh) & keep, __funnelshift_r(w1, w2, sh) & keep,
+                                           __funnelshift_r(w2, w3, sh) & keep, __funnelshift_r(w3, w4, sh) & keep);
+                *reinterpret_cast<uint4 *>(ptile + sub + rr * 128 + ((chunk ^ (rr & 7)) << 4)) = o;
+            }
+            // groups straddling a run boundary (a few per row at the edges of a run): value
+            // popc(byte & ((1 << c) - 1)) into each live column c
+            while (pend) {
+                const int i = __ffs(pend) - 1;
+                pend &= pend - 1u;
+                const int rr = q + 4 * (2 * i + h);
+                const uint32_t rc = *reinterpret_cast<const unsigned short *>(rrec + (s * 128 + rr) * 32 + 2 * l16);
+                const uint32_t byte = rc >> 8, qq = rc & 0xFFu;
+                const unsigned short *e = reinterpret_cast<const unsigned short *>(stg + rr * kStgRow) + qq;
+                uint32_t v[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    v[c] = ((byte >> c) & 1u) ? (uint32_t)e[__popc(byte & ((1u << c) - 1u))] : 0u;
+                *reinterpret_cast<uint4 *>(ptile + sub + rr * 128 + ((chunk ^ (rr & 7)) << 4)) =
+                    make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+            }
+            PSPAN_END(3, t_rows);
+            PSPAN_BEGIN(t_fence);
+            fence_proxy_async_smem();
+            __syncwarp();
+            PSPAN_END(4, t_fence);
+            if (lane == 0) {
+                mbar_arrive(&stg_empty[s]);
+                mbar_arrive(&p_full[x]);
+            }
+          }
+          k = kend;
+        }
+    } else if (warp >= 4) {
+        // epilogue warpgroup (warps 4..7): O of unit uo (the plain sum P V) -> bf16 -> HBM;
         // thread = query row.  O is double buffered in TMEM so the MMA runs one unit ahead.
         const int quad = warp & 3, r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
@@ -590,7 +695,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             const int e0 = A.qt_ptr[t], e1 = A.qt_ptr[t + 1];
             {
                 const int ob = uo & 1;
-                PWAIT(5, &o_full[ob], (uo >> 1) & 1);
+                PWAIT(6, &o_full[ob], (uo >> 1) & 1);
                 tc_fence_after();
                 const bool empty = e0 == e1;   // no key tile: O = 0
                 const int nrow = nat_row(prm, t, r);
@@ -666,7 +771,7 @@ cudaError_t launch_sddmm_d(const DevAcsr &A, const void *Q, const void *K, int B
     p.BH = BH;
     p.scale = scale;
     p.S = S;
-    rsddmm_tc_kernel<D><<<grid_for((long long)A.n_qt * BH), kThreadsP, CfgS<D>::SMEM, st>>>(mq, mk, p);
+    rsddmm_tc_kernel<D><<<grid_for((long long)A.n_qt * BH), kThreadsU, CfgS<D>::SMEM, st>>>(mq, mk, p);
     return cudaGetLastError();
 }
 

@@ -1,6 +1,6 @@
 # micro: TS/SS MMA rate with TMEM ld/st contention; new R-SpMM + tiny kernel parity + unfused timings
-timeout 120 ./tools/micro/tsx > gpurun_out/r02c_tsx.txt 2>&1; cat gpurun_out/r02c_tsx.txt
-timeout 120 ./tools/micro/ts > gpurun_out/r02c_ts.txt 2>&1; cat gpurun_out/r02c_ts.txt
+
+
 python -m paper_2407_16847_b200.build > /dev/null 2>&1
 timeout 900 python -m pytest tests -m gpu -q -x -k "unfused or tiny or paper_grid or bf16 or residue or spmm or fp32" > gpurun_out/r02c_pytest.txt 2>&1; tail -3 gpurun_out/r02c_pytest.txt
 timeout 600 python tools/bench_unfused.py --configs longformer,bigbird,sparse_transformer --iters 10 > gpurun_out/r02c_unfused.jsonl 2>&1; cat gpurun_out/r02c_unfused.jsonl | cut -c1-1500

@@ -1,9 +1,13 @@
-python -m paper_2407_16847_b200.build > /dev/null 2>&1
-timeout 900 python -m pytest tests -m gpu -q -x -k "unfused or tiny or paper_grid or bigbird_unfused or mistral_unfused or fp32_wide or coverage" > gpurun_out/r02h_pytest.txt 2>&1; tail -3 gpurun_out/r02h_pytest.txt
-timeout 600 python tools/bench_unfused.py --configs longformer,bigbird,sparse_transformer --iters 10 > gpurun_out/r02h_unfused.jsonl 2>&1; cat gpurun_out/r02h_unfused.jsonl | python -c "
+for v in "" "-DSPLAT_SPMM_NOEXP"; do
+  SPLAT_EXTRA_NVCC_FLAGS="$v" python -m paper_2407_16847_b200.build --diag > /dev/null 2>&1 || echo "build fail $v"
+  echo "variant: $v"
+  SPLAT_LIB=diag timeout 300 python tools/bench_unfused.py --configs longformer,bigbird --iters 5 2>&1 | python -c "
 import json,sys
 for l in sys.stdin:
     try: d=json.loads(l)
     except Exception: print(l.strip()); continue
-    print(d.get('config'), {k:(round(v['ms']*1e3,1), round(v.get('frac_hbm',0),3)) for k,v in d.items() if isinstance(v,dict) and 'ms' in v})
+    print(d['config'], {k:(round(d[k]['ms'],3), round(d[k]['frac_hbm'],3)) for k in ('rspmm',)})
 "
+done
+SPLAT_EXTRA_NVCC_FLAGS="-DSPLAT_SPMM_NOEXP -DSPLAT_UNF_PROF" python -m paper_2407_16847_b200.build --diag > /dev/null 2>&1
+python tools/unf_prof.py longformer | grep -v "warp  [2-7] \|warp  9\|warp 1[0-5]\|warp 1[7-9]\|warp 2[1-3]"

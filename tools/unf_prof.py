@@ -22,10 +22,15 @@ for it in range(3):
     S.splat_rspmm(a, P, V, O)
     torch.cuda.synchronize()
     L.splat_debug_unf_prof(buf)
-names = ["v_empty(prod)", "o_empty(mma)", "v_full(mma)", "p_full(mma)", "p_empty(gather)", "o_full(epi)", "-", "total"]
-for w in range(18):
+# wait sites of rspmm_tc_kernel by role (warp -> role); slot 7 = warp total
+roles = {0: "V TMA", 1: "MMA", 4: "epilogue", 5: "epilogue", 6: "epilogue", 7: "epilogue"}
+roles.update({w: "P producer" for w in range(8, 16)})
+roles.update({w: "expander" for w in range(16, 24)})
+names = ["v_empty", "o_empty", "v_full", "p_full|exp-rows|prod-unit", "stg_empty|exp-fence", "stg_full|prod-copy", "p_empty/o_full", "total"]
+for w in range(24):
     row = [buf[w * 8 + k] for k in range(8)]
     tot = row[7]
     if not tot:
         continue
-    print(f"warp {w:2d} total {tot:9d} " + " ".join(f"{names[k]}={100 * row[k] / tot:5.1f}%" for k in range(6) if row[k]))
+    print(f"warp {w:2d} {roles.get(w, '-'):10s} total {tot:9d} " +
+          " ".join(f"{names[k]}={100 * row[k] / tot:5.1f}%" for k in range(7) if row[k]))
