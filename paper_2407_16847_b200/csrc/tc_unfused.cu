@@ -589,19 +589,26 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     }
                     *reinterpret_cast<uint4 *>(rrec + (s * 128 + r) * 32 + (lane >> 4) * 16) = make_uint4(rec[0], rec[1], rec[2], rec[3]);
                 }
-                // The warp copies its 16 rows one row per instruction: lane c moves the row's 16-byte
-                // granule c (<= 17 granules, one coalesced 272-byte request), then every thread
+                // The warp copies its 16 rows' spans (16-byte granules, <= 17 per row, coalesced), then every thread
                 // registers an arrive-on for its copies and lane 0 arrives for the warp (releasing
                 // the row table and tail bytes written above).
                 PSPAN_BEGIN(t_copy);
                 const uint32_t ng = bytes >> 4;
                 const uint32_t stg_row0 = (uint32_t)(s * 128 + (warp - 8) * 16) * kStgRow;
+                // two rows per instruction (half-warp hh: row rr + 8 hh, lane l16: granule l16), then
+                // the 17th granule of all 16 rows (a span not 16-byte aligned) in one instruction
+                {
+                    const int hh = lane >> 4, l16 = lane & 15;
 #pragma unroll 4
-                for (int rr = 0; rr < 16; ++rr) {
-                    const uint32_t n_rr = __shfl_sync(0xffffffffu, ng, rr);
-                    const long long a_rr = __shfl_sync(0xffffffffu, a0, rr);
-                    if ((uint32_t)lane < n_rr)
-                        cp_async16(smem + C::OFF_STG + stg_row0 + rr * kStgRow + 16 * lane, Pb + a_rr + 16 * lane);
+                    for (int rr = 0; rr < 8; ++rr) {
+                        const int row = rr + 8 * hh;
+                        const uint32_t n_rr = __shfl_sync(0xffffffffu, ng, row);
+                        const long long a_rr = __shfl_sync(0xffffffffu, a0, row);
+                        if ((uint32_t)l16 < n_rr)
+                            cp_async16(smem + C::OFF_STG + stg_row0 + row * kStgRow + 16 * l16, Pb + a_rr + 16 * l16);
+                    }
+                    if (lane < 16 && ng > 16u)
+                        cp_async16(smem + C::OFF_STG + stg_row0 + lane * kStgRow + 256, Pb + a0 + 256);
                 }
                 cp_async_mbar_arrive(&stg_full[s]);
                 __syncwarp();
@@ -641,18 +648,31 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             if (false)
 #endif
             uint32_t pend = 0;      // rows i whose group straddles a run boundary (bit i)
-#pragma unroll 4
-            for (int i = 0; i < 16; ++i) {
-                const int rr = q + 4 * (2 * i + h);
-                const uint32_t rc = *reinterpret_cast<const unsigned short *>(rrec + (s * 128 + rr) * 32 + 2 * l16);
-                const uint32_t byte = rc >> 8, qq = rc & 0xFFu;    // qq: staged element index (<= 127)
-                const uint32_t *w = reinterpret_cast<const uint32_t *>(stg + rr * kStgRow) + (qq >> 1);
-                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
-                const uint32_t sh = (qq & 1u) << 4, keep = byte == 0xFFu ? ~0u : 0u;
-                pend |= (byte != 0u && byte != 0xFFu) ? (1u << i) : 0u;
-                const uint4 o = make_uint4(__funnelshift_r(w0, w1, sh) & keep, __funnelshift_r(w1, w2, sh) & keep,
-                                           __funnelshift_r(w2, w3, sh) & keep, __funnelshift_r(w3, w4, sh) & keep);
-                *reinterpret_cast<uint4 *>(ptile + sub + rr * 128 + ((chunk ^ (rr & 7)) << 4)) = o;
+            // four rows at a time, every shared-memory load issued before any store (the stores to
+            // the dense tile would otherwise order the next row's loads behind them)
+#pragma unroll 1
+            for (int i0 = 0; i0 < 16; i0 += 4) {
+                uint32_t rc[4], w[4][5];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    rc[u] = *reinterpret_cast<const unsigned short *>(rrec + (s * 128 + q + 4 * (2 * (i0 + u) + h)) * 32 + 2 * l16);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int rr = q + 4 * (2 * (i0 + u) + h);
+                    const uint32_t *wp = reinterpret_cast<const uint32_t *>(stg + rr * kStgRow) + ((rc[u] & 0xFFu) >> 1);
+#pragma unroll
+                    for (int c = 0; c < 5; ++c) w[u][c] = wp[c];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int rr = q + 4 * (2 * (i0 + u) + h);
+                    const uint32_t byte = rc[u] >> 8;
+                    const uint32_t sh = (rc[u] & 1u) << 4, keep = byte == 0xFFu ? ~0u : 0u;
+                    pend |= (byte != 0u && byte != 0xFFu) ? (1u << (i0 + u)) : 0u;
+                    const uint4 o = make_uint4(__funnelshift_r(w[u][0], w[u][1], sh) & keep, __funnelshift_r(w[u][1], w[u][2], sh) & keep,
+                                               __funnelshift_r(w[u][2], w[u][3], sh) & keep, __funnelshift_r(w[u][3], w[u][4], sh) & keep);
+                    *reinterpret_cast<uint4 *>(ptile + sub + rr * 128 + ((chunk ^ (rr & 7)) << 4)) = o;
+                }
             }
             // groups straddling a run boundary (a few per row at the edges of a run): value
             // popc(byte & ((1 << c) - 1)) into each live column c
