@@ -543,6 +543,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             PSPAN_END(3, t_unit);
             for (int e = e0; e < e1; ++e, ++k) {
                 const uint4 mc = rvalid ? m4 : make_uint4(0u, 0u, 0u, 0u);
+                const int ent_cur = ent;
                 if (e + 1 < e1) {
                     ent = ent_of(e + 1 - e0);
                     m4 = mask_of(e + 1 - e0, ent);
@@ -574,6 +575,13 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     const uint32_t wa = lane < 16 ? mc.x : mc.z, wb = lane < 16 ? mc.y : mc.w;
                     const uint32_t base = shift + (lane < 16 ? 0u : (uint32_t)(__popc(mc.x) + __popc(mc.y)));
                     uint32_t rec[4];
+                    if (!(ent_cur & kPartialBit)) {
+                        // FULL entry: every group of a valid row is live, group g starts at shift + 8 g
+                        const uint32_t b8 = rvalid ? 0xFF00u : 0u, g0 = shift + (lane < 16 ? 0u : 64u);
+#pragma unroll
+                        for (int g2 = 0; g2 < 4; ++g2)
+                            rec[g2] = ((g0 + 16u * g2) | b8) | (((g0 + 16u * g2 + 8u) | b8) << 16);
+                    } else
 #pragma unroll
                     for (int g2 = 0; g2 < 4; ++g2) {
                         uint32_t v = 0;
