@@ -352,6 +352,9 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
     if (!a) return set_error(SPLAT_ERR_OOM, "host allocation failed");
     a->pat = *p;
     a->n = p->seq_len;
+    // sub-handles of the residue decomposition / permuted strided path run residue-major views whose
+    // tile arithmetic needs 128-aligned key windows
+    a->plan.kv_align = internal ? 2 : 1;
     const int N = a->n;
     a->seg_h.assign((size_t)N * 16, 0);
     a->nseg_h.assign(N, 0);

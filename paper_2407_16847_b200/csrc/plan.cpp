@@ -1,7 +1,8 @@
 // plan.cpp -- host tile planner.
 //
 // From the ACSR runs of every row it derives, per 128-row query tile, the
-// 128-column key tiles touched by any row of the tile.  This is the B200
+// 128-column key windows (starting on 64-column boundaries) that cover the
+// columns touched by any row of the tile.  This is the B200
 // form of the paper's span specialisation (a row group only iterates
 // over [min start, max end] of its rows) applied at tile granularity, and of
 // the R-SDDMM thread-block arrangement (Sec. 7.2): every plan
@@ -26,47 +27,53 @@ void build_plan(splat_acsr_s &a)
     // diagnostics build only: SPLAT_PLAN_ABLATE=1 drops the FULL flags (every tile masked), =2 also
     // drops the span (every query tile visits every key tile).  Product build: always 0.
     const int ablate = diag_env("SPLAT_PLAN_ABLATE");
+    // Key windows are bn = 128 columns wide and start on a multiple of kKvUnit = 64 columns (kv =
+    // start / 64); kv_align = 2 keeps them 128-aligned (sub-handles whose tiles are residue-major
+    // views).  Per query tile, the 64-column blocks holding a non-zero of any row are covered
+    // greedily from the left -- a window at the first uncovered live block -- which uses the fewest
+    // windows of that width (interval covering); with 128-aligned windows only, BigBird's
+    // three-block band (192 columns at 64-column block offsets) would need three.
+    const int align = P.kv_align, nb = (N + kKvUnit - 1) / kKvUnit, wb = bn / kKvUnit;
     P.n_qt = (N + bm - 1) / bm;
     P.n_kt = (N + bn - 1) / bn;
     P.qt_ptr.assign(P.n_qt + 1, 0);
     P.kv.clear();
-    std::vector<int32_t> stamp(P.n_kt, -1), fullc(P.n_kt, 0);
-    std::vector<int32_t> touched;
-    touched.reserve(P.n_kt);
+    std::vector<int32_t> stamp(nb, -1);
     for (int t = 0; t < P.n_qt; ++t) {
         const int r0 = t * bm, r1 = std::min(N, r0 + bm), nrows = r1 - r0;
-        touched.clear();
-        auto touch = [&](int j) {
-            if (stamp[j] != t) {
-                stamp[j] = t;
-                fullc[j] = 0;
-                touched.push_back(j);
-            }
-        };
+        auto mark = [&](int blk) { stamp[blk] = t; };
         for (int i = r0; i < r1; ++i) {
             const int32_t *sg = &a.seg_h[(size_t)i * 16];
             for (int s = 0; s < a.nseg_h[i]; ++s) {
                 const int start = sg[4 * s], step = sg[4 * s + 1], count = sg[4 * s + 2];
                 const int last = start + step * (count - 1);
-                if (step == 1) {
-                    for (int j = start / bn; j <= last / bn; ++j) {
-                        touch(j);
-                        const int c0 = j * bn, c1 = std::min(N, c0 + bn) - 1;
-                        if (start <= c0 && c1 <= last) ++fullc[j];
-                    }
-                } else if (step < bn) {
-                    for (int j = start / bn; j <= last / bn; ++j) touch(j);
+                if (step < kKvUnit) {
+                    for (int j = start / kKvUnit; j <= last / kKvUnit; ++j) mark(j);
                 } else {
-                    for (int x = 0; x < count; ++x) touch((start + step * x) / bn);
+                    for (int x = 0; x < count; ++x) mark((start + step * x) / kKvUnit);
                 }
             }
         }
         if (ablate >= 2)
-            for (int j = 0; j < P.n_kt; ++j) touch(j);
-        std::sort(touched.begin(), touched.end());
-        for (int j : touched) {
-            const bool full = ablate == 0 && (j + 1) * bn <= N && fullc[j] == nrows;
-            P.kv.push_back(j | (full ? 0 : kPartialBit));
+            for (int j = 0; j < nb; ++j) mark(j);
+        for (int j = 0; j < nb;) {
+            if (stamp[j] != t) { ++j; continue; }
+            const int kv = j - j % align;                       // window [64 kv, 64 kv + bn)
+            const int c0 = kv * kKvUnit, c1 = std::min(N, c0 + bn) - 1;
+            // FULL: every row of the query tile holds every column of the window (one step-1 run)
+            bool full = ablate == 0 && c0 + bn <= N;
+            for (int i = r0; i < r1 && full; ++i) {
+                const int32_t *sg = &a.seg_h[(size_t)i * 16];
+                bool row_full = false;
+                for (int s = 0; s < a.nseg_h[i] && !row_full; ++s) {
+                    const int start = sg[4 * s], step = sg[4 * s + 1], count = sg[4 * s + 2];
+                    row_full = (step == 1 || count == 1) && start <= c0 && c1 <= start + step * (count - 1);
+                }
+                full = row_full;
+            }
+            (void)nrows;
+            P.kv.push_back(kv | (full ? 0 : kPartialBit));
+            j = kv + wb;
         }
         P.qt_ptr[t + 1] = (int32_t)P.kv.size();
     }
@@ -169,7 +176,7 @@ void build_plan(splat_acsr_s &a)
     P.masks.clear();
     for (int p = 0; p < P.n_pairs; ++p) {
         for (int e = P.pair_ptr[p]; e < P.pair_ptr[p + 1]; ++e) {
-            const int ent = P.pair_ent[e], c0 = (ent & kKvMask) * bn;
+            const int ent = P.pair_ent[e], c0 = (ent & kKvMask) * kKvUnit;
             for (int g = 0; g < 2; ++g) {
                 const int t = 2 * p + g;
                 if (!(ent & (g == 0 ? kUseA : kUseB))) continue;

@@ -22,6 +22,7 @@ namespace splat {
 // 128-column key tiles).
 constexpr int kBM = 128;
 constexpr int kBN = 128;
+constexpr int kKvUnit = 64;          // plan entries: key window [64 kv, 64 kv + kBN)
 constexpr int kPartialBit = 1 << 24;
 constexpr int kKvMask = (1 << 24) - 1;
 
@@ -169,6 +170,7 @@ constexpr int kMaxBuckets = 24;
 
 struct Plan {
     int bm = kBM, bn = kBN, n_qt = 0, n_entries = 0, n_kt = 0;
+    int kv_align = 1;                     // window starts: multiples of kv_align * 64 columns
     std::vector<int32_t> qt_ptr, kv, order;          // per query tile (ABI: splat_plan_copy)
     // query-tile pairs
     int n_pairs = 0, n_pair_entries = 0, n_buckets = 0, n_masks = 0;

@@ -333,9 +333,9 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     for (int c = 0; c < C::kChunks; ++c)
                         if (VIEW)
                             tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c,
-                                        (kv << 7) & (prm.rv_nk - 1), (kv << 7) >> prm.rv_sh, bh);
+                                        (kv << 6) & (prm.rv_nk - 1), (kv << 6) >> prm.rv_sh, bh);
                         else
-                            tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * 128, bh);
+                            tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * kKvUnit, bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -877,7 +877,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                     mbar_arrive(&v_full[vi]);
                 } else {
                     mbar_expect_tx(&v_full[vi], C::TB);
-                    tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * 128, pv_bh);
+                    tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * kKvUnit, pv_bh);
                 }
             }
             ++vc;
@@ -930,7 +930,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                         mbar_arrive(&k_full[ki]);
                     } else {
                         mbar_expect_tx(&k_full[ki], C::TB);
-                        tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * 128, un.bh);
+                        tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * kKvUnit, un.bh);
                     }
                 }
                 ++kc;

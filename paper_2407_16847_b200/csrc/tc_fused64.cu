@@ -174,7 +174,7 @@ mhsa64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
             PROF(3);
             if (lane == 0) {
                 mbar_expect_tx(&v_full[vi], C::TB);
-                tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * 128, pv_bh);
+                tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * kKvUnit, pv_bh);
             }
             ++vc;
             if (++vi == C::VS) { vi = 0; vph ^= 1; }
@@ -242,7 +242,7 @@ mhsa64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ C
                 PROF(2);
                 if (lane == 0) {
                     mbar_expect_tx(&k_full[ki], C::TB);
-                    tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * 128, un.bh);
+                    tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * kKvUnit, un.bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }

@@ -100,12 +100,13 @@ __device__ __forceinline__ int nat_row(const ParamsU &prm, int t, int r)
     return prm.pass == 1 ? (p >> prm.rv_sh) + prm.rv_l * (p & (prm.rv_nk - 1)) : p;
 }
 
-// 3-D (natural) or 4-D (residue-major, pass 1) tile load of 128 rows starting at tile `tile`
+// 3-D (natural) or 4-D (residue-major, pass 1) load of the 128 rows starting at row `row0` (a query
+// tile: 128 t; a key window: 64 kv)
 __device__ __forceinline__ void load_tile_rows(const ParamsU &prm, void *dst, const CUtensorMap *m, uint64_t *bar,
-                                               int c0, int tile, int bh)
+                                               int c0, int row0, int bh)
 {
-    if (prm.pass == 1) tma_load_4d(dst, m, bar, c0, (tile << 7) & (prm.rv_nk - 1), (tile << 7) >> prm.rv_sh, bh);
-    else tma_load_3d(dst, m, bar, c0, tile * 128, bh);
+    if (prm.pass == 1) tma_load_4d(dst, m, bar, c0, row0 & (prm.rv_nk - 1), row0 >> prm.rv_sh, bh);
+    else tma_load_3d(dst, m, bar, c0, row0, bh);
 }
 
 __device__ __forceinline__ void unit_tile(const DevAcsr &A, int u, int &bh, int &t)
@@ -236,7 +237,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 mbar_expect_tx(&q_full[qi], C::kTileBytes);
 #pragma unroll
                 for (int c = 0; c < C::kChunks; ++c)
-                    load_tile_rows(prm, smem + C::OFF_Q + qi * C::kTileBytes + c * kSub, &tmQ, &q_full[qi], 64 * c, t, bh);
+                    load_tile_rows(prm, smem + C::OFF_Q + qi * C::kTileBytes + c * kSub, &tmQ, &q_full[qi], 64 * c, t * 128, bh);
             }
             ++qc;
             if (++qi == C::QS) { qi = 0; qph ^= 1; }
@@ -248,7 +249,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
                         load_tile_rows(prm, smem + C::OFF_K + ki * C::kTileBytes + c * kSub, &tmK, &k_full[ki], 64 * c,
-                                       kv, bh);
+                                       kv * kKvUnit, bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -314,7 +315,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             const long long rowoff = row_offset(prm, bh, t, r, R);
             for (; e < e1; e += kNWG) {
                 const int ent = A.kv[e];
-                const int c0 = (ent & kKvMask) * 128;
+                const int c0 = (ent & kKvMask) * kKvUnit;
                 const bool partial = (ent & kPartialBit) != 0;
                 const int tb = k & 1;
                 uint4 m4 = make_uint4(~0u, ~0u, ~0u, ~0u);
@@ -468,7 +469,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
                         load_tile_rows(prm, smem + C::OFF_V + ki * C::kTileBytes + c * kSub, &tmV, &v_full[ki], 64 * c,
-                                       kv, bh);
+                                       kv * kKvUnit, bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }

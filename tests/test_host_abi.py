@@ -108,26 +108,51 @@ def test_closed_form_meta_bit_exact_exhaustive(N):
         compare_meta_with_oracle(p)
 
 
-def plan_reference(m, bm, bn):
-    """Tiles touched / FULL from the oracle's explicit mask (independent of the planner)."""
-    N = m.shape[0]
+def plan_reference(m, bm, bn, unit=64):
+    """Key windows / FULL from the oracle's explicit mask (independent of the planner): per query
+    tile, the 64-column blocks holding a non-zero of any row, covered greedily from the left by
+    bn-wide windows starting at a block boundary (the fewest such windows); FULL = every row holds
+    every column of the window.  Entries are (start / 64, full)."""
+    N, NC = m.shape
     out = []
     for t in range((N + bm - 1) // bm):
         rows = m[t * bm:(t + 1) * bm]
-        ents = []
-        for j in range((N + bn - 1) // bn):
-            blk = rows[:, j * bn:(j + 1) * bn]
-            if blk.any():
-                full = blk.shape[1] == bn and bool(blk.all())
-                ents.append((j, full))
+        live = [bool(rows[:, b * unit:(b + 1) * unit].any()) for b in range((NC + unit - 1) // unit)]
+        ents, b = [], 0
+        while b < len(live):
+            if not live[b]:
+                b += 1
+                continue
+            blk = rows[:, b * unit:b * unit + bn]
+            full = b * unit + bn <= NC and bool(blk.all())
+            ents.append((b, full))
+            b += bn // unit
         out.append(ents)
     return out
+
+
+def test_plan_reference_greedy_is_minimal():
+    """Brute force on small masks: no set of fewer 64-aligned windows covers the live blocks."""
+    import itertools
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        nb = int(rng.integers(1, 9))
+        live = rng.random(nb) < 0.5
+        m = np.zeros((1, nb * 64), dtype=bool)
+        for b in range(nb):
+            m[0, b * 64] = live[b]
+        greedy = len(plan_reference(m, 1, 128)[0])
+        need = [b for b in range(nb) if live[b]]
+        best = 0 if not need else min(k for k in range(1, nb + 1) for c in itertools.combinations(range(nb), k)
+                                      if all(any(s <= b <= s + 1 for s in c) for b in need))
+        assert greedy == best
 
 
 @pytest.mark.parametrize("p", [Pattern("window", 700, lo=64, hi=64), Pattern("global_local", 1000, lo=128, hi=128, n_global=32),
                                Pattern("bigbird", 1024, block=64, radius=1), Pattern("strided_local", 1100, stride=128, causal=1),
                                Pattern("strided", 600, stride=7), Pattern("dilated", 900, stride=3, radius=50),
-                               Pattern("blocked", 640, block=96), Pattern("window", 300, lo=299, hi=0)],
+                               Pattern("blocked", 640, block=96), Pattern("window", 300, lo=299, hi=0),
+                               Pattern("bigbird", 4096, block=64, radius=1)],
                          ids=lambda p: p.kind)
 def test_tile_plan_matches_mask(p):
     a = S.Acsr(p, device=-1)
