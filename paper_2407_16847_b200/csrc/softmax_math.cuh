@@ -68,7 +68,7 @@ __device__ __forceinline__ float max32(const float *v)
 #define SPLAT_NEMU128 4       // d = 128 (MUFU has more slack against the tensor pipe there)
 #endif
 #ifndef SPLAT_NEMU
-#define SPLAT_NEMU 8
+#define SPLAT_NEMU 12
 #endif
 
 __device__ __forceinline__ uint64_t fmax2_clamp(uint64_t z)
