@@ -337,6 +337,38 @@ splat_status splat_tiling_cost_eval(const splat_pattern *p, int32_t m, int32_t n
 splat_status splat_acsr_from_mask(const uint32_t *mask, int32_t n, int32_t max_runs, int device, void *stream,
                                   splat_acsr *out, int32_t *bad_row, int32_t *bad_col);
 
+/* ---------------------------------------------------------------------------
+ * Data-layout reordering (PAPER "Data-layout reordering"
+ * P:722, density analysis Listing 4 line 5 P:716, Fig. 15).  R-SDDMM
+ * and the softmax produce S / P row-compressed & row-major (ACSR order of M);
+ * the paper transposes P to column-compressed & column-major before its SIMT
+ * R-SpMM when the mask density reaches alpha = 0.10, so that a column's
+ * consecutive rows are read from consecutive addresses.
+ *
+ * splat_acsr_transpose: handle `at` of M^T (row j of M^T = the rows i with j
+ *   in cols(i), ascending; greedy runs, reading R-4), built from a's runs
+ *   through the mask-ingest builder on the same device (host handle if a is
+ *   one).  Synchronous; allocates at build time only.  Errors: INVALID_ARG,
+ *   UNSUPPORTED (N > 131072), NOT_REGULAR (a column of M needs more than
+ *   SPLAT_MAX_SEGS runs), OOM, CUDA.  Free `at` with splat_acsr_destroy.
+ * splat_transpose_values: Y[b,h, row_ptr_T[j] + rank of i in row j of M^T]
+ *   = X[b,h, row_ptr[i] + rank of j in row i] for every non-zero (i, j):
+ *   X, Y device [B,H,nnz] of dtype dt (bf16 or fp32), caller-owned; async on
+ *   stream.  `at` must be splat_acsr_transpose(a).
+ * splat_rspmm_cc: R-SpMM from column-compressed P (PT as written by
+ *   splat_transpose_values): O[b,h,i,:] = sum_j PT[b,h, row_ptr_T[j] +
+ *   rank_T(j, i)] V[b,h,j,:], SIMT with fp32 accumulation (the paper's
+ *   precision), 1 <= d <= 256, V and O [B,H,N,d] of dtype dt.
+ * splat_layout_choice: 1 (column-compressed) when nnz / N^2 >= alpha, else 0
+ *   (row-compressed) -- the paper's density classification; 0 for NULL.
+ * ------------------------------------------------------------------------- */
+splat_status splat_acsr_transpose(splat_acsr a, void *stream, splat_acsr *at);
+splat_status splat_transpose_values(splat_acsr a, splat_acsr at, const void *X, void *Y, splat_dtype dt,
+                                    int32_t B, int32_t H, void *stream);
+splat_status splat_rspmm_cc(splat_acsr a, splat_acsr at, const void *PT, const void *V, splat_dtype dt,
+                            int32_t B, int32_t H, int32_t d, void *O, void *stream);
+int32_t splat_layout_choice(splat_acsr a, double alpha);
+
 /* Algorithmic FLOPs of one fused call: 4 * nnz * d * B * H (QK^T and PV at
  * 2*nnz*d each; the softmax is not counted; SURVEY reading A-14). */
 double splat_flops(splat_acsr a, int32_t B, int32_t H, int32_t d);

@@ -862,6 +862,86 @@ splat_status splat_sparse_mhsa_host(splat_acsr a, const void *Qh, const void *Kh
     return SPLAT_OK;
 }
 
+// ---- data-layout reordering (NEXT #3): column-compressed ACSR values for R-SpMM
+splat_status splat_acsr_transpose(splat_acsr a, void *stream, splat_acsr *at)
+{
+    clear_error();
+    if (!a || !at) return set_error(SPLAT_ERR_INVALID_ARG, "null handle or out pointer");
+    *at = nullptr;
+    const int n = a->n;
+    if (n > kMaxMaskN) return set_error(SPLAT_ERR_UNSUPPORTED, "transpose needs N <= %d, got %d", kMaxMaskN, n);
+    const size_t W = ((size_t)n + 31) / 32;
+    std::vector<uint32_t> mt;
+    try {
+        mt.assign((size_t)n * W, 0u);
+    } catch (const std::exception &) {
+        return set_error(SPLAT_ERR_OOM, "host allocation of the transposed mask failed");
+    }
+    // M^T as an explicit bit mask: row c of M^T holds bit i for every non-zero (i, c) of M
+    for (int i = 0; i < n; ++i)
+        for (int s = 0; s < a->nseg_h[i]; ++s) {
+            const int32_t *g = &a->seg_h[(size_t)i * 16 + 4 * s];
+            for (int x = 0; x < g[2]; ++x) {
+                const int c = g[0] + g[1] * x;
+                mt[(size_t)c * W + (size_t)(i >> 5)] |= 1u << (i & 31);
+            }
+        }
+    if (a->device < 0) return splat_acsr_from_mask(mt.data(), n, SPLAT_MAX_SEGS, -1, stream, at, nullptr, nullptr);
+    DeviceGuard g(a->device);
+    uint32_t *d = nullptr;
+    cudaError_t e = dev_alloc(&d, mt.size() * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemcpy(d, mt.data(), mt.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        return cuda_fail(e, "transposed mask upload");
+    }
+    const splat_status st = splat_acsr_from_mask(d, n, SPLAT_MAX_SEGS, a->device, stream, at, nullptr, nullptr);
+    cudaFree(d);      // the build is synchronous
+    return st;
+}
+
+splat_status splat_transpose_values(splat_acsr a, splat_acsr at, const void *X, void *Y, splat_dtype dt, int32_t B,
+                                    int32_t H, void *stream)
+{
+    splat_status st = check_compute(a, B, H);
+    if (st != SPLAT_OK) return st;
+    if (!at || at->device != a->device || at->n != a->n || at->nnz != a->nnz)
+        return set_error(SPLAT_ERR_INVALID_ARG, "at is not the transpose handle of a (splat_acsr_transpose)");
+    if (dt != SPLAT_BF16 && dt != SPLAT_FP32) return set_error(SPLAT_ERR_INVALID_ARG, "unknown dtype %d", (int)dt);
+    if (!X || !Y) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
+    DeviceGuard g(a->device);
+    const cudaError_t e = launch_transpose_values(dev_view(a), dev_view(at), X, Y, dt == SPLAT_BF16, B * H,
+                                                  (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "splat_transpose_values launch");
+    note_launches(1);
+    return SPLAT_OK;
+}
+
+splat_status splat_rspmm_cc(splat_acsr a, splat_acsr at, const void *PT, const void *V, splat_dtype dt, int32_t B,
+                            int32_t H, int32_t d, void *O, void *stream)
+{
+    splat_status st = check_compute(a, B, H);
+    if (st != SPLAT_OK) return st;
+    if (!at || at->device != a->device || at->n != a->n || at->nnz != a->nnz)
+        return set_error(SPLAT_ERR_INVALID_ARG, "at is not the transpose handle of a (splat_acsr_transpose)");
+    if (dt != SPLAT_BF16 && dt != SPLAT_FP32) return set_error(SPLAT_ERR_INVALID_ARG, "unknown dtype %d", (int)dt);
+    if (d < 1 || d > 256) return set_error(SPLAT_ERR_UNSUPPORTED, "splat_rspmm_cc needs 1 <= d <= 256, got %d", d);
+    if (!PT || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
+    DeviceGuard g(a->device);
+    const cudaError_t e = launch_rspmm_cc(dev_view(a), dev_view(at), PT, V, dt == SPLAT_BF16, B * H, d, O,
+                                          (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "splat_rspmm_cc launch");
+    note_launches(1);
+    return SPLAT_OK;
+}
+
+int32_t splat_layout_choice(splat_acsr a, double alpha)
+{
+    if (!a || a->n < 1) return 0;
+    const double density = (double)a->nnz / ((double)a->n * (double)a->n);
+    return density >= alpha ? 1 : 0;
+}
+
 double splat_flops(splat_acsr a, int32_t B, int32_t H, int32_t d)
 {
     if (!a) return 0.0;

@@ -52,6 +52,12 @@ cudaError_t launch_mhsa_tc_permuted(const DevAcsr &perm, int l, int nk, int R, c
 cudaError_t launch_acsr_from_mask(const uint32_t *mask, int n, int max_runs, int4 *seg, uint8_t *nseg,
                                   int64_t *row_ptr, unsigned long long *bad, cudaStream_t st);
 
+// data-layout reordering (layout.cu): Y (M^T's ACSR order) from X (M's); R-SpMM from column-compressed P
+cudaError_t launch_transpose_values(const DevAcsr &A, const DevAcsr &AT, const void *X, void *Y, bool bf16, int BH,
+                                    cudaStream_t st);
+cudaError_t launch_rspmm_cc(const DevAcsr &A, const DevAcsr &AT, const void *PT, const void *V, bool bf16, int BH,
+                            int d, void *O, cudaStream_t st);
+
 // SIMT kernels (fp32 path; any d <= 256)
 cudaError_t launch_rsddmm_simt(const DevAcsr &A, const void *Q, const void *K, bool bf16, int BH, int d,
                                float scale, float *S, cudaStream_t st);

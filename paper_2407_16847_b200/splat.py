@@ -29,7 +29,8 @@ KINDS = {"window": 0, "blocked": 1, "strided": 2, "dilated": 3, "global_local": 
 EXPORTS = ("splat_acsr_build", "splat_acsr_info", "splat_acsr_copy_meta", "splat_plan_info",
            "splat_plan_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
            "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_acsr_from_mask", "splat_poset_tile", "splat_naive_tile",
-           "splat_tiling_cost_eval", "splat_flops", "splat_last_launch_count", "splat_device_alloc_count",
+           "splat_tiling_cost_eval", "splat_acsr_transpose", "splat_transpose_values", "splat_rspmm_cc",
+           "splat_layout_choice", "splat_flops", "splat_last_launch_count", "splat_device_alloc_count",
            "splat_last_error")
 
 
@@ -85,12 +86,17 @@ def lib():
         L.splat_poset_tile.argtypes = [P(splat_pattern), i32, i32, i32, vp, i64, P(splat_tiling_cost)]
         L.splat_naive_tile.argtypes = [P(splat_pattern), i32, i32, vp, i64, P(splat_tiling_cost)]
         L.splat_tiling_cost_eval.argtypes = [P(splat_pattern), i32, i32, i32, vp, i64, P(splat_tiling_cost)]
+        L.splat_acsr_transpose.argtypes = [vp, vp, P(vp)]
+        L.splat_transpose_values.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, vp]
+        L.splat_rspmm_cc.argtypes = [vp, vp, vp, vp, C.c_int, i32, i32, i32, vp, vp]
+        L.splat_layout_choice.argtypes = [vp, C.c_double]
+        L.splat_layout_choice.restype = i32
         L.splat_flops.argtypes = [vp, i32, i32, i32]
         L.splat_flops.restype = C.c_double
         L.splat_last_launch_count.restype = i32
         L.splat_last_error.restype = C.c_char_p
         for name in EXPORTS:
-            if name not in ("splat_flops", "splat_last_error", "splat_last_launch_count"):
+            if name not in ("splat_flops", "splat_last_error", "splat_last_launch_count", "splat_layout_choice"):
                 getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -258,6 +264,39 @@ def splat_rspmm(a: Acsr, P, V, O, stream=None):
     _check(lib().splat_rspmm(a.handle, P.data_ptr(), V.data_ptr(), _dt(V), B, H, d, O.data_ptr(),
                              C.c_void_p(_stream(stream))))
     return O
+
+
+ALPHA = 0.10     # the paper's density threshold for the column-compressed layout
+
+
+def splat_acsr_transpose(a: Acsr, stream=None) -> Acsr:
+    """Handle of M^T (column-compressed ACSR of a's mask), on a's device."""
+    h = C.c_void_p()
+    st = _stream(stream) if a.device >= 0 else 0
+    _check(lib().splat_acsr_transpose(a.handle, C.c_void_p(st), C.byref(h)))
+    return Acsr(None, a.device, _handle=h)
+
+
+def splat_transpose_values(a: Acsr, at: Acsr, X, Y, B: int, H: int, stream=None):
+    if X.dtype != Y.dtype or X.numel() != B * H * a.nnz or Y.numel() != X.numel():
+        raise SplatError(3, "X and Y: same dtype, B*H*nnz elements")
+    _check(lib().splat_transpose_values(a.handle, at.handle, X.data_ptr(), Y.data_ptr(), _dt(X), B, H,
+                                        C.c_void_p(_stream(stream))))
+    return Y
+
+
+def splat_rspmm_cc(a: Acsr, at: Acsr, PT, V, O, stream=None):
+    B, H, d = _check_qkv(a, V, O)
+    if PT.dtype != V.dtype or PT.numel() != B * H * a.nnz:
+        raise SplatError(3, "PT must have V's dtype and B*H*nnz elements")
+    _check(lib().splat_rspmm_cc(a.handle, at.handle, PT.data_ptr(), V.data_ptr(), _dt(V), B, H, d, O.data_ptr(),
+                                C.c_void_p(_stream(stream))))
+    return O
+
+
+def splat_layout_choice(a: Acsr, alpha: float = ALPHA) -> int:
+    """1 = column-compressed (density >= alpha), 0 = row-compressed."""
+    return int(lib().splat_layout_choice(a.handle, alpha))
 
 
 def splat_sparse_mhsa(a: Acsr, Q, K, V, O, scale: float, stream=None):
