@@ -927,9 +927,13 @@ splat_status splat_rspmm_cc(splat_acsr a, splat_acsr at, const void *PT, const v
     if (dt != SPLAT_BF16 && dt != SPLAT_FP32) return set_error(SPLAT_ERR_INVALID_ARG, "unknown dtype %d", (int)dt);
     if (d < 1 || d > 256) return set_error(SPLAT_ERR_UNSUPPORTED, "splat_rspmm_cc needs 1 <= d <= 256, got %d", d);
     if (!PT || !V || !O) return set_error(SPLAT_ERR_INVALID_ARG, "null tensor pointer");
+    // Fig. 14 ablation knob (diagnostics build only; 0 in the product build): SPLAT_CC_ALIGN = X runs
+    // the lanes along the stride lattice of STRIDED(X)
+    const int align_x = diag_env("SPLAT_CC_ALIGN");
+    if (align_x > 1 && a->n % align_x != 0) return set_error(SPLAT_ERR_INVALID_ARG, "SPLAT_CC_ALIGN must divide N");
     DeviceGuard g(a->device);
     const cudaError_t e = launch_rspmm_cc(dev_view(a), dev_view(at), PT, V, dt == SPLAT_BF16, B * H, d, O,
-                                          (cudaStream_t)stream);
+                                          (cudaStream_t)stream, align_x);
     if (e != cudaSuccess) return cuda_fail(e, "splat_rspmm_cc launch");
     note_launches(1);
     return SPLAT_OK;

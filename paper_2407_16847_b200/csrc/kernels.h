@@ -56,7 +56,7 @@ cudaError_t launch_acsr_from_mask(const uint32_t *mask, int n, int max_runs, int
 cudaError_t launch_transpose_values(const DevAcsr &A, const DevAcsr &AT, const void *X, void *Y, bool bf16, int BH,
                                     cudaStream_t st);
 cudaError_t launch_rspmm_cc(const DevAcsr &A, const DevAcsr &AT, const void *PT, const void *V, bool bf16, int BH,
-                            int d, void *O, cudaStream_t st);
+                            int d, void *O, cudaStream_t st, int align_x = 0);
 
 // SIMT kernels (fp32 path; any d <= 256)
 cudaError_t launch_rsddmm_simt(const DevAcsr &A, const void *Q, const void *K, bool bf16, int BH, int d,

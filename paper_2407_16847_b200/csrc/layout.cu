@@ -83,12 +83,21 @@ transpose_values_kernel(DevAcsr A, DevAcsr AT, const T *__restrict__ X, T *__res
 
 template <typename T>
 __global__ void __launch_bounds__(256)
-rspmm_cc_kernel(DevAcsr A, DevAcsr AT, const T *__restrict__ PT, const T *__restrict__ V, int d, T *__restrict__ O)
+rspmm_cc_kernel(DevAcsr A, DevAcsr AT, const T *__restrict__ PT, const T *__restrict__ V, int d, T *__restrict__ O,
+                int align_x)
 {
     const int n_rt = (A.n + 31) / 32;
     const int bh = blockIdx.x / n_rt, i0 = (blockIdx.x % n_rt) * 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int i = i0 + lane;
+    // align_x > 1 (diagnostics build, the Fig. 14 ablation): lanes take rows along the stride
+    // lattice of STRIDED(align_x) -- row r' of the residue-major order is (r' mod nk) X + r' div nk
+    // -- so every lane of a warp is a row of the same column residue (the paper's
+    // linear-transformation alignment); 0: natural consecutive rows
+    int i = i0 + lane;
+    if (align_x > 1 && i < A.n) {
+        const int nk = A.n / align_x;
+        i = (i % nk) * align_x + i / nk;
+    }
     // span of the 32 rows' columns
     int jlo = 0x7fffffff, jhi = -1;
     if (i < A.n) {
@@ -146,16 +155,16 @@ cudaError_t launch_transpose_values(const DevAcsr &A, const DevAcsr &AT, const v
 }
 
 cudaError_t launch_rspmm_cc(const DevAcsr &A, const DevAcsr &AT, const void *PT, const void *V, bool bf16, int BH,
-                            int d, void *O, cudaStream_t st)
+                            int d, void *O, cudaStream_t st, int align_x)
 {
     const int n_rt = (A.n + 31) / 32;
     const dim3 grid((unsigned)(BH * n_rt));
     const int threads = 32 * ((d + 31) / 32);
     if (bf16)
         rspmm_cc_kernel<__nv_bfloat16><<<grid, threads, 0, st>>>(A, AT, (const __nv_bfloat16 *)PT,
-                                                                 (const __nv_bfloat16 *)V, d, (__nv_bfloat16 *)O);
+                                                                 (const __nv_bfloat16 *)V, d, (__nv_bfloat16 *)O, align_x);
     else
-        rspmm_cc_kernel<float><<<grid, threads, 0, st>>>(A, AT, (const float *)PT, (const float *)V, d, (float *)O);
+        rspmm_cc_kernel<float><<<grid, threads, 0, st>>>(A, AT, (const float *)PT, (const float *)V, d, (float *)O, align_x);
     return cudaGetLastError();
 }
 
