@@ -163,6 +163,8 @@ DevAcsr dev_view(const splat_acsr_s *a, int slot = 0)
 {
     DevAcsr A;
     A.seg = reinterpret_cast<const int4 *>(a->d_seg);
+    A.pat = a->pat;
+    A.has_pat = a->pat.kind >= SPLAT_WINDOW && a->pat.kind <= SPLAT_STRIDED_LOCAL;
     A.nseg = a->d_nseg;
     A.row_ptr = a->d_row_ptr;
     A.n = a->n;

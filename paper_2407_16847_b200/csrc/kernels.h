@@ -32,6 +32,10 @@ struct DevAcsr {
     int t_n_buckets;
     int t_bucket_start[kMaxBuckets + 1];
     unsigned long long *sched;  // [2]: dynamic work counter + done counter of the split kernel
+    // the descriptor of a descriptor-built handle (has_pat = 1): kernels may evaluate a row's runs
+    // in closed form (row_segments) instead of loading them; 0 for mask-ingest handles
+    splat_pattern pat;
+    int has_pat;
 };
 
 cudaError_t launch_acsr_build(const splat_pattern &p, int4 *seg, uint8_t *nseg, int64_t *row_ptr,

@@ -368,6 +368,30 @@ mhsa_simt_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K, co
 constexpr int kRowThreads = 128;
 
 template <typename T>
+__device__ __forceinline__ float dot_full(const float *q, const T *__restrict__ k, int d);
+
+// fp32 rows: 16-byte loads when d % 4 == 0 (rows are then 16-byte aligned)
+template <>
+__device__ __forceinline__ float dot_full<float>(const float *q, const float *__restrict__ k, int d)
+{
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    if ((d & 3) == 0) {
+        const float4 *k4 = reinterpret_cast<const float4 *>(k);
+#pragma unroll 8
+        for (int t = 0; t < d / 4; ++t) {
+            const float4 kv = __ldg(k4 + t);
+            a0 = fmaf(q[4 * t], kv.x, a0);
+            a1 = fmaf(q[4 * t + 1], kv.y, a1);
+            a2 = fmaf(q[4 * t + 2], kv.z, a2);
+            a3 = fmaf(q[4 * t + 3], kv.w, a3);
+        }
+        return (a0 + a1) + (a2 + a3);
+    }
+    for (int t = 0; t < d; ++t) a0 = fmaf(q[t], k[t], a0);
+    return a0;
+}
+
+template <typename T>
 __device__ __forceinline__ float dot_full(const float *q, const T *__restrict__ k, int d)
 {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -396,10 +420,24 @@ mhsa_simt_row_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K
     const T *q = Q + ((size_t)bh * A.n + i) * d;
     for (int t = tid; t < d; t += kRowThreads) qsh[t] = to_f(q[t]);
     int4 g[4];
-    const int ns = A.nseg[i];
+    int ns, len;
+    if (A.has_pat) {
+        // the row's runs in closed form from the descriptor (the affine indices of P:216-219):
+        // no dependent metadata load before the K rows are fetched
+        Seg sg[4];
+        ns = row_segments(A.pat, i, sg);
+        len = 0;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) g[s] = A.seg[(size_t)i * 4 + s];
-    const int len = (int)(A.row_ptr[i + 1] - A.row_ptr[i]);
+        for (int s = 0; s < 4; ++s) {
+            g[s] = s < ns ? make_int4(sg[s].start, sg[s].step, sg[s].count, len) : make_int4(0, 1, 0, len);
+            if (s < ns) len += sg[s].count;
+        }
+    } else {
+        ns = A.nseg[i];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) g[s] = A.seg[(size_t)i * 4 + s];
+        len = (int)(A.row_ptr[i + 1] - A.row_ptr[i]);
+    }
     const T *Kb = K + (size_t)bh * A.n * d;
     const T *Vb = V + (size_t)bh * A.n * d;
     __syncthreads();
@@ -408,6 +446,11 @@ mhsa_simt_row_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K
         const int e = e0 + tid;
         const bool valid = e < len;
         const int col = valid ? col_of(g, ns, e) : 0;
+        if (valid) {
+            // the key's V row into L2 now: the accumulation below then reads it from L2, not HBM
+            const char *vrow = reinterpret_cast<const char *>(Vb + (size_t)col * d);
+            for (int b = 0; b < d * (int)sizeof(T); b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(vrow + b));
+        }
         const float s = valid ? scale * dot_full(qsh, Kb + (size_t)col * d, d) : -INFINITY;
         float cm = s;
 #pragma unroll
@@ -430,7 +473,14 @@ mhsa_simt_row_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K
         acc0 *= alpha;
         acc1 *= alpha;
         const int cnt = min(kRowThreads, len - e0);
-        if (tid < d) {
+        if (d <= kRowThreads / 2) {
+            // two key groups (even / odd keys) over the same output column: twice the loads in flight
+            const int t = tid & (kRowThreads / 2 - 1), grp = tid / (kRowThreads / 2);
+            if (t < d) {
+#pragma unroll 16
+                for (int j = grp; j < cnt; j += 2) acc0 = fmaf(psh[j], to_f(Vb[(size_t)csh[j] * d + t]), acc0);
+            }
+        } else if (tid < d) {
             const bool two = tid + kRowThreads < d;
 #pragma unroll 8
             for (int j = 0; j < cnt; ++j) {
@@ -443,6 +493,13 @@ mhsa_simt_row_kernel(DevAcsr A, const T *__restrict__ Q, const T *__restrict__ K
     }
     const float inv = l > 0.f ? 1.f / l : 0.f;
     T *o = O + ((size_t)bh * A.n + i) * d;
+    if (d <= kRowThreads / 2) {
+        // the odd-key group's partial sums join the even group's (fixed order: deterministic)
+        if (tid >= kRowThreads / 2) psh[tid - kRowThreads / 2] = acc0;
+        __syncthreads();
+        if (tid < d) o[tid] = from_f<T>((acc0 + psh[tid]) * inv);
+        return;
+    }
     if (tid < d) o[tid] = from_f<T>(acc0 * inv);
     if (tid + kRowThreads < d) o[tid + kRowThreads] = from_f<T>(acc1 * inv);
 }
