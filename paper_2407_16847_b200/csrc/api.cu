@@ -145,6 +145,8 @@ void free_device(splat_acsr_s *a)
     cudaFree(a->plan.d_pair_ent);
     cudaFree(a->plan.d_pair_info);
     cudaFree(a->plan.d_masks);
+    cudaFree(a->plan.d_mask_rec);
+    cudaFree(a->plan.d_mask_cnt);
     cudaFree(a->plan.d_kv_mask);
     cudaFree(a->plan.d_qt_bits);
     cudaFree(a->plan.d_t_info);
@@ -176,6 +178,8 @@ DevAcsr dev_view(const splat_acsr_s *a, int slot = 0)
     A.pair_ent = a->plan.d_pair_ent;
     A.pair_info = reinterpret_cast<const int4 *>(a->plan.d_pair_info);
     A.masks = reinterpret_cast<const uint4 *>(a->plan.d_masks);
+    A.mask_rec = reinterpret_cast<const uint4 *>(a->plan.d_mask_rec);
+    A.mask_cnt = a->plan.d_mask_cnt;
     A.kv_mask = a->plan.d_kv_mask;
     A.qt_bits = a->plan.d_qt_bits;
     A.n_pairs = a->plan.n_pairs;
@@ -262,6 +266,8 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
         (e = dev_alloc(&P.d_pair_ent, sizeof(int32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
         (e = dev_alloc(&P.d_pair_info, sizeof(int32_t) * 8 * P.n_pairs)) != cudaSuccess ||
         (e = dev_alloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_mask_rec, sizeof(uint16_t) * (P.mask_rec.empty() ? 16 : P.mask_rec.size()))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_mask_cnt, P.mask_cnt.empty() ? 16 : P.mask_cnt.size())) != cudaSuccess ||
         (e = dev_alloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
         (e = dev_alloc(&P.d_qt_bits, sizeof(uint32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
         (e = dev_alloc(&P.d_t_info, sizeof(int32_t) * 4 * P.n_qt)) != cudaSuccess ||
@@ -281,6 +287,10 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
         e = cudaMemcpyAsync(P.d_pair_info, P.pair_info.data(), sizeof(int32_t) * 8 * P.n_pairs, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && !P.masks.empty())
         e = cudaMemcpyAsync(P.d_masks, P.masks.data(), sizeof(uint32_t) * P.masks.size(), cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && !P.mask_rec.empty())
+        e = cudaMemcpyAsync(P.d_mask_rec, P.mask_rec.data(), sizeof(uint16_t) * P.mask_rec.size(), cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && !P.mask_cnt.empty())
+        e = cudaMemcpyAsync(P.d_mask_cnt, P.mask_cnt.data(), P.mask_cnt.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && P.n_entries > 0)
         e = cudaMemcpyAsync(P.d_kv_mask, P.kv_mask.data(), sizeof(int32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && P.n_entries > 0)

@@ -23,6 +23,8 @@ struct DevAcsr {
     const int32_t *pair_ent;    // kv | kUseA | kUseB | kPartA | kPartB
     const int4 *pair_info;      // [n_pairs][2]: (pair, e0, e1, jA0), (jA1, jB1, 0, 0) in pair_order order
     const uint4 *masks;         // [n_masks][128]: row column masks
+    const uint4 *mask_rec;      // [n_masks][128][2]: R-SpMM row records (16 x u16 per row)
+    const uint8_t *mask_cnt;    // [n_masks][128]: live columns per row
     const int32_t *kv_mask;     // [n_entries]: mask id per (query tile, key tile) entry, -1 = FULL
     const uint32_t *qt_bits;    // [n_entries]: chunk live (bit 4 quad + w) / full (bit 16 + 4 quad + w)
     int n_pairs, n_buckets;

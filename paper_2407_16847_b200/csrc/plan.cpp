@@ -214,6 +214,21 @@ void build_plan(splat_acsr_s &a)
         }
     }
     P.n_masks = (int)(P.masks.size() / (128 * 4));
+    // R-SpMM row records of every PARTIAL mask: per row and 8-column group g the live columns left
+    // of the group (low byte) and the group's 8 mask bits (high byte), and per row the live count
+    P.mask_rec.assign((size_t)P.n_masks * 128 * 16, 0);
+    P.mask_cnt.assign((size_t)P.n_masks * 128, 0);
+    for (int m = 0; m < P.n_masks; ++m)
+        for (int r = 0; r < 128; ++r) {
+            const uint32_t *w = &P.masks[((size_t)m * 128 + r) * 4];
+            int pre = 0;
+            for (int g = 0; g < 16; ++g) {
+                const uint32_t byte = (w[g >> 2] >> (8 * (g & 3))) & 0xFFu;
+                P.mask_rec[((size_t)m * 128 + r) * 16 + g] = (uint16_t)(pre | (byte << 8));
+                pre += __builtin_popcount(byte);
+            }
+            P.mask_cnt[(size_t)m * 128 + r] = (uint8_t)(pre > 255 ? 255 : pre);   // <= 128
+        }
     P.kv_mask.assign(P.n_entries, -1);
     for (int e = 0; e < P.n_pair_entries; ++e)
         for (int g = 0; g < 2; ++g)

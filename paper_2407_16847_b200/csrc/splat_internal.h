@@ -178,6 +178,8 @@ struct Plan {
     std::vector<int32_t> pair_info;   // [n_pairs][8]: pair, e0, e1, jA0, jA1, jB1, 0, 0 -- in pair_order order
     std::vector<int32_t> pair_mask;   // [n_pair_entries][2]: mask id of tile A / B (-1: FULL or unused)
     std::vector<uint32_t> masks;      // [n_masks][128 rows][4 words]: column mask of each row
+    std::vector<uint16_t> mask_rec;   // [n_masks][128 rows][16 groups]: live columns before the group | group bits << 8
+    std::vector<uint8_t> mask_cnt;    // [n_masks][128 rows]: live columns of the row
     std::vector<int32_t> kv_mask;     // [n_entries]: mask id of each (query tile, key tile) entry (-1: FULL)
     std::vector<uint32_t> qt_bits;    // [n_entries]: per-warp chunk live (bits 0-15) / full (bits 16-31)
     int t_n_buckets = 0;
@@ -186,6 +188,8 @@ struct Plan {
     int32_t *d_qt_ptr = nullptr, *d_kv = nullptr, *d_order = nullptr;
     int32_t *d_pair_ent = nullptr, *d_pair_info = nullptr;
     uint32_t *d_masks = nullptr;
+    uint16_t *d_mask_rec = nullptr;
+    uint8_t *d_mask_cnt = nullptr;
     int32_t *d_kv_mask = nullptr;
     uint32_t *d_qt_bits = nullptr;
     int32_t *d_t_info = nullptr;

@@ -527,31 +527,40 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             const bool rvalid = t * 128 + r < A.n;
             long long run = 0;
             // the unit's plan words and mask ids, lane l holding entry e0 + l (the warp's copy is
-            // broadcast by shuffle; entries past 32 are read from global memory), and the row mask
-            // of the next entry loaded one entry ahead
+            // broadcast by shuffle; entries past 32 are read from global memory); a PARTIAL entry's
+            // row record (precomputed per mask by the planner: live columns before each 8-column
+            // group, the group's bits) and live count are loaded one entry ahead
             const int ne = e1 - e0;
             const int ent_l = lane < ne ? A.kv[e0 + lane] : 0;
             const int mid_l = lane < ne ? A.kv_mask[e0 + lane] : -1;
             auto ent_of = [&](int i) { return i < 32 ? __shfl_sync(0xffffffffu, ent_l, i) : A.kv[e0 + i]; };
-            auto mask_of = [&](int i, int en) {
-                const int mid = i < 32 ? __shfl_sync(0xffffffffu, mid_l, i) : A.kv_mask[e0 + i];
-                uint4 m = make_uint4(~0u, ~0u, ~0u, ~0u);
-                if (en & kPartialBit) m = A.masks[(size_t)mid * 128 + r];
-                return m;
+            auto rec_of = [&](int i, int en, uint4 &rc, int &cn) {
+                if (en & kPartialBit) {
+                    const int mid = i < 32 ? __shfl_sync(0xffffffffu, mid_l, i) : A.kv_mask[e0 + i];
+                    rc = A.mask_rec[((size_t)mid * 128 + r) * 2 + (lane >> 4)];
+                    cn = A.mask_cnt[(size_t)mid * 128 + r];
+                } else {
+                    // FULL entry: every group of a valid row is live, group g starts at 8 g
+                    const uint32_t b8 = rvalid ? 0xFF00u : 0u, g0 = lane < 16 ? 0u : 64u;
+                    rc = make_uint4((g0 | b8) | ((g0 + 8u) | b8) << 16, ((g0 + 16u) | b8) | ((g0 + 24u) | b8) << 16,
+                                    ((g0 + 32u) | b8) | ((g0 + 40u) | b8) << 16, ((g0 + 48u) | b8) | ((g0 + 56u) | b8) << 16);
+                    cn = rvalid ? 128 : 0;
+                }
             };
             int ent = ne > 0 ? ent_of(0) : 0;
-            uint4 m4 = ne > 0 ? mask_of(0, ent) : make_uint4(0u, 0u, 0u, 0u);
+            uint4 rc4 = make_uint4(0u, 0u, 0u, 0u);
+            int cn4 = 0;
+            if (ne > 0) rec_of(0, ent, rc4, cn4);
             PSPAN_END(3, t_unit);
             for (int e = e0; e < e1; ++e, ++k) {
-                const uint4 mc = rvalid ? m4 : make_uint4(0u, 0u, 0u, 0u);
-                const int ent_cur = ent;
+                const uint4 rc = rc4;
+                const int cnt = cn4;
                 if (e + 1 < e1) {
                     ent = ent_of(e + 1 - e0);
-                    m4 = mask_of(e + 1 - e0, ent);
+                    rec_of(e + 1 - e0, ent, rc4, cn4);
                 }
                 const int s = k % C::NSTG;
                 if (k >= C::NSTG) PWAIT(4, &stg_empty[s], ((k / C::NSTG) - 1) & 1);
-                const int cnt = __popc(mc.x) + __popc(mc.y) + __popc(mc.z) + __popc(mc.w);
                 const long long b0 = 2ll * (rowoff + run), b1 = b0 + 2ll * cnt;
                 run += cnt;
                 const long long a0 = b0 & ~15ll;
@@ -570,33 +579,11 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     bytes = (uint32_t)(a1 - a0);
                 }
                 {
-                    // row record: lanes 0-15 write column groups 0-7 (mask words 0, 1), lanes 16-31
-                    // groups 8-15 (words 2, 3) of row r
-                    const uint32_t shift = (uint32_t)((b0 - a0) >> 1);
-                    const uint32_t wa = lane < 16 ? mc.x : mc.z, wb = lane < 16 ? mc.y : mc.w;
-                    const uint32_t base = shift + (lane < 16 ? 0u : (uint32_t)(__popc(mc.x) + __popc(mc.y)));
-                    uint32_t rec[4];
-                    if (!(ent_cur & kPartialBit)) {
-                        // FULL entry: every group of a valid row is live, group g starts at shift + 8 g
-                        const uint32_t b8 = rvalid ? 0xFF00u : 0u, g0 = shift + (lane < 16 ? 0u : 64u);
-#pragma unroll
-                        for (int g2 = 0; g2 < 4; ++g2)
-                            rec[g2] = ((g0 + 16u * g2) | b8) | (((g0 + 16u * g2 + 8u) | b8) << 16);
-                    } else
-#pragma unroll
-                    for (int g2 = 0; g2 < 4; ++g2) {
-                        uint32_t v = 0;
-#pragma unroll
-                        for (int hh = 0; hh < 2; ++hh) {
-                            const int g = 2 * g2 + hh;            // group within this half: word g / 4, byte g % 4
-                            const uint32_t wd = g < 4 ? wa : wb;
-                            const uint32_t bsh = 8u * (uint32_t)(g & 3);
-                            const uint32_t pre = (g < 4 ? 0u : (uint32_t)__popc(wa)) + (uint32_t)__popc(wd & ((1u << bsh) - 1u));
-                            v |= ((base + pre) | (((wd >> bsh) & 0xFFu) << 8)) << (16 * hh);
-                        }
-                        rec[g2] = v;
-                    }
-                    *reinterpret_cast<uint4 *>(rrec + (s * 128 + r) * 32 + (lane >> 4) * 16) = make_uint4(rec[0], rec[1], rec[2], rec[3]);
+                    // row record: lanes 0-15 write column groups 0-7, lanes 16-31 groups 8-15 of row r;
+                    // the span's element shift in its staged row is added to every group's index
+                    const uint32_t sh2 = (uint32_t)((b0 - a0) >> 1) * 0x00010001u;
+                    *reinterpret_cast<uint4 *>(rrec + (s * 128 + r) * 32 + (lane >> 4) * 16) =
+                        make_uint4(rc.x + sh2, rc.y + sh2, rc.z + sh2, rc.w + sh2);
                 }
                 // The warp copies its 16 rows' spans (16-byte granules, <= 17 per row, coalesced), then every thread
                 // registers an arrive-on for its copies and lane 0 arrives for the warp (releasing
