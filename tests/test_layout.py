@@ -107,3 +107,25 @@ def test_column_compressed_rspmm_matches_oracle(p, dt, d):
     # and against the oracle's attention output (P in fp64): same bound
     err2 = np.abs(Oc.float().cpu().numpy().reshape(B * H, n, d) - np.stack(Os)).max()
     assert err2 <= tol, err2
+
+
+def test_layout_abi_errors():
+    L = S.lib()
+    import ctypes as C
+    assert L.splat_layout_choice(None, 0.1) == 0
+    h = C.c_void_p()
+    assert L.splat_acsr_transpose(None, None, C.byref(h)) == 1            # INVALID_ARG
+    a = S.Acsr(Pattern("window", 64, lo=2, hi=2), device=-1)
+    at = S.splat_acsr_transpose(a)
+    # host inspection handles have no compute path (no CPU fallback)
+    assert L.splat_transpose_values(a.handle, at.handle, None, None, 1, 1, 1, None) == 1
+    assert L.splat_rspmm_cc(a.handle, at.handle, None, None, 1, 1, 1, 16, None, None) == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", PATTERNS, ids=lambda p: p.kind)
+def test_device_transpose_handle_equals_host(p):
+    ah, ad = S.Acsr(p, device=-1), S.Acsr(p)
+    th, td = S.splat_acsr_transpose(ah), S.splat_acsr_transpose(ad)
+    for x, y in zip(th.copy_meta(), td.copy_meta()):
+        assert torch.equal(x, y)

@@ -17,3 +17,9 @@ done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"mhsa_tc" -s 6 -c 2 \
     -o gpurun_out/${TAG}_prof_sparse_transformer python bench.py --config sparse_transformer --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ls -la gpurun_out | tail -20
+# unfused primitives (Longformer): one ncu --set full capture each, and their timings
+for k in rsddmm softmax rspmm; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+      -o gpurun_out/${TAG}_prof_unf_$k python tools/bench_unfused.py --configs longformer --iters 2 > /dev/null 2>&1
+done
+timeout 600 python tools/bench_unfused.py --configs longformer,bigbird,sparse_transformer --iters 10 > gpurun_out/${TAG}_unfused.jsonl 2>&1
