@@ -10,6 +10,7 @@
 #include <cstring>
 #include <atomic>
 #include <new>
+#include <stdexcept>
 
 #include "kernels.h"
 #include "splat_internal.h"
@@ -241,6 +242,20 @@ namespace {
 
 // Device metadata is in a->d_seg / d_nseg / d_row_ptr (queued on cs): copy it to the host,
 // build the tile plan and upload it.  Frees `a` on failure.
+// The tile plan, with host allocation failures and oversize plans reported instead of thrown
+// through the C ABI.
+splat_status plan_or_error(splat_acsr_s &a)
+{
+    try {
+        build_plan(a);
+    } catch (const std::bad_alloc &) {
+        return set_error(SPLAT_ERR_OOM, "host allocation of the tile plan failed");
+    } catch (const std::length_error &e) {
+        return set_error(SPLAT_ERR_UNSUPPORTED, "tile plan: %s", e.what());
+    }
+    return SPLAT_OK;
+}
+
 splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *out)
 {
     const int N = a->n;
@@ -258,7 +273,11 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
         return cuda_fail(e, "acsr build");
     }
     finish_host_meta(a);
-    build_plan(*a);
+    if (const splat_status ps = plan_or_error(*a); ps != SPLAT_OK) {
+        free_device(a);
+        delete a;
+        return ps;
+    }
     Plan &P = a->plan;
     if ((e = dev_alloc(&P.d_qt_ptr, sizeof(int32_t) * (P.n_qt + 1))) != cudaSuccess ||
         (e = dev_alloc(&P.d_kv, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
@@ -387,7 +406,10 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
             a->row_ptr_h[i + 1] = a->row_ptr_h[i] + off;
         }
         finish_host_meta(a);
-        build_plan(*a);
+        if (const splat_status ps = plan_or_error(*a); ps != SPLAT_OK) {
+            delete a;
+            return ps;
+        }
         *out = a;
         return SPLAT_OK;
     }
@@ -582,7 +604,14 @@ extern "C" {
 
 splat_status splat_acsr_build(const splat_pattern *p, int device, void *stream, splat_acsr *out)
 {
-    splat_status st = build_impl(p, device, stream, out, false);
+    splat_status st;
+    try {
+        st = build_impl(p, device, stream, out, false);
+    } catch (const std::bad_alloc &) {
+        // host metadata of a huge N (the per-row vectors are allocated before the plan)
+        if (out) *out = nullptr;
+        return set_error(SPLAT_ERR_OOM, "host allocation of the ACSR metadata failed");
+    }
     if (st == SPLAT_OK) build_residue_split(*out, stream);
     if (st == SPLAT_OK && (st = create_call_resources(*out)) != SPLAT_OK) {
         free_device(*out);
@@ -631,7 +660,10 @@ splat_status splat_acsr_from_mask(const uint32_t *mask, int32_t n, int32_t max_r
             a->row_ptr_h[i + 1] = a->row_ptr_h[i] + cnt;
         }
         finish_host_meta(a);
-        build_plan(*a);
+        if (const splat_status ps = plan_or_error(*a); ps != SPLAT_OK) {
+            delete a;
+            return ps;
+        }
         *out = a;
         return SPLAT_OK;
     }

@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <numeric>
+#include <stdexcept>
+#include <unordered_map>
 
 #include "splat_internal.h"
 
@@ -75,6 +77,7 @@ void build_plan(splat_acsr_s &a)
             P.kv.push_back(kv | (full ? 0 : kPartialBit));
             j = kv + wb;
         }
+        if (P.kv.size() > (size_t)0x7fffffff) throw std::length_error("tile plan exceeds 2^31 entries");
         P.qt_ptr[t + 1] = (int32_t)P.kv.size();
     }
     P.n_entries = (int)P.kv.size();
@@ -174,6 +177,10 @@ void build_plan(splat_acsr_s &a)
     // (the softmax skips the fast-index mask there).
     P.qt_bits.assign(P.n_entries, 0xFFFFFFFFu);
     P.masks.clear();
+    // masks are deduplicated by content (a strided or windowed pattern repeats a few row masks
+    // across its tiles): hash -> mask ids with that hash
+    std::unordered_map<uint64_t, std::vector<int32_t>> seen;
+    std::vector<uint32_t> mbuf(128 * 4);
     for (int p = 0; p < P.n_pairs; ++p) {
         for (int e = P.pair_ptr[p]; e < P.pair_ptr[p + 1]; ++e) {
             const int ent = P.pair_ent[e], c0 = (ent & kKvMask) * kKvUnit;
@@ -181,9 +188,8 @@ void build_plan(splat_acsr_s &a)
                 const int t = 2 * p + g;
                 if (!(ent & (g == 0 ? kUseA : kUseB))) continue;
                 if (!(ent & (g == 0 ? kPartA : kPartB))) continue;
-                const size_t base = P.masks.size();
-                P.masks.resize(base + 128 * 4, 0u);
-                uint32_t *m = &P.masks[base];
+                std::fill(mbuf.begin(), mbuf.end(), 0u);
+                uint32_t *m = mbuf.data();
                 for (int r = 0; r < 128; ++r) {
                     const int i = t * bm + r;
                     if (i >= N) continue;
@@ -197,7 +203,18 @@ void build_plan(splat_acsr_s &a)
                         for (int c = first; c <= hi; c += step) m[4 * r + ((c - c0) >> 5)] |= 1u << ((c - c0) & 31);
                     }
                 }
-                P.pair_mask[(size_t)e * 2 + g] = (int32_t)(base / (128 * 4));
+                uint64_t h = 1469598103934665603ull;                 // FNV-1a over the 512 words
+                for (uint32_t x : mbuf) h = (h ^ x) * 1099511628211ull;
+                int32_t id = -1;
+                auto &cand = seen[h];
+                for (int32_t c : cand)
+                    if (std::equal(mbuf.begin(), mbuf.end(), P.masks.begin() + (size_t)c * 128 * 4)) { id = c; break; }
+                if (id < 0) {
+                    id = (int32_t)(P.masks.size() / (128 * 4));
+                    P.masks.insert(P.masks.end(), mbuf.begin(), mbuf.end());
+                    cand.push_back(id);
+                }
+                P.pair_mask[(size_t)e * 2 + g] = id;
                 uint32_t bits = 0;
                 for (int q = 0; q < 4; ++q)
                     for (int w = 0; w < 4; ++w) {
