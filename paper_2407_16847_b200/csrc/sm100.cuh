@@ -171,18 +171,17 @@ __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gsrc, uint
                  : "memory");
 }
 
-// 16-byte asynchronous copy global -> shared (L2 only), and the arrive-on that fires once every
-// cp.async issued so far by this thread has landed (pending count +1 now, -1 then)
+// 16-byte asynchronous copy global -> shared (L2 only), completion tracked by commit / wait groups
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc)
 {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
                  "l"(reinterpret_cast<uint64_t>(gsrc))
                  : "memory");
 }
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar)
-{
-    asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// every committed cp.async group but the newest one / all of them have landed (this thread's)
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // the source smem of every committed bulk store has been read (may be overwritten)

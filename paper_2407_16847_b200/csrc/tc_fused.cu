@@ -842,9 +842,12 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         for (int gg = 0; gg < 2; ++gg) {
             uint64_t *b = reinterpret_cast<uint64_t *>(smem + C::OFF_BAR) + gg * C::NB;
             for (int i = 0; i < 2 * C::QS + 4 * C::KS; ++i) mbar_init(&b[i], 1);
-            // q_empty: the unit's last PV (MMA commit) and the 4 softmax warps, done with the unit's
-            // header and entry table -- the producer rewrites both only after all five
-            for (int i = 0; i < C::QS; ++i) mbar_init(&b[C::QS + i], 5);
+            // q_full: every lane of the producer warp publishes its writes of the unit's header /
+            // entry table itself (lane 0's arrival carries the Q tile's bytes); q_empty: the unit's
+            // last PV (MMA commit) and every softmax thread, done reading them -- the producer
+            // rewrites both only after all of these
+            for (int i = 0; i < C::QS; ++i) mbar_init(&b[i], 32);
+            for (int i = 0; i < C::QS; ++i) mbar_init(&b[C::QS + i], 129);
             const int o = 2 * C::QS + 4 * C::KS;
             mbar_init(&b[o + 0], 1);   // s_full  (MMA commit)
             mbar_init(&b[o + 1], 4);   // s_empty (4 softmax warps)
@@ -902,20 +905,20 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             const KvRegs kr = nkr;
             if (qc >= C::QS) FWAIT(8, &q_empty[qi], qph ^ 1);
             if (un.t < 0) {
-                if (lane == 0) {
-                    hdr[qi] = make_int4(-1, 0, 0, 0);
-                    mbar_arrive(&q_full[qi]);
-                }
+                if (lane == 0) hdr[qi] = make_int4(-1, 0, 0, 0);
+                mbar_arrive(&q_full[qi]);
                 break;
             }
             nx = grab();                      // next unit, fetched in the shadow of this one
             if (lane < un.j1 - un.j0 && lane < C::kInfo)
                 info[qi * C::kInfo + lane] = make_int2(A.kv_mask[un.j0 + lane], (int)A.qt_bits[un.j0 + lane]);
             if (lane == 0) hdr[qi] = make_int4(un.t, un.bh, un.j0, un.j1);
-            __syncwarp();                     // header + table published by lane 0's arrive (release)
+            // header + table: each lane's arrival releases its own writes; lane 0's carries the Q bytes
             if (lane == 0) {
                 mbar_expect_tx(&q_full[qi], C::TB);
                 tma_load_3d(gs + C::OFF_Q + qi * C::TB, &tmQ, &q_full[qi], 0, un.t * 128, un.bh);
+            } else {
+                mbar_arrive(&q_full[qi]);
             }
             ++qc;
             if (++qi == C::QS) { qi = 0; qph ^= 1; }
@@ -1124,8 +1127,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 SPLAT_NEXT_UNIT_PREFETCH();
                 if (pe_on) { epilogue(pe_l, pe_t, pe_bh); pe_on = false; }
                 epilogue(0.f, un.t, un.bh);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&q_empty[slot]);
+                mbar_arrive(&q_empty[slot]);
                 continue;
             }
             for (int j = j0; j < j1; ++j) {
@@ -1224,8 +1226,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 first = false;
             }
 #undef SPLAT_NEXT_UNIT_PREFETCH
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&q_empty[slot]);   // header + entry table of this slot consumed
+            mbar_arrive(&q_empty[slot]);   // header + entry table of this slot consumed (every thread)
             pe_on = true;
             pe_l = l_run;
             pe_t = un.t;

@@ -380,7 +380,8 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 // (row, key tile) span is one contiguous run of <= 256 bytes.  The P producer warpgroup (thread =
 // query row) publishes the row's column mask and alignment shift, and each producer warp copies
 // its 32 rows' spans (16-byte aligned supersets, one coalesced cp.async request per row) into a
-// staging ring in SMEM -- the whole tile (up to 32 KB) in flight at once, no registers held.  (One
+// staging ring in SMEM -- a tile (up to 32 KB) in flight while the previous one completes, no
+// registers held.  (One
 // cp.async.bulk per row was tried: the TMA unit takes ~80 cycles per small copy, 0.71 ms on
 // Longformer.)  Two expander warpgroups take the
 // staged tiles in turn and scatter them into a dense 128B-swizzled bf16 P tile (lane = 4 columns:
@@ -391,6 +392,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 //   warp 0 : V producer (TMA)            warp 1 : MMA issuer
 //   warps 4-7   : epilogue (thread = query row = TMEM lane)
 //   warps 8-15          : P producer (warp w: rows 16 (w - 8) .. +15, lane = row for the row table;
+//                         a stage is published one entry late, when its cp.async group completes;
 //                         one warp's copies issue at ~one 272-byte request per 125 cycles, so eight
 //                         warps share each tile)
 //   warps 16-19, 20-23  : expanders (entry k -> expander k % 2, dense P buffer k % 2)
@@ -443,7 +445,9 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < C::KS; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
-        for (int i = 0; i < C::NSTG; ++i) { mbar_init(&stg_full[i], 8); mbar_init(&stg_empty[i], 4); }
+        // every producer thread publishes its own copies and row-record writes (stg_full), every
+        // expander thread its reads of the stage (stg_empty): each writer / reader arrives itself
+        for (int i = 0; i < C::NSTG; ++i) { mbar_init(&stg_full[i], 256); mbar_init(&stg_empty[i], 128); }
         for (int i = 0; i < kNExp; ++i) { mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&o_full[i], 1); mbar_init(&o_empty[i], 4); }
         fence_mbar_init();
@@ -515,6 +519,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
         const long long total_b = 2ll * (long long)prm.BH * (prm.pass ? prm.nat_nnz : A.nnz);   // bytes of P
         const long long end_a = total_b & ~15ll;       // bulk copies stay below this (16-byte granules)
         uint32_t k = 0;
+        int s_prev = -1;             // stage of the previous entry: published once its copies land
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
             unit_tile(A, u, bh, t);
@@ -585,9 +590,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     *reinterpret_cast<uint4 *>(rrec + (s * 128 + r) * 32 + (lane >> 4) * 16) =
                         make_uint4(rc.x + sh2, rc.y + sh2, rc.z + sh2, rc.w + sh2);
                 }
-                // The warp copies its 16 rows' spans (16-byte granules, <= 17 per row, coalesced), then every thread
-                // registers an arrive-on for its copies and lane 0 arrives for the warp (releasing
-                // the row table and tail bytes written above).
+                // The warp copies its 16 rows' spans (16-byte granules, <= 17 per row, coalesced).
                 PSPAN_BEGIN(t_copy);
                 const uint32_t ng = bytes >> 4;
                 const uint32_t stg_row0 = (uint32_t)(s * 128 + (warp - 8) * 16) * kStgRow;
@@ -606,12 +609,17 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     if (lane < 16 && ng > 16u)
                         cp_async16(smem + C::OFF_STG + stg_row0 + lane * kStgRow + 256, Pb + a0 + 256);
                 }
-                cp_async_mbar_arrive(&stg_full[s]);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&stg_full[s]);
+                // this entry's copies form one cp.async group; the previous entry's group (all but
+                // the newest) is complete after wait_group 1, and its stage is published then
+                cp_async_commit();
+                cp_async_wait1();
+                if (s_prev >= 0) mbar_arrive(&stg_full[s_prev]);
+                s_prev = s;
                 PSPAN_END(5, t_copy);
             }
         }
+        cp_async_wait0();
+        if (s_prev >= 0) mbar_arrive(&stg_full[s_prev]);
     } else if (warp >= 16) {
         // ---------------------------------------------------------------- expanders
         // expander x takes entries k = x, x + 2, ...; warp q of it fills rows q, q + 4, ... (rows
@@ -691,10 +699,8 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             fence_proxy_async_smem();
             __syncwarp();
             PSPAN_END(4, t_fence);
-            if (lane == 0) {
-                mbar_arrive(&stg_empty[s]);
-                mbar_arrive(&p_full[x]);
-            }
+            mbar_arrive(&stg_empty[s]);
+            if (lane == 0) mbar_arrive(&p_full[x]);
           }
           k = kend;
         }
