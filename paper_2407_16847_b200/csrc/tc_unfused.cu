@@ -405,17 +405,18 @@ struct CfgP {
     static constexpr int kChunks = D / 64;
     static constexpr int kTileBytes = kChunks * kSub;                 // V tile
     static constexpr int KS = D == 64 ? 3 : 2;                        // V ring
-    static constexpr int NSTG = D == 64 ? 3 : 2;                      // P staging ring
+    static constexpr int NSTG = 4;                                    // P staging ring
     static constexpr int OFF_V = 0;
-    static constexpr int OFF_P = OFF_V + KS * kTileBytes;             // [kNExp] dense P tiles, 32 KB each
-    static constexpr int OFF_STG = OFF_P + kNExp * 2 * kSub;          // [NSTG][128 rows][kStgRow]
+    static constexpr int OFF_STG = OFF_V + KS * kTileBytes;           // [NSTG][128 rows][kStgRow]
     // [NSTG][128 rows][16 column groups of 8] u16: low byte = staged element index of the group's
     // first live value, high byte = the group's 8 mask bits
     static constexpr int OFF_RM = OFF_STG + NSTG * 128 * kStgRow;
     static constexpr int OFF_BAR = OFF_RM + NSTG * 128 * 32;
     static constexpr int NBAR = 2 * KS + 2 * NSTG + 2 * kNExp + 4;
     static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16;   // the dynamic buffer is 1024-aligned (checked)
-    static constexpr int TMEM_COLS = 2 * D;                           // O double buffer
+    // TMEM: O double buffer [0, 2D), then the dense P tile of each expander (128 keys as 64
+    // columns of bf16 pairs) at 2D + 64 x
+    static constexpr int TMEM_COLS = 2 * D + kNExp * 64 <= 256 ? 256 : 512;
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(OFF_STG % 16 == 0 && OFF_RM % 16 == 0 && OFF_BAR % 8 == 0, "alignment");
 };
@@ -448,7 +449,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
         // every producer thread publishes its own copies and row-record writes (stg_full), every
         // expander thread its reads of the stage (stg_empty): each writer / reader arrives itself
         for (int i = 0; i < C::NSTG; ++i) { mbar_init(&stg_full[i], 256); mbar_init(&stg_empty[i], 128); }
-        for (int i = 0; i < kNExp; ++i) { mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1); }
+        for (int i = 0; i < kNExp; ++i) { mbar_init(&p_full[i], 128); mbar_init(&p_empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&o_full[i], 1); mbar_init(&o_empty[i], 4); }
         fence_mbar_init();
         tma_prefetch(&tmV);
@@ -481,7 +482,7 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
         }
     } else if (warp == 1) {
         constexpr uint32_t idO = idesc_bf16(128, D, true);
-        const uint32_t sV = smem_u32(smem + C::OFF_V), sP = smem_u32(smem + C::OFF_P);
+        const uint32_t sV = smem_u32(smem + C::OFF_V);
         int ki = 0;
         uint32_t kph = 0, np = 0, uo = 0;   // np: P tiles consumed; uo: units started
         for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++uo) {
@@ -496,12 +497,12 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                 PWAIT(3, &p_full[pb], (np / kNExp) & 1);
                 ++np;
                 tc_fence_after();
-                const uint32_t vb = sV + ki * C::kTileBytes, pa = sP + pb * 2 * kSub;
+                const uint32_t vb = sV + ki * C::kTileBytes, pt = tmem + 2 * D + 64 * pb;
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk)
-                        mma_bf16_ss(tmem + ob * D, sdesc_sw128(pa + (kk >> 2) * kSub + (kk & 3) * 32, 16, 1024),
-                                    sdesc_sw128(vb + kk * 2048, kSub, 1024), idO, (first && kk == 0) ? 0u : 1u);
+                        mma_bf16_ts(tmem + ob * D, pt + kk * 8, sdesc_sw128(vb + kk * 2048, kSub, 1024), idO,
+                                    (first && kk == 0) ? 0u : 1u);
                     mma_commit(&v_empty[ki]);
                     mma_commit(&p_empty[pb]);
                 }
@@ -625,13 +626,12 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
         // expander x takes entries k = x, x + 2, ...; warp q of it fills rows q, q + 4, ... (rows
         // with many non-zeros, e.g. Longformer's global rows, all in the first 32 rows of tile 0,
         // are spread over the four warps).  Lane l owns columns 4l .. 4l + 3.
-        const int x = (warp - 16) >> 2, q = warp & 3;
-        uint8_t *ptile = smem + C::OFF_P + x * 2 * kSub;
-        // Half-warp h = lane / 16 takes one row, lane l16 = lane % 16 its columns 8 l16 .. 8 l16 + 7:
-        // one 16-byte swizzle chunk of the dense tile (sub-tile l16 / 8, chunk l16 % 8), the byte
-        // l16 % 4 of mask word l16 / 4.
-        const int h = lane >> 4, l16 = lane & 15;
-        const int sub = (l16 >> 3) * kSub, chunk = l16 & 7;
+        // Thread = query row = TMEM lane (warp q of the expander owns lanes 32 q .. 32 q + 31): the
+        // thread expands its own row, 8 columns (one group of its row record) at a time, from the
+        // staged span into bf16 pairs and writes them to the expander's P tile in TMEM (64 columns)
+        // with tcgen05.st; the MMA reads P from TMEM (TS form).
+        const int x = (warp - 16) >> 2, q = warp & 3, r = q * 32 + lane;
+        const uint32_t p_tm = tmem + ((uint32_t)(q * 32) << 16) + 2 * D + 64 * x;
         uint32_t k = 0, j = 0;     // k: CTA entry counter, j: this expander's tile counter
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
           int bh, t;
@@ -641,66 +641,59 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
             const int s = k % C::NSTG;
             PWAIT(5, &stg_full[s], (k / C::NSTG) & 1);
             if (j >= 1) PWAIT(6, &p_empty[x], (j - 1) & 1);
-            const uint8_t *stg = smem + C::OFF_STG + s * 128 * kStgRow;
-            // Rows q + 4 (2 i + h), i < 16: the group's 8 staged values from element qq (the row
-            // record: shift + live columns left of 8 l16) are one unaligned 16-byte read (five aligned
-            // words, funnel-shifted by the element parity), stored as is when all 8 columns are live,
-            // as zeros otherwise (branch-free, so the unrolled rows overlap); groups straddling a run
-            // boundary are redone below.
+            tc_fence_after();
             PSPAN_BEGIN(t_rows);
-#ifdef SPLAT_SPMM_NOEXP
-            if (false)
-#endif
-            uint32_t pend = 0;      // rows i whose group straddles a run boundary (bit i)
-            // four rows at a time, every shared-memory load issued before any store (the stores to
-            // the dense tile would otherwise order the next row's loads behind them)
-#pragma unroll 1
-            for (int i0 = 0; i0 < 16; i0 += 4) {
-                uint32_t rc[4], w[4][5];
+            const uint8_t *srow = smem + C::OFF_STG + (s * 128 + r) * kStgRow;
+            const uint4 *rp4 = reinterpret_cast<const uint4 *>(rrec + (s * 128 + r) * 32);
+            const uint4 ra = rp4[0], rb = rp4[1];
+            const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    rc[u] = *reinterpret_cast<const unsigned short *>(rrec + (s * 128 + q + 4 * (2 * (i0 + u) + h)) * 32 + 2 * l16);
+            for (int c4 = 0; c4 < 4; ++c4) {          // 4 groups = 32 keys = 16 TMEM columns per store
+                uint32_t pk[16];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int rr = q + 4 * (2 * (i0 + u) + h);
-                    const uint32_t *wp = reinterpret_cast<const uint32_t *>(stg + rr * kStgRow) + ((rc[u] & 0xFFu) >> 1);
+                for (int gg = 0; gg < 4; ++gg) {
+                    const int g = 4 * c4 + gg;
+                    const uint32_t rc = (rw[g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
+                    const uint32_t byte = rc >> 8, qq = rc & 0xFFu;           // staged element index
+                    // 8 values from element qq: an 8-byte-aligned 24-byte window (three LDS.64), the
+                    // words shifted by the window offset (0 / 1 word, 0 / 16 bits)
+                    const uint32_t b0 = 2u * qq, a8 = b0 & ~7u, o = b0 - a8;   // o in {0, 2, 4, 6}
+                    const uint2 *wp = reinterpret_cast<const uint2 *>(srow + a8);
+                    const uint2 u0 = wp[0], u1 = wp[1], u2 = wp[2];
+                    const uint32_t w[6] = {u0.x, u0.y, u1.x, u1.y, u2.x, u2.y};
+                    const uint32_t sw = o >> 2, sb = (o & 3u) * 8u;
+                    uint32_t v[4];
 #pragma unroll
-                    for (int c = 0; c < 5; ++c) w[u][c] = wp[c];
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const uint32_t lo = sw ? w[jj + 1] : w[jj], hi = sw ? w[jj + 2] : w[jj + 1];
+                        v[jj] = __funnelshift_r(lo, hi, sb);
+                    }
+                    if (byte != 0xFFu) {
+                        if (byte == 0u) {
+                            v[0] = v[1] = v[2] = v[3] = 0u;
+                        } else {
+                            // a group straddling a run boundary: value popc(byte & ((1 << c) - 1))
+                            // into each live column c
+                            const unsigned short *e = reinterpret_cast<const unsigned short *>(srow) + qq;
+                            uint32_t h[8];
+#pragma unroll
+                            for (int c = 0; c < 8; ++c)
+                                h[c] = ((byte >> c) & 1u) ? (uint32_t)e[__popc(byte & ((1u << c) - 1u))] : 0u;
+#pragma unroll
+                            for (int jj = 0; jj < 4; ++jj) v[jj] = h[2 * jj] | (h[2 * jj + 1] << 16);
+                        }
+                    }
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) pk[4 * gg + jj] = v[jj];
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int rr = q + 4 * (2 * (i0 + u) + h);
-                    const uint32_t byte = rc[u] >> 8;
-                    const uint32_t sh = (rc[u] & 1u) << 4, keep = byte == 0xFFu ? ~0u : 0u;
-                    pend |= (byte != 0u && byte != 0xFFu) ? (1u << (i0 + u)) : 0u;
-                    const uint4 o = make_uint4(__funnelshift_r(w[u][0], w[u][1], sh) & keep, __funnelshift_r(w[u][1], w[u][2], sh) & keep,
-                                               __funnelshift_r(w[u][2], w[u][3], sh) & keep, __funnelshift_r(w[u][3], w[u][4], sh) & keep);
-                    *reinterpret_cast<uint4 *>(ptile + sub + rr * 128 + ((chunk ^ (rr & 7)) << 4)) = o;
-                }
+                tmem_st16(p_tm + 16 * c4, pk);
             }
-            // groups straddling a run boundary (a few per row at the edges of a run): value
-            // popc(byte & ((1 << c) - 1)) into each live column c
-            while (pend) {
-                const int i = __ffs(pend) - 1;
-                pend &= pend - 1u;
-                const int rr = q + 4 * (2 * i + h);
-                const uint32_t rc = *reinterpret_cast<const unsigned short *>(rrec + (s * 128 + rr) * 32 + 2 * l16);
-                const uint32_t byte = rc >> 8, qq = rc & 0xFFu;
-                const unsigned short *e = reinterpret_cast<const unsigned short *>(stg + rr * kStgRow) + qq;
-                uint32_t v[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c)
-                    v[c] = ((byte >> c) & 1u) ? (uint32_t)e[__popc(byte & ((1u << c) - 1u))] : 0u;
-                *reinterpret_cast<uint4 *>(ptile + sub + rr * 128 + ((chunk ^ (rr & 7)) << 4)) =
-                    make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
-            }
+            tmem_wait_st();
             PSPAN_END(3, t_rows);
-            PSPAN_BEGIN(t_fence);
-            fence_proxy_async_smem();
-            __syncwarp();
-            PSPAN_END(4, t_fence);
+            tc_fence_before();
+            // every thread publishes its own row (P tile) and releases its staged row
             mbar_arrive(&stg_empty[s]);
-            if (lane == 0) mbar_arrive(&p_full[x]);
+            mbar_arrive(&p_full[x]);
           }
           k = kend;
         }
