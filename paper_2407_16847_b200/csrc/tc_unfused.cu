@@ -448,7 +448,9 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
         for (int i = 0; i < C::KS; ++i) { mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1); }
         // every producer thread publishes its own copies and row-record writes (stg_full), every
         // expander thread its reads of the stage (stg_empty): each writer / reader arrives itself
-        for (int i = 0; i < C::NSTG; ++i) { mbar_init(&stg_full[i], 256); mbar_init(&stg_empty[i], 128); }
+        // stg_full: per producer thread one arrival (its row-record writes) and one cp.async arrive-on
+        // (its copies) per stage use
+        for (int i = 0; i < C::NSTG; ++i) { mbar_init(&stg_full[i], 512); mbar_init(&stg_empty[i], 128); }
         for (int i = 0; i < kNExp; ++i) { mbar_init(&p_full[i], 128); mbar_init(&p_empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&o_full[i], 1); mbar_init(&o_empty[i], 4); }
         fence_mbar_init();
@@ -520,7 +522,6 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
         const long long total_b = 2ll * (long long)prm.BH * (prm.pass ? prm.nat_nnz : A.nnz);   // bytes of P
         const long long end_a = total_b & ~15ll;       // bulk copies stay below this (16-byte granules)
         uint32_t k = 0;
-        int s_prev = -1;             // stage of the previous entry: published once its copies land
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             int bh, t;
             unit_tile(A, u, bh, t);
@@ -610,17 +611,11 @@ rspmm_tc_kernel(const __grid_constant__ CUtensorMap tmV, const ParamsU prm)
                     if (lane < 16 && ng > 16u)
                         cp_async16(smem + C::OFF_STG + stg_row0 + lane * kStgRow + 256, Pb + a0 + 256);
                 }
-                // this entry's copies form one cp.async group; the previous entry's group (all but
-                // the newest) is complete after wait_group 1, and its stage is published then
-                cp_async_commit();
-                cp_async_wait1();
-                if (s_prev >= 0) mbar_arrive(&stg_full[s_prev]);
-                s_prev = s;
+                cp_async_mbar_arrive_noinc(&stg_full[s]);   // fires when this thread's copies land
+                mbar_arrive(&stg_full[s]);                  // releases this thread's record writes
                 PSPAN_END(5, t_copy);
             }
         }
-        cp_async_wait0();
-        if (s_prev >= 0) mbar_arrive(&stg_full[s_prev]);
     } else if (warp >= 16) {
         // ---------------------------------------------------------------- expanders
         // expander x takes entries k = x, x + 2, ...; warp q of it fills rows q, q + 4, ... (rows
