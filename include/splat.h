@@ -170,6 +170,20 @@ splat_status splat_plan_info(splat_acsr a, int32_t *bm, int32_t *bn, int32_t *n_
  *            used by the persistent kernels; ties by tile index) */
 splat_status splat_plan_copy(splat_acsr a, int32_t *qt_ptr, int32_t *kv, int32_t *order);
 
+/* Work of the d = 64 fused (split-group) kernel: its query tiles are two 64-row segments; with
+ * row_classes = 1 the planner regrouped the segments by row class (rows touching nearly every key
+ * block share tiles) because that needs fewer (tile, key window) entries; n_split_entries
+ * is the number of entries per (b, h) that kernel walks. */
+splat_status splat_plan_split_info(splat_acsr a, int32_t *row_classes, int32_t *n_split_entries);
+
+/* Inspection of the split kernel's plan (host copies, synchronous): splat_plan_sizes(a, 0) units
+ * per (b, h), (a, 1) entries (natural ones first, then the row-class ones), (a, 2) masks;
+ * splat_plan_split_copy copies units int32 [n][4] (tile -- or segments a | b << 16 when
+ * row_classes -- , j0, j1, 0), kv int32 [entries] (window start / 64 | PARTIAL bit 24), mask_id
+ * int32 [entries] (-1 = FULL) and masks uint32 [n_masks][128 rows][4] (column bits of the window). */
+int64_t splat_plan_sizes(splat_acsr a, int32_t which);
+splat_status splat_plan_split_copy(splat_acsr a, int32_t *units, int32_t *kv, int32_t *mask_id, uint32_t *masks);
+
 /* Free a handle and its device memory.  NULL is a no-op. */
 splat_status splat_acsr_destroy(splat_acsr a);
 

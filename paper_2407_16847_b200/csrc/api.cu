@@ -189,6 +189,7 @@ DevAcsr dev_view(const splat_acsr_s *a, int slot = 0)
     A.t_info = reinterpret_cast<const int4 *>(a->plan.d_t_info);
     A.sched = a->plan.d_sched ? a->plan.d_sched + 2 * slot : nullptr;
     A.t_n_buckets = a->plan.t_n_buckets;
+    A.row_classes = a->plan.row_classes;
     for (int b = 0; b <= a->plan.t_n_buckets && b <= kMaxBuckets; ++b) A.t_bucket_start[b] = a->plan.t_bucket_start[b];
     return A;
 }
@@ -280,15 +281,15 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
     }
     Plan &P = a->plan;
     if ((e = dev_alloc(&P.d_qt_ptr, sizeof(int32_t) * (P.n_qt + 1))) != cudaSuccess ||
-        (e = dev_alloc(&P.d_kv, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_kv, sizeof(int32_t) * (P.kv.empty() ? 1 : P.kv.size()))) != cudaSuccess ||
         (e = dev_alloc(&P.d_order, sizeof(int32_t) * P.n_qt)) != cudaSuccess ||
         (e = dev_alloc(&P.d_pair_ent, sizeof(int32_t) * (P.n_pair_entries > 0 ? P.n_pair_entries : 1))) != cudaSuccess ||
         (e = dev_alloc(&P.d_pair_info, sizeof(int32_t) * 8 * P.n_pairs)) != cudaSuccess ||
         (e = dev_alloc(&P.d_masks, sizeof(uint32_t) * (P.masks.empty() ? 4 : P.masks.size()))) != cudaSuccess ||
         (e = dev_alloc(&P.d_mask_rec, sizeof(uint16_t) * (P.mask_rec.empty() ? 16 : P.mask_rec.size()))) != cudaSuccess ||
         (e = dev_alloc(&P.d_mask_cnt, P.mask_cnt.empty() ? 16 : P.mask_cnt.size())) != cudaSuccess ||
-        (e = dev_alloc(&P.d_kv_mask, sizeof(int32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
-        (e = dev_alloc(&P.d_qt_bits, sizeof(uint32_t) * (P.n_entries > 0 ? P.n_entries : 1))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_kv_mask, sizeof(int32_t) * (P.kv_mask.empty() ? 1 : P.kv_mask.size()))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_qt_bits, sizeof(uint32_t) * (P.qt_bits.empty() ? 1 : P.qt_bits.size()))) != cudaSuccess ||
         (e = dev_alloc(&P.d_t_info, sizeof(int32_t) * 4 * P.n_qt)) != cudaSuccess ||
         (e = dev_alloc(&P.d_sched, kLaunchSlots * 2 * sizeof(unsigned long long))) != cudaSuccess) {
         free_device(a);
@@ -296,8 +297,8 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
         return cuda_fail(e, "plan allocation");
     }
     e = cudaMemcpyAsync(P.d_qt_ptr, P.qt_ptr.data(), sizeof(int32_t) * (P.n_qt + 1), cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess && P.n_entries > 0)
-        e = cudaMemcpyAsync(P.d_kv, P.kv.data(), sizeof(int32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && !P.kv.empty())
+        e = cudaMemcpyAsync(P.d_kv, P.kv.data(), sizeof(int32_t) * P.kv.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_order, P.order.data(), sizeof(int32_t) * P.n_qt, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && P.n_pair_entries > 0)
@@ -310,10 +311,10 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
         e = cudaMemcpyAsync(P.d_mask_rec, P.mask_rec.data(), sizeof(uint16_t) * P.mask_rec.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess && !P.mask_cnt.empty())
         e = cudaMemcpyAsync(P.d_mask_cnt, P.mask_cnt.data(), P.mask_cnt.size(), cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess && P.n_entries > 0)
-        e = cudaMemcpyAsync(P.d_kv_mask, P.kv_mask.data(), sizeof(int32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
-    if (e == cudaSuccess && P.n_entries > 0)
-        e = cudaMemcpyAsync(P.d_qt_bits, P.qt_bits.data(), sizeof(uint32_t) * P.n_entries, cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && !P.kv_mask.empty())
+        e = cudaMemcpyAsync(P.d_kv_mask, P.kv_mask.data(), sizeof(int32_t) * P.kv_mask.size(), cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && !P.qt_bits.empty())
+        e = cudaMemcpyAsync(P.d_qt_bits, P.qt_bits.data(), sizeof(uint32_t) * P.qt_bits.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(P.d_t_info, P.t_info.data(), sizeof(int32_t) * 4 * P.n_qt, cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(P.d_sched, 0, kLaunchSlots * 2 * sizeof(unsigned long long), cs);
@@ -744,6 +745,40 @@ splat_status splat_plan_info(splat_acsr a, int32_t *bm, int32_t *bn, int32_t *n_
     if (bn) *bn = a->plan.bn;
     if (n_qtiles) *n_qtiles = a->plan.n_qt;
     if (n_entries) *n_entries = a->plan.n_entries;
+    return SPLAT_OK;
+}
+
+splat_status splat_plan_split_info(splat_acsr a, int32_t *row_classes, int32_t *n_split_entries)
+{
+    clear_error();
+    if (!a) return set_error(SPLAT_ERR_INVALID_ARG, "null handle");
+    const Plan &P = a->plan;
+    if (row_classes) *row_classes = P.row_classes;
+    if (n_split_entries) *n_split_entries = P.row_classes ? (int32_t)(P.kv.size() - (size_t)P.n_entries) : P.n_entries;
+    return SPLAT_OK;
+}
+
+int64_t splat_plan_sizes(splat_acsr a, int32_t which)
+{
+    if (!a) return -1;
+    const Plan &P = a->plan;
+    switch (which) {
+    case 0: return (int64_t)P.t_info.size() / 4;   // split-kernel units per (b, h)
+    case 1: return (int64_t)P.kv.size();           // all entries (natural, then classed)
+    case 2: return (int64_t)P.n_masks;
+    default: return -1;
+    }
+}
+
+splat_status splat_plan_split_copy(splat_acsr a, int32_t *units, int32_t *kv, int32_t *mask_id, uint32_t *masks)
+{
+    clear_error();
+    if (!a) return set_error(SPLAT_ERR_INVALID_ARG, "null handle");
+    const Plan &P = a->plan;
+    if (units) memcpy(units, P.t_info.data(), sizeof(int32_t) * P.t_info.size());
+    if (kv) memcpy(kv, P.kv.data(), sizeof(int32_t) * P.kv.size());
+    if (mask_id) memcpy(mask_id, P.kv_mask.data(), sizeof(int32_t) * P.kv_mask.size());
+    if (masks) memcpy(masks, P.masks.data(), sizeof(uint32_t) * P.masks.size());
     return SPLAT_OK;
 }
 

@@ -32,6 +32,7 @@ struct DevAcsr {
     // single query tiles (split-group fused kernel)
     const int4 *t_info;         // [n_qt]: (tile, j0, j1, 0), bucketed longest first
     int t_n_buckets;
+    int row_classes;            // t_info tiles are packed 64-row segment pairs (a | b << 16)
     int t_bucket_start[kMaxBuckets + 1];
     unsigned long long *sched;  // [2]: dynamic work counter + done counter of the split kernel
     // the descriptor of a descriptor-built handle (has_pat = 1): kernels may evaluate a row's runs

@@ -87,30 +87,6 @@ void build_plan(splat_acsr_s &a)
         return (P.qt_ptr[x + 1] - P.qt_ptr[x]) > (P.qt_ptr[y + 1] - P.qt_ptr[y]);
     });
 
-    // ---- single query tiles in cost buckets (floor(log2(entries))), longest first: the work
-    // units of the split-group kernel (d = 64), walked head-major inside a bucket.
-    {
-        auto tb = [&](int t) {
-            int len = P.qt_ptr[t + 1] - P.qt_ptr[t], b = 0;
-            while (len > 1) { len >>= 1; ++b; }
-            return b;
-        };
-        std::vector<int> to(P.n_qt);
-        std::iota(to.begin(), to.end(), 0);
-        std::stable_sort(to.begin(), to.end(), [&](int x, int y) { return tb(x) > tb(y); });
-        P.t_bucket_start.clear();
-        for (int i = 0; i < P.n_qt; ++i)
-            if (i == 0 || tb(to[i]) != tb(to[i - 1])) P.t_bucket_start.push_back(i);
-        P.t_bucket_start.push_back(P.n_qt);
-        P.t_n_buckets = (int)P.t_bucket_start.size() - 1;
-        P.t_info.assign((size_t)P.n_qt * 4, 0);
-        for (int k = 0; k < P.n_qt; ++k) {
-            P.t_info[4 * k + 0] = to[k];
-            P.t_info[4 * k + 1] = P.qt_ptr[to[k]];
-            P.t_info[4 * k + 2] = P.qt_ptr[to[k] + 1];
-        }
-    }
-
     // ---- pairs of adjacent query tiles (2p, 2p+1): union of the two sorted key-tile
     // lists, each entry flagged with which tile uses it and whether it is PARTIAL there.
     P.n_pairs = (P.n_qt + 1) / 2;
@@ -231,6 +207,172 @@ void build_plan(splat_acsr_s &a)
         }
     }
     P.n_masks = (int)(P.masks.size() / (128 * 4));
+    P.kv_mask.assign(P.n_entries, -1);
+    for (int e = 0; e < P.n_pair_entries; ++e)
+        for (int g = 0; g < 2; ++g)
+            if (qent_of_pair_ent[g][e] >= 0) P.kv_mask[qent_of_pair_ent[g][e]] = P.pair_mask[(size_t)e * 2 + g];
+
+    // ---- row classes of the split-group kernel (d = 64): a query tile is two 64-row segments.
+    // Rows are grouped by the key blocks they touch (the paper's row classes by segment shape,
+    // alignment P:575-576): segments whose rows touch nearly every key block (global rows) share
+    // tiles, the others keep their natural order, so a band segment is not dragged across every
+    // key window by a global segment (BigBird: the first and last blocks are global rows).  Used
+    // only when it needs fewer plan entries than the natural tiles; the classed entries are
+    // appended after the natural ones (kv / kv_mask / qt_bits), which every other kernel uses.
+    const int nseg = (N + 63) / 64;
+    std::vector<int> seg_a, seg_b;          // per split-kernel tile
+    std::vector<int32_t> tj0, tj1;          // its entry range
+    for (int t = 0; t < P.n_qt; ++t) {      // natural: segments 2t, 2t + 1
+        seg_a.push_back(2 * t);
+        seg_b.push_back(2 * t + 1 < nseg ? 2 * t + 1 : nseg);
+        tj0.push_back(P.qt_ptr[t]);
+        tj1.push_back(P.qt_ptr[t + 1]);
+    }
+    if (ablate == 0 && N <= 65536 && nseg >= 4) {
+        const int W = (nb + 63) / 64;
+        std::vector<uint64_t> foot((size_t)nseg * W, 0ull);
+        std::vector<int> fsz(nseg, 0);
+        for (int sg = 0; sg < nseg; ++sg) {
+            uint64_t *f = &foot[(size_t)sg * W];
+            for (int i = sg * 64; i < std::min(N, sg * 64 + 64); ++i) {
+                const int32_t *rs = &a.seg_h[(size_t)i * 16];
+                for (int q = 0; q < a.nseg_h[i]; ++q) {
+                    const int start = rs[4 * q], step = rs[4 * q + 1], count = rs[4 * q + 2];
+                    const int last = start + step * (count - 1);
+                    if (step < kKvUnit) {
+                        for (int j = start / kKvUnit; j <= last / kKvUnit; ++j) f[j >> 6] |= 1ull << (j & 63);
+                    } else {
+                        for (int x = 0; x < count; ++x) {
+                            const int j = (start + step * x) / kKvUnit;
+                            f[j >> 6] |= 1ull << (j & 63);
+                        }
+                    }
+                }
+            }
+            for (int w = 0; w < W; ++w) fsz[sg] += __builtin_popcountll(f[w]);
+        }
+        std::vector<int> full, rest;
+        for (int sg = 0; sg < nseg; ++sg) (4 * fsz[sg] >= 3 * nb ? full : rest).push_back(sg);
+        if (full.size() >= 2) {
+            std::vector<int> order = full;
+            order.insert(order.end(), rest.begin(), rest.end());
+            std::vector<int> ca, cb;
+            for (size_t k = 0; k < order.size(); k += 2) {
+                ca.push_back(order[k]);
+                cb.push_back(k + 1 < order.size() ? order[k + 1] : nseg);
+            }
+            // windows of a classed tile: greedy cover of its rows' live 64-column blocks
+            std::vector<int32_t> ckv, cj0, cj1;
+            std::vector<uint64_t> u(W);
+            for (size_t t = 0; t < ca.size(); ++t) {
+                cj0.push_back((int32_t)(P.kv.size() + ckv.size()));
+                for (int w = 0; w < W; ++w)
+                    u[w] = foot[(size_t)ca[t] * W + w] | (cb[t] < nseg ? foot[(size_t)cb[t] * W + w] : 0ull);
+                for (int j = 0; j < nb;) {
+                    if (!((u[j >> 6] >> (j & 63)) & 1ull)) { ++j; continue; }
+                    const int kv = j - j % P.kv_align;
+                    ckv.push_back(kv);
+                    j = kv + bn / kKvUnit;
+                }
+                cj1.push_back((int32_t)(P.kv.size() + ckv.size()));
+            }
+            if ((long long)ckv.size() < (long long)P.n_entries) {
+                // adopt: FULL flags, masks, chunk bits of the classed entries (rows in tile order)
+                for (size_t t = 0; t < ca.size(); ++t) {
+                    int rows[128];
+                    for (int r = 0; r < 128; ++r) {
+                        const int sg = r < 64 ? ca[t] : cb[t];
+                        const int i = sg * 64 + (r & 63);
+                        rows[r] = sg < nseg && i < N ? i : -1;
+                    }
+                    for (int e = cj0[t]; e < cj1[t]; ++e) {
+                        const int kv = ckv[e - P.n_entries];
+                        const int c0 = kv * kKvUnit;
+                        std::fill(mbuf.begin(), mbuf.end(), 0u);
+                        bool full_all = c0 + bn <= N;
+                        for (int r = 0; r < 128; ++r) {
+                            const int i = rows[r];
+                            if (i < 0) continue;
+                            const int32_t *rs = &a.seg_h[(size_t)i * 16];
+                            for (int q = 0; q < a.nseg_h[i]; ++q) {
+                                const int start = rs[4 * q], step = rs[4 * q + 1], count = rs[4 * q + 2];
+                                const int last = start + step * (count - 1);
+                                const int lo = std::max(start, c0), hi = std::min(last, c0 + bn - 1);
+                                if (lo > hi) continue;
+                                const int first = start + ((lo - start + step - 1) / step) * step;
+                                for (int c = first; c <= hi; c += step)
+                                    mbuf[4 * r + ((c - c0) >> 5)] |= 1u << ((c - c0) & 31);
+                            }
+                            for (int w = 0; w < 4; ++w) full_all &= mbuf[4 * r + w] == ~0u;
+                        }
+                        for (int r = 0; r < 128; ++r)
+                            if (rows[r] < 0) full_all = false;
+                        int32_t id = -1;
+                        uint32_t bits = 0xFFFFFFFFu;
+                        if (!full_all) {
+                            uint64_t h = 1469598103934665603ull;
+                            for (uint32_t x : mbuf) h = (h ^ x) * 1099511628211ull;
+                            auto &cand = seen[h];
+                            for (int32_t c : cand)
+                                if (std::equal(mbuf.begin(), mbuf.end(), P.masks.begin() + (size_t)c * 128 * 4)) { id = c; break; }
+                            if (id < 0) {
+                                id = (int32_t)(P.masks.size() / (128 * 4));
+                                P.masks.insert(P.masks.end(), mbuf.begin(), mbuf.end());
+                                cand.push_back(id);
+                            }
+                            bits = 0;
+                            for (int q = 0; q < 4; ++q)
+                                for (int w = 0; w < 4; ++w) {
+                                    bool any = false, all = true;
+                                    for (int r = 32 * q; r < 32 * q + 32; ++r) {
+                                        any |= mbuf[4 * r + w] != 0u;
+                                        all &= mbuf[4 * r + w] == ~0u;
+                                    }
+                                    if (any) bits |= 1u << (4 * q + w);
+                                    if (all) bits |= 1u << (16 + 4 * q + w);
+                                }
+                        }
+                        P.kv.push_back(kv | (full_all ? 0 : kPartialBit));
+                        P.kv_mask.push_back(id);
+                        P.qt_bits.push_back(bits);
+                    }
+                }
+                seg_a = ca;
+                seg_b = cb;
+                tj0 = cj0;
+                tj1 = cj1;
+                P.row_classes = 1;
+            }
+        }
+    }
+    P.n_masks = (int)(P.masks.size() / (128 * 4));
+
+    // ---- split-kernel work units: its tiles in cost buckets (floor(log2(entries))), longest
+    // first, walked head-major inside a bucket; (tile or segments a | b << 16, j0, j1, 0)
+    {
+        const int nt = (int)seg_a.size();
+        auto tb = [&](int t) {
+            int len = tj1[t] - tj0[t], b = 0;
+            while (len > 1) { len >>= 1; ++b; }
+            return b;
+        };
+        std::vector<int> to(nt);
+        std::iota(to.begin(), to.end(), 0);
+        std::stable_sort(to.begin(), to.end(), [&](int x, int y) { return tb(x) > tb(y); });
+        P.t_bucket_start.clear();
+        for (int i = 0; i < nt; ++i)
+            if (i == 0 || tb(to[i]) != tb(to[i - 1])) P.t_bucket_start.push_back(i);
+        P.t_bucket_start.push_back(nt);
+        P.t_n_buckets = (int)P.t_bucket_start.size() - 1;
+        P.t_info.assign((size_t)nt * 4, 0);
+        for (int k = 0; k < nt; ++k) {
+            // natural tiles: the tile index (segments 2t, 2t + 1); classed (N <= 65536): packed segments
+            P.t_info[4 * k + 0] = P.row_classes ? (seg_a[to[k]] | (seg_b[to[k]] << 16)) : to[k];
+            P.t_info[4 * k + 1] = tj0[to[k]];
+            P.t_info[4 * k + 2] = tj1[to[k]];
+        }
+        P.n_split_tiles = nt;
+    }
     // R-SpMM row records of every PARTIAL mask: per row and 8-column group g the live columns left
     // of the group (low byte) and the group's 8 mask bits (high byte), and per row the live count
     P.mask_rec.assign((size_t)P.n_masks * 128 * 16, 0);
@@ -246,10 +388,6 @@ void build_plan(splat_acsr_s &a)
             }
             P.mask_cnt[(size_t)m * 128 + r] = (uint8_t)(pre > 255 ? 255 : pre);   // <= 128
         }
-    P.kv_mask.assign(P.n_entries, -1);
-    for (int e = 0; e < P.n_pair_entries; ++e)
-        for (int g = 0; g < 2; ++g)
-            if (qent_of_pair_ent[g][e] >= 0) P.kv_mask[qent_of_pair_ent[g][e]] = P.pair_mask[(size_t)e * 2 + g];
 }
 
 }  // namespace splat

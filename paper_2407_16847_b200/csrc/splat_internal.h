@@ -171,6 +171,8 @@ constexpr int kMaxBuckets = 24;
 struct Plan {
     int bm = kBM, bn = kBN, n_qt = 0, n_entries = 0, n_kt = 0;
     int kv_align = 1;                     // window starts: multiples of kv_align * 64 columns
+    int row_classes = 0;                  // split-kernel tiles regrouped by row class (plan.cpp)
+    int n_split_tiles = 0;                // split-kernel work units per (b, h)
     std::vector<int32_t> qt_ptr, kv, order;          // per query tile (ABI: splat_plan_copy)
     // query-tile pairs
     int n_pairs = 0, n_pair_entries = 0, n_buckets = 0, n_masks = 0;

@@ -915,8 +915,11 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             if (lane == 0) hdr[qi] = make_int4(un.t, un.bh, un.j0, un.j1);
             // header + table: each lane's arrival releases its own writes; lane 0's carries the Q bytes
             if (lane == 0) {
+                // the tile's two 64-row segments (row classes, plan.cpp): rows 0-63 and 64-127
                 mbar_expect_tx(&q_full[qi], C::TB);
-                tma_load_3d(gs + C::OFF_Q + qi * C::TB, &tmQ, &q_full[qi], 0, un.t * 128, un.bh);
+                const int sa = A.row_classes ? (un.t & 0xFFFF) : 2 * un.t, sb = A.row_classes ? (un.t >> 16) : 2 * un.t + 1;
+                tma_load_3d(gs + C::OFF_Q + qi * C::TB, &tmQ, &q_full[qi], 0, sa * 64, un.bh);
+                tma_load_3d(gs + C::OFF_Q + qi * C::TB + C::TB / 2, &tmQ, &q_full[qi], 0, sb * 64, un.bh);
             } else {
                 mbar_arrive(&q_full[qi]);
             }
@@ -1078,7 +1081,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             fence_proxy_async_smem();
             named_bar(1 + g, 128);
             if (store_leader) {
-                tma_store_3d(&tmO, ostage, 0, t * 128, bh);
+                const int sa = A.row_classes ? (t & 0xFFFF) : 2 * t, sb = A.row_classes ? (t >> 16) : 2 * t + 1;
+                tma_store_3d(&tmO, ostage, 0, sa * 64, bh);
+                tma_store_3d(&tmO, ostage + C::TB / 2, 0, sb * 64, bh);
                 bulk_commit();
             }
             tc_fence_before();
@@ -1314,8 +1319,9 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
                            void *O, cudaStream_t st)
 {
     CUtensorMap mq, mk, mv, mo;
-    if (!make_map(&mq, Q, BH, A.n, 64) || !make_map(&mk, K, BH, A.n, 64) || !make_map(&mv, V, BH, A.n, 64) ||
-        !make_map(&mo, O, BH, A.n, 64))
+    // Q and O move as two 64-row segments per tile (row classes), K and V as 128-row key windows
+    if (!make_map(&mq, Q, BH, A.n, 64, 64) || !make_map(&mk, K, BH, A.n, 64) || !make_map(&mv, V, BH, A.n, 64) ||
+        !make_map(&mo, O, BH, A.n, 64, 64))
         return cudaErrorInvalidValue;
     static bool attr_set[64] = {false};
     int dev = 0;

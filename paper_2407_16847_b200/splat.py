@@ -27,7 +27,7 @@ KINDS = {"window": 0, "blocked": 1, "strided": 2, "dilated": 3, "global_local": 
 
 # every symbol include/splat.h declares (tests check the library exports them all)
 EXPORTS = ("splat_acsr_build", "splat_acsr_info", "splat_acsr_copy_meta", "splat_plan_info",
-           "splat_plan_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
+           "splat_plan_copy", "splat_plan_split_info", "splat_plan_sizes", "splat_plan_split_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
            "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_acsr_from_mask", "splat_poset_tile", "splat_naive_tile",
            "splat_tiling_cost_eval", "splat_acsr_transpose", "splat_transpose_values", "splat_rspmm_cc",
            "splat_layout_choice", "splat_flops", "splat_last_launch_count", "splat_device_alloc_count",
@@ -75,6 +75,10 @@ def lib():
         L.splat_acsr_copy_meta.argtypes = [vp, vp, vp, vp]
         L.splat_plan_info.argtypes = [vp, P(i32), P(i32), P(i32), P(i32)]
         L.splat_plan_copy.argtypes = [vp, vp, vp, vp]
+        L.splat_plan_split_info.argtypes = [vp, P(i32), P(i32)]
+        L.splat_plan_sizes.argtypes = [vp, i32]
+        L.splat_plan_sizes.restype = i64
+        L.splat_plan_split_copy.argtypes = [vp, vp, vp, vp, vp]
         L.splat_acsr_destroy.argtypes = [vp]
         L.splat_rsddmm.argtypes = [vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp]
         L.splat_sparse_softmax.argtypes = [vp, vp, vp, C.c_int, i32, i32, vp]
@@ -96,7 +100,8 @@ def lib():
         L.splat_last_launch_count.restype = i32
         L.splat_last_error.restype = C.c_char_p
         for name in EXPORTS:
-            if name not in ("splat_flops", "splat_last_error", "splat_last_launch_count", "splat_layout_choice"):
+            if name not in ("splat_flops", "splat_last_error", "splat_last_launch_count", "splat_layout_choice",
+                            "splat_plan_sizes"):
                 getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -156,6 +161,23 @@ class Acsr:
         bm, bn, nq, ne = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
         _check(lib().splat_plan_info(self.handle, C.byref(bm), C.byref(bn), C.byref(nq), C.byref(ne)))
         return bm.value, bn.value, nq.value, ne.value
+
+    def split_info(self):
+        """(row_classes, entries per (b, h)) of the d = 64 split-group kernel's plan."""
+        rc, ne = C.c_int32(), C.c_int32()
+        _check(lib().splat_plan_split_info(self.handle, C.byref(rc), C.byref(ne)))
+        return rc.value, ne.value
+
+    def split_plan_copy(self):
+        """The split kernel's units, entries (kv, mask ids) and masks as CPU tensors."""
+        L = lib()
+        nu, ne, nm = (L.splat_plan_sizes(self.handle, w) for w in (0, 1, 2))
+        units = torch.zeros((nu, 4), dtype=torch.int32)
+        kv = torch.zeros(max(ne, 1), dtype=torch.int32)
+        mid = torch.zeros(max(ne, 1), dtype=torch.int32)
+        masks = torch.zeros((max(nm, 1), 128, 4), dtype=torch.int64).to(torch.int32)
+        _check(L.splat_plan_split_copy(self.handle, units.data_ptr(), kv.data_ptr(), mid.data_ptr(), masks.data_ptr()))
+        return units, kv[:ne], mid[:ne], masks[:nm]
 
     def plan_copy(self):
         _, _, nq, ne = self.plan_info()

@@ -213,3 +213,41 @@ def test_product_library_has_no_debug_exports():
     for name in ("splat_debug_trace", "splat_debug_fused_prof", "splat_debug_hang", "splat_debug_prof64",
                  "splat_debug_unf_prof"):
         assert name not in exported, name
+
+
+def split_plan_coverage(p):
+    """Times each (row, column) is covered by the split kernel's plan (its units' two 64-row
+    segments x key windows x row masks) -- must equal the oracle's explicit mask."""
+    a = S.Acsr(p, device=-1)
+    rc, ne = a.split_info()
+    units, kv, mid, masks = a.split_plan_copy()
+    N = p.seq_len
+    nseg = (N + 63) // 64
+    cover = np.zeros((N, N), dtype=np.int32)
+    masks = masks.numpy().astype(np.int64) & 0xFFFFFFFF
+    for t, j0, j1, _ in units.tolist():
+        sa, sb = (t & 0xFFFF, t >> 16) if rc else (2 * t, 2 * t + 1)
+        rows = np.array([s * 64 + r if s < nseg and s * 64 + r < N else -1 for s in (sa, sb) for r in range(64)])
+        ok = rows >= 0
+        for e in range(j0, j1):
+            c0 = (int(kv[e]) & 0xFFFFFF) * 64
+            cols = np.arange(c0, min(N, c0 + 128))
+            if (int(kv[e]) >> 24) & 1:
+                w = masks[int(mid[e])]                                   # [128, 4]
+                bits = (w[:, (cols - c0) >> 5] >> ((cols - c0) & 31)) & 1
+            else:
+                bits = np.ones((128, len(cols)), dtype=np.int64)
+            cover[np.ix_(rows[ok], cols)] += bits[ok].astype(np.int32)
+    return cover, rc, ne
+
+
+@pytest.mark.parametrize("p", [Pattern("bigbird", 4096, block=64, radius=1), Pattern("bigbird", 1000, block=64, radius=1),
+                               Pattern("bigbird", 520, block=32, radius=1),
+                               Pattern("global_local", 1000, lo=128, hi=128, n_global=32),
+                               Pattern("window", 700, lo=64, hi=64), Pattern("strided_local", 1100, stride=128, causal=1),
+                               Pattern("strided", 600, stride=7)], ids=lambda p: f"{p.kind}{p.seq_len}")
+def test_split_plan_covers_mask_exactly_once(p):
+    cover, rc, ne = split_plan_coverage(p)
+    assert np.array_equal(cover, O.mask(p).astype(np.int32)), p
+    if p.kind == "bigbird" and p.seq_len == 4096:
+        assert rc == 1 and ne == 154          # row classes: the two global blocks share a tile
