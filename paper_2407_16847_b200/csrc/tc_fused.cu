@@ -583,6 +583,17 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 continue;
             }
             const int bh = un.bh;
+            if (!VIEW && prm.merge) {
+                // the merging epilogue of this tile (deferred past the next unit's first tile) reads
+                // this row's strided-pass O_s and lse: pull them into L2 now
+                const int nat = t * 128 + r;
+                if (nat < prm.N) {
+                    const char *orow = reinterpret_cast<const char *>(prm.O + ((size_t)bh * prm.N + nat) * D);
+#pragma unroll
+                    for (int b = 0; b < D * 2; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(orow + b));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(prm.lse + (size_t)bh * prm.N + nat));
+                }
+            }
             float m_run = -INFINITY, l_run = 0.f;
             bool first = true;
             if (j0 == j1) SPLAT_NEXT_UNIT_PREFETCH();
