@@ -128,7 +128,11 @@ softmax_short_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P,
 // stores only the non-zeros; reading R-1).  Warp per row, three streaming passes over the row --
 // max, sum of exp, write -- with 16-byte loads of S on the aligned body of the row (the second and
 // third reads hit L2); exp(x - m) = 2^((x - m) log2 e) on MUFU.EX2.
-template <typename TP>
+//
+// RC > 0: rows of at most 128 RC elements are held in registers (RC float4 per lane, all loads
+// issued at once, streaming / evict-first: S is read exactly once) and take one exponential per
+// element; longer rows take the three passes.
+template <typename TP, int RC>
 __global__ void __launch_bounds__(kWarps * 32)
 softmax_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P)
 {
@@ -147,6 +151,49 @@ softmax_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P)
     const float4 *s4 = reinterpret_cast<const float4 *>(s + head);
     constexpr float L2E = 1.4426950408889634f;
     float m = -INFINITY, l = 0.f;
+    if (RC > 0 && len <= 128 * RC) {
+        constexpr int R = RC > 0 ? RC : 1;
+        float4 v[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int q = lane + 32 * k;
+            v[k] = q < nv ? __ldcs(s4 + q) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        }
+        // head (< 4 elements before the first 16-byte boundary) and tail (< 4 after the last)
+        const int xt = tail0 + lane;
+        float hv = lane < head ? __ldcs(s + lane) : -INFINITY;
+        float tv = xt < len ? __ldcs(s + xt) : -INFINITY;
+        m = fmaxf(hv, tv);
+#pragma unroll
+        for (int k = 0; k < R; ++k) m = fmaxf(m, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const float mL = m * L2E;
+        // masked-out slots hold -inf: 2^(-inf) = 0 adds nothing
+        hv = ex2f(fmaf(hv, L2E, -mL));
+        tv = ex2f(fmaf(tv, L2E, -mL));
+        l = hv + tv;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            v[k].x = ex2f(fmaf(v[k].x, L2E, -mL));
+            v[k].y = ex2f(fmaf(v[k].y, L2E, -mL));
+            v[k].z = ex2f(fmaf(v[k].z, L2E, -mL));
+            v[k].w = ex2f(fmaf(v[k].w, L2E, -mL));
+            l += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+        const float inv = 1.f / l;
+        if (lane < head) p[lane] = from_f<TP>(hv * inv);
+        if (xt < len) p[xt] = from_f<TP>(tv * inv);
+        TP *p4 = p + head;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int q = lane + 32 * k;
+            if (q < nv) store4(p4 + 4 * q, v[k].x * inv, v[k].y * inv, v[k].z * inv, v[k].w * inv);
+        }
+        return;
+    }
     if (len > 2048) {
         // long rows (their re-reads would miss L2): one online pass for max and sum
         // (the sum is rescaled when the running max grows), then the write pass
@@ -540,10 +587,20 @@ cudaError_t launch_softmax(const DevAcsr &A, const float *S, void *P, bool p_bf1
             softmax_short_kernel<float, 16><<<grid, kWarps * 32, 0, st>>>(A, S, (float *)P, BH);
         return cudaGetLastError();
     }
-    if (p_bf16)
-        softmax_kernel<__nv_bfloat16><<<grid_rows(A, BH), kWarps * 32, 0, st>>>(A, S, (__nv_bfloat16 *)P);
-    else
-        softmax_kernel<float><<<grid_rows(A, BH), kWarps * 32, 0, st>>>(A, S, (float *)P);
+    // register capacity by the mean row length: Longformer / BigBird rows (~440-560) fit 8 float4
+    // per lane, a 4096-key window 32; the rare longer rows (global rows) take the three passes
+    const int knob = diag_env("SPLAT_SOFTMAX_RC");      // diagnostics build: 1 = three passes only
+    const int rc = knob == 1 ? 0 : A.nnz <= 640ll * A.n ? 8 : A.nnz <= 4096ll * A.n ? 32 : 0;
+    const dim3 grid = grid_rows(A, BH);
+#define SPLAT_SOFTMAX_LAUNCH(RC)                                                                         \
+    do {                                                                                               \
+        if (p_bf16) softmax_kernel<__nv_bfloat16, RC><<<grid, kWarps * 32, 0, st>>>(A, S, (__nv_bfloat16 *)P); \
+        else softmax_kernel<float, RC><<<grid, kWarps * 32, 0, st>>>(A, S, (float *)P);                \
+    } while (0)
+    if (rc == 8) SPLAT_SOFTMAX_LAUNCH(8);
+    else if (rc == 32) SPLAT_SOFTMAX_LAUNCH(32);
+    else SPLAT_SOFTMAX_LAUNCH(0);
+#undef SPLAT_SOFTMAX_LAUNCH
     return cudaGetLastError();
 }
 
