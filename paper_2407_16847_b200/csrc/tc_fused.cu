@@ -1153,8 +1153,11 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 if (j + 1 < j1) pf = mask_for(entry(slot, j0, j + 1));
                 else SPLAT_NEXT_UNIT_PREFETCH();
                 const uint32_t mk[4] = {m4.x, m4.y, m4.z, m4.w};
-                uint32_t live = (bits >> (4 * quad)) & 0xFu;
-                const uint32_t need = live & ~(bits >> (16 + 4 * quad));
+                // chunk bits of this warp, broadcast so the per-chunk branches are provably uniform
+                const uint32_t live4 = (bits >> (4 * quad)) & 0xFu, need4 = live4 & ~(bits >> (16 + 4 * quad));
+                const uint32_t wbits = __shfl_sync(0xffffffffu, live4 | (need4 << 4), 0);
+                uint32_t live = wbits & 0xFu;
+                const uint32_t need = (wbits >> 4) & 0xFu;
                 FWAIT(0, s_full, s_cnt & 1);
                 ++s_cnt;
                 tc_fence_after();
