@@ -113,6 +113,37 @@ softmax_short_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P,
     const float *s = S + e0;
     TP *p = P + e0;
     float m = -INFINITY, l = 0.f;
+    // rows of at most 16 LPR elements (every row of the group, a warp-uniform test): held in
+    // registers, S read once (streaming), one exponential per element
+    constexpr int CAP = 16;
+    const bool fits = __all_sync(0xffffffffu, len <= CAP * LPR);
+    if (fits) {
+        float v[CAP];
+#pragma unroll
+        for (int k = 0; k < CAP; ++k) {
+            const int x = sl + LPR * k;
+            v[k] = x < len ? __ldcs(s + x) : -INFINITY;
+        }
+#pragma unroll
+        for (int k = 0; k < CAP; ++k) m = fmaxf(m, v[k]);
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const float mL = m * L2E;
+#pragma unroll
+        for (int k = 0; k < CAP; ++k) {
+            v[k] = sl + LPR * k < len ? ex2f(fmaf(v[k], L2E, -mL)) : 0.f;
+            l += v[k];
+        }
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+        const float inv = 1.f / l;
+#pragma unroll
+        for (int k = 0; k < CAP; ++k) {
+            const int x = sl + LPR * k;
+            if (x < len) p[x] = from_f<TP>(v[k] * inv);
+        }
+        return;
+    }
     for (int x = sl; x < len; x += LPR) m = fmaxf(m, s[x]);
 #pragma unroll
     for (int o = LPR / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -164,8 +195,10 @@ softmax_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P)
         float hv = lane < head ? __ldcs(s + lane) : -INFINITY;
         float tv = xt < len ? __ldcs(s + xt) : -INFINITY;
         m = fmaxf(hv, tv);
+        const int kmax = (nv + 31) >> 5;                   // float4 groups holding row data (warp-uniform)
 #pragma unroll
-        for (int k = 0; k < R; ++k) m = fmaxf(m, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
+        for (int k = 0; k < R; ++k)
+            if (k < kmax) m = fmaxf(m, fmaxf(fmaxf(v[k].x, v[k].y), fmaxf(v[k].z, v[k].w)));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         const float mL = m * L2E;
@@ -175,11 +208,13 @@ softmax_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P)
         l = hv + tv;
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-            v[k].x = ex2f(fmaf(v[k].x, L2E, -mL));
-            v[k].y = ex2f(fmaf(v[k].y, L2E, -mL));
-            v[k].z = ex2f(fmaf(v[k].z, L2E, -mL));
-            v[k].w = ex2f(fmaf(v[k].w, L2E, -mL));
-            l += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+            if (k < kmax) {                                 // no exponentials of the padding groups
+                v[k].x = ex2f(fmaf(v[k].x, L2E, -mL));
+                v[k].y = ex2f(fmaf(v[k].y, L2E, -mL));
+                v[k].z = ex2f(fmaf(v[k].z, L2E, -mL));
+                v[k].w = ex2f(fmaf(v[k].w, L2E, -mL));
+                l += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
