@@ -130,6 +130,12 @@ void free_device(splat_acsr_s *a)
     a->sub_band = a->sub_str = a->sub_perm = nullptr;
     cudaFree(a->d_lse);
     a->d_lse = nullptr;
+    for (void *q : {(void *)a->d_mix_ent, (void *)a->d_mix_info, (void *)a->d_mix_kv_mask, (void *)a->d_mix_masks,
+                    (void *)a->d_mix_qt_bits, (void *)a->d_dep})
+        cudaFree(q);
+    a->d_mix_ent = a->d_mix_info = a->d_mix_kv_mask = nullptr;
+    a->d_mix_masks = a->d_mix_qt_bits = nullptr;
+    a->d_dep = nullptr;
     for (int i = 0; i < kLaunchSlots; ++i)
         if (a->slots[i].ev) cudaEventDestroy((cudaEvent_t)a->slots[i].ev);
     for (int i = 0; i < 3; ++i)
@@ -226,6 +232,29 @@ bool use_residue_split(const splat_acsr_s *a)
 {
     static const bool off = diag_env("SPLAT_NO_RESIDUE_SPLIT") != 0;
     return a->sub_band != nullptr && !off;
+}
+
+// One launch for the residue decomposition: an experiment, selected only in the diagnostics build
+// (SPLAT_RESIDUE_1PASS=1).  It cuts the DRAM traffic of the Sparse-Transformer step from 1.16 GB to
+// 0.70 GB but runs ~40 % slower than the two launches: the product keeps two.
+bool use_residue1(const splat_acsr_s *a)
+{
+    static const bool on = diag_env("SPLAT_RESIDUE_1PASS") != 0;
+    return a->d_dep != nullptr && on;
+}
+
+// Device view of the merged plan of the one-launch residue decomposition
+DevAcsr mix_view(const splat_acsr_s *a)
+{
+    DevAcsr A = dev_view(a->sub_str);
+    A.pair_ent = a->d_mix_ent;
+    A.pair_info = reinterpret_cast<const int4 *>(a->d_mix_info);
+    A.kv_mask = a->d_mix_kv_mask;
+    A.masks = reinterpret_cast<const uint4 *>(a->d_mix_masks);
+    A.qt_bits = a->d_mix_qt_bits;
+    A.n_pairs = a->mix_u1 + a->mix_u2;
+    A.n_buckets = 0;
+    return A;
 }
 
 bool use_perm()
@@ -440,6 +469,68 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
     return finish_device_build(a, cs, out);
 }
 
+// Merged plan of the one-launch residue decomposition: the strided pass's pairs, then the band
+// pass's, with the band part's entry (pair_ent), entry-table (kv_mask / qt_bits) and mask indices
+// offset past the strided part's; plus zeroed dependency counters per launch slot.  Optional: on
+// any failure the two-launch form is used.
+void build_residue_merged(splat_acsr_s *a, cudaStream_t cs)
+{
+    const Plan &P1 = a->sub_str->plan, &P2 = a->sub_band->plan;
+    if (P1.n_qt != P2.n_qt || P1.n_pairs <= 0 || P2.n_pairs <= 0) return;
+    std::vector<int32_t> ent, info, kvm;
+    std::vector<uint32_t> masks, bits;
+    try {
+        ent.assign(P1.pair_ent.begin(), P1.pair_ent.begin() + P1.n_pair_entries);
+        ent.insert(ent.end(), P2.pair_ent.begin(), P2.pair_ent.begin() + P2.n_pair_entries);
+        info.assign(P1.pair_info.begin(), P1.pair_info.begin() + 8 * (size_t)P1.n_pairs);
+        const int n_ent1 = (int)P1.kv_mask.size();
+        for (int k = 0; k < P2.n_pairs; ++k) {
+            const int32_t *x = &P2.pair_info[8 * (size_t)k];
+            // pair, e0, e1, jA0, jA1, jB1, 0, 0
+            info.insert(info.end(), {x[0], x[1] + P1.n_pair_entries, x[2] + P1.n_pair_entries, x[3] + n_ent1,
+                                     x[4] + n_ent1, x[5] + n_ent1, x[6], x[7]});
+        }
+        kvm = P1.kv_mask;
+        for (int32_t m : P2.kv_mask) kvm.push_back(m >= 0 ? m + P1.n_masks : m);
+        bits = P1.qt_bits;
+        bits.insert(bits.end(), P2.qt_bits.begin(), P2.qt_bits.end());
+        masks.assign(P1.masks.begin(), P1.masks.begin() + (size_t)P1.n_masks * 128 * 4);
+        masks.insert(masks.end(), P2.masks.begin(), P2.masks.begin() + (size_t)P2.n_masks * 128 * 4);
+    } catch (const std::bad_alloc &) {
+        return;
+    }
+    if (masks.empty()) masks.assign(4, 0u);
+    const size_t n_dep = (size_t)kLaunchSlots * (kLseHeads + 1);
+    cudaError_t e = cudaSuccess;
+    if ((e = dev_alloc(&a->d_mix_ent, sizeof(int32_t) * ent.size())) != cudaSuccess ||
+        (e = dev_alloc(&a->d_mix_info, sizeof(int32_t) * info.size())) != cudaSuccess ||
+        (e = dev_alloc(&a->d_mix_kv_mask, sizeof(int32_t) * kvm.size())) != cudaSuccess ||
+        (e = dev_alloc(&a->d_mix_qt_bits, sizeof(uint32_t) * bits.size())) != cudaSuccess ||
+        (e = dev_alloc(&a->d_mix_masks, sizeof(uint32_t) * masks.size())) != cudaSuccess ||
+        (e = dev_alloc(&a->d_dep, sizeof(unsigned) * n_dep)) != cudaSuccess) {
+    } else if ((e = cudaMemcpyAsync(a->d_mix_ent, ent.data(), sizeof(int32_t) * ent.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+               (e = cudaMemcpyAsync(a->d_mix_info, info.data(), sizeof(int32_t) * info.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+               (e = cudaMemcpyAsync(a->d_mix_kv_mask, kvm.data(), sizeof(int32_t) * kvm.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+               (e = cudaMemcpyAsync(a->d_mix_qt_bits, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+               (e = cudaMemcpyAsync(a->d_mix_masks, masks.data(), sizeof(uint32_t) * masks.size(), cudaMemcpyHostToDevice, cs)) != cudaSuccess ||
+               (e = cudaMemsetAsync(a->d_dep, 0, sizeof(unsigned) * n_dep, cs)) != cudaSuccess) {
+    } else {
+        e = cudaStreamSynchronize(cs);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        for (void *q : {(void *)a->d_mix_ent, (void *)a->d_mix_info, (void *)a->d_mix_kv_mask, (void *)a->d_mix_masks,
+                        (void *)a->d_mix_qt_bits, (void *)a->d_dep})
+            cudaFree(q);
+        a->d_mix_ent = a->d_mix_info = a->d_mix_kv_mask = nullptr;
+        a->d_mix_masks = a->d_mix_qt_bits = nullptr;
+        a->d_dep = nullptr;
+        return;
+    }
+    a->mix_u1 = P1.n_pairs;
+    a->mix_u2 = P2.n_pairs;
+}
+
 // Residue decomposition of STRIDED_LOCAL(l) (see splat_acsr_s::sub_band): applicable when the
 // residue classes tile the sequence exactly (N % l == 0) and whole classes fill a 128-row tile
 // (nk = N / l divides 128, nk >= 2).
@@ -499,6 +590,7 @@ void build_residue_split(splat_acsr_s *a, void *stream)
     a->rv_l = l;
     a->rv_nk = nk;
     a->rv_R = 128 / nk;
+    build_residue_merged(a, (cudaStream_t)stream);
 }
 
 // Launch slots and the host pipeline's streams / events of a top-level device handle (build time,
@@ -580,9 +672,15 @@ cudaError_t launch_mhsa(splat_acsr a, const void *Q, const void *K, const void *
             const int nh = BH - h0 < kLseHeads ? BH - h0 : kLseHeads;
             const size_t off = slice * h0;
             int n1 = 0;
-            e = launch_mhsa_tc_residue(dev_view(a->sub_band), dev_view(a->sub_str), a->rv_l, a->rv_nk, a->rv_R, lse,
-                                       (const char *)Q + off, (const char *)K + off, (const char *)V + off, nh, d,
-                                       scale, (char *)O + off, s, &n1);
+            if (use_residue1(a))
+                e = launch_mhsa_tc_residue1(mix_view(a), a->mix_u1, a->mix_u2, a->rv_l, a->rv_nk, a->rv_R, lse,
+                                            a->d_dep + (size_t)su.index * (kLseHeads + 1), (const char *)Q + off,
+                                            (const char *)K + off, (const char *)V + off, nh, d, scale,
+                                            (char *)O + off, s, &n1);
+            else
+                e = launch_mhsa_tc_residue(dev_view(a->sub_band), dev_view(a->sub_str), a->rv_l, a->rv_nk, a->rv_R,
+                                           lse, (const char *)Q + off, (const char *)K + off, (const char *)V + off,
+                                           nh, d, scale, (char *)O + off, s, &n1);
             nl += n1;
         }
     } else if (dt == SPLAT_BF16 && a->sub_perm && use_perm())

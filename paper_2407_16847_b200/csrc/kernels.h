@@ -87,6 +87,12 @@ cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const
 cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int l, int nk, int R, float *lse,
                                    const void *Q, const void *K, const void *V, int BH, int d, float scale, void *O,
                                    cudaStream_t st, int *n_launch);
+// The same decomposition in ONE launch: `mix` is the merged plan (strided-pass pairs [0, u1), band-pass
+// pairs [u1, u1 + u2)); units run head-interleaved and a band unit's merging epilogue waits on the
+// head's counter in `dep` ([kLseHeads + 1], zero between launches; reset by the last CTA).
+cudaError_t launch_mhsa_tc_residue1(const DevAcsr &mix, int u1, int u2, int l, int nk, int R, float *lse, unsigned *dep,
+                                    const void *Q, const void *K, const void *V, int BH, int d, float scale, void *O,
+                                    cudaStream_t st, int *n_launch);
 // Unfused R-SDDMM (sddmm = true: X = Q, Y = K, out = S) or R-SpMM (X = P, Y = V, out = O) over the
 // residue decomposition: pass 1 on the strided sub-pattern (residue-major views), pass 2 on the band.
 cudaError_t launch_unfused_residue(bool sddmm, const DevAcsr &band, const DevAcsr &str, const DevAcsr &nat, int l,

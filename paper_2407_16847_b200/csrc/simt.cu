@@ -155,6 +155,73 @@ softmax_short_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P,
     for (int x = sl; x < len; x += LPR) p[x] = from_f<TP>(ex2f(fmaf(s[x], L2E, -mL)) * inv);
 }
 
+// Three streaming passes over one ACSR row (max, sum of exp, write) by one warp; rows over 2048
+// elements fold max and sum into one online pass.
+template <typename TP>
+__device__ __forceinline__ void softmax_row_passes(const float *__restrict__ s, TP *__restrict__ p, int len, int head,
+                                                   int nv, int tail0, int lane)
+{
+    constexpr float L2E = 1.4426950408889634f;
+    const float4 *s4 = reinterpret_cast<const float4 *>(s + head);
+    float m = -INFINITY, l = 0.f;
+    if (len > 2048) {
+        // long rows (their re-reads would miss L2): one online pass for max and sum
+        // (the sum is rescaled when the running max grows), then the write pass
+        auto add = [&](float vmax, float s0) {   // s0 = sum of 2^((v - vmax) log2 e) of the group
+            const float mn = fmaxf(m, vmax);
+            l = l * ex2f((m - mn) * L2E) + s0 * ex2f((vmax - mn) * L2E);
+            m = mn;
+        };
+        if (lane < head) add(s[lane], 1.f);
+#pragma unroll 4
+        for (int q = lane; q < nv; q += 32) {
+            const float4 v = s4[q];
+            const float vm = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)), vmL = vm * L2E;
+            add(vm, (ex2f(fmaf(v.x, L2E, -vmL)) + ex2f(fmaf(v.y, L2E, -vmL))) +
+                        (ex2f(fmaf(v.z, L2E, -vmL)) + ex2f(fmaf(v.w, L2E, -vmL))));
+        }
+        for (int x = tail0 + lane; x < len; x += 32) add(s[x], 1.f);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, m, o), l2 = __shfl_xor_sync(0xffffffffu, l, o);
+            const float mn = fmaxf(m, m2);
+            l = (m == -INFINITY ? 0.f : l * ex2f((m - mn) * L2E)) + (m2 == -INFINITY ? 0.f : l2 * ex2f((m2 - mn) * L2E));
+            m = mn;
+        }
+    } else {
+        if (lane < head) m = s[lane];
+#pragma unroll 4
+        for (int q = lane; q < nv; q += 32) {
+            const float4 v = s4[q];
+            m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+        }
+        for (int x = tail0 + lane; x < len; x += 32) m = fmaxf(m, s[x]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const float mL0 = m * L2E;
+        if (lane < head) l = ex2f(fmaf(s[lane], L2E, -mL0));
+#pragma unroll 4
+        for (int q = lane; q < nv; q += 32) {
+            const float4 v = s4[q];
+            l += (ex2f(fmaf(v.x, L2E, -mL0)) + ex2f(fmaf(v.y, L2E, -mL0))) + (ex2f(fmaf(v.z, L2E, -mL0)) + ex2f(fmaf(v.w, L2E, -mL0)));
+        }
+        for (int x = tail0 + lane; x < len; x += 32) l += ex2f(fmaf(s[x], L2E, -mL0));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    }
+    const float mL = m * L2E;
+    const float inv = 1.f / l;
+    if (lane < head) p[lane] = from_f<TP>(ex2f(fmaf(s[lane], L2E, -mL)) * inv);
+    TP *p4 = p + head;
+#pragma unroll 4
+    for (int q = lane; q < nv; q += 32) {
+        const float4 v = s4[q];
+        store4(p4 + 4 * q, ex2f(fmaf(v.x, L2E, -mL)) * inv, ex2f(fmaf(v.y, L2E, -mL)) * inv,
+               ex2f(fmaf(v.z, L2E, -mL)) * inv, ex2f(fmaf(v.w, L2E, -mL)) * inv);
+    }
+    for (int x = tail0 + lane; x < len; x += 32) p[x] = from_f<TP>(ex2f(fmaf(s[x], L2E, -mL)) * inv);
+}
+
 // Row softmax over the ACSR row (the softmax of each input row of the ACSR, which
 // stores only the non-zeros; reading R-1).  Warp per row, three streaming passes over the row --
 // max, sum of exp, write -- with 16-byte loads of S on the aligned body of the row (the second and
@@ -229,62 +296,7 @@ softmax_kernel(DevAcsr A, const float *__restrict__ S, TP *__restrict__ P)
         }
         return;
     }
-    if (len > 2048) {
-        // long rows (their re-reads would miss L2): one online pass for max and sum
-        // (the sum is rescaled when the running max grows), then the write pass
-        auto add = [&](float vmax, float s0) {   // s0 = sum of 2^((v - vmax) log2 e) of the group
-            const float mn = fmaxf(m, vmax);
-            l = l * ex2f((m - mn) * L2E) + s0 * ex2f((vmax - mn) * L2E);
-            m = mn;
-        };
-        if (lane < head) add(s[lane], 1.f);
-#pragma unroll 4
-        for (int q = lane; q < nv; q += 32) {
-            const float4 v = s4[q];
-            const float vm = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)), vmL = vm * L2E;
-            add(vm, (ex2f(fmaf(v.x, L2E, -vmL)) + ex2f(fmaf(v.y, L2E, -vmL))) +
-                        (ex2f(fmaf(v.z, L2E, -vmL)) + ex2f(fmaf(v.w, L2E, -vmL))));
-        }
-        for (int x = tail0 + lane; x < len; x += 32) add(s[x], 1.f);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const float m2 = __shfl_xor_sync(0xffffffffu, m, o), l2 = __shfl_xor_sync(0xffffffffu, l, o);
-            const float mn = fmaxf(m, m2);
-            l = (m == -INFINITY ? 0.f : l * ex2f((m - mn) * L2E)) + (m2 == -INFINITY ? 0.f : l2 * ex2f((m2 - mn) * L2E));
-            m = mn;
-        }
-    } else {
-        if (lane < head) m = s[lane];
-#pragma unroll 4
-        for (int q = lane; q < nv; q += 32) {
-            const float4 v = s4[q];
-            m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-        }
-        for (int x = tail0 + lane; x < len; x += 32) m = fmaxf(m, s[x]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        const float mL0 = m * L2E;
-        if (lane < head) l = ex2f(fmaf(s[lane], L2E, -mL0));
-#pragma unroll 4
-        for (int q = lane; q < nv; q += 32) {
-            const float4 v = s4[q];
-            l += (ex2f(fmaf(v.x, L2E, -mL0)) + ex2f(fmaf(v.y, L2E, -mL0))) + (ex2f(fmaf(v.z, L2E, -mL0)) + ex2f(fmaf(v.w, L2E, -mL0)));
-        }
-        for (int x = tail0 + lane; x < len; x += 32) l += ex2f(fmaf(s[x], L2E, -mL0));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    }
-    const float mL = m * L2E;
-    const float inv = 1.f / l;
-    if (lane < head) p[lane] = from_f<TP>(ex2f(fmaf(s[lane], L2E, -mL)) * inv);
-    TP *p4 = p + head;
-#pragma unroll 4
-    for (int q = lane; q < nv; q += 32) {
-        const float4 v = s4[q];
-        store4(p4 + 4 * q, ex2f(fmaf(v.x, L2E, -mL)) * inv, ex2f(fmaf(v.y, L2E, -mL)) * inv,
-               ex2f(fmaf(v.z, L2E, -mL)) * inv, ex2f(fmaf(v.w, L2E, -mL)) * inv);
-    }
-    for (int x = tail0 + lane; x < len; x += 32) p[x] = from_f<TP>(ex2f(fmaf(s[x], L2E, -mL)) * inv);
+    softmax_row_passes(s, p, len, head, nv, tail0, lane);
 }
 
 // <q, k> for one key row: 16-byte loads and four independent FMA chains when d % 4 == 0 and the

@@ -117,8 +117,10 @@ __device__ __forceinline__ void exp32(const float *v, uint64_t cc, uint64_t mm, 
             unpack2(z1, c, d);
             a = ex2(a); b = ex2(b); c = ex2(c); d = ex2(d);
         }
+#ifndef SPLAT_X_NOSUM
         acc0 = fadd2(acc0, pack2(a, b));
         acc1 = fadd2(acc1, pack2(c, d));
+#endif
         pw[x / 2] = pack_bf16(a, b);
         pw[x / 2 + 1] = pack_bf16(c, d);
     }

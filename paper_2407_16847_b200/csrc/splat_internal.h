@@ -244,6 +244,13 @@ struct splat_acsr_s {
     splat_acsr_s *sub_perm = nullptr;
     int32_t rv_l = 0, rv_nk = 0, rv_R = 0;   // stride, rows per residue (N / l), residues per 128-row tile
     float *d_lse = nullptr;                   // [kLaunchSlots][kLseHeads * N] log2-sum-exp of the strided pass
+    // merged plan of the one-launch decomposition (strided-pass pairs, then band-pass pairs; entry,
+    // entry-table and mask indices of the band part offset past the strided part's) and the per-slot
+    // dependency counters [kLaunchSlots][kLseHeads + 1]; null when not built
+    int32_t *d_mix_ent = nullptr, *d_mix_info = nullptr, *d_mix_kv_mask = nullptr;
+    uint32_t *d_mix_masks = nullptr, *d_mix_qt_bits = nullptr;
+    unsigned *d_dep = nullptr;
+    int32_t mix_u1 = 0, mix_u2 = 0;
     // launch slots (top-level device handles only)
     splat::LaunchSlot slots[splat::kLaunchSlots];
     std::atomic<unsigned> next_slot{0};

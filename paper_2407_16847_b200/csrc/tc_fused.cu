@@ -84,6 +84,12 @@ struct Params {
     int rv_sh;                   // log2(rv_nk) (a power of two: nk | 128 or 128 | nk)
     float *lse;
     unsigned long long *sched;   // split kernel: [work counter, done counter], zero between launches
+    // one-launch residue decomposition (VM = 2): the plan is the strided pass's pairs [0, mix_u1)
+    // followed by the band pass's [mix_u1, mix_u1 + mix_u2); units run head-interleaved with a lag of
+    // mix_lag heads (fetch_unit_mixed); dep[bh] counts the strided-pass tiles of head bh whose O_s and
+    // lse are in memory (dep_target = all of them), dep[kLseHeads] the CTAs done (the last resets all)
+    int mix_u1, mix_u2, mix_lag, dep_target;
+    unsigned *dep;
 };
 
 // Profiling knobs (SPLAT_TC_DEBUG) exist only in the diagnostics build (libsplat_diag.so); in the
@@ -95,6 +101,9 @@ struct Params {
 #endif
 #if defined(SPLAT_FUSED_PROF) && !defined(SPLAT_DIAG)
 #error "SPLAT_FUSED_PROF needs the diagnostics build (-DSPLAT_DIAG)"
+#endif
+#if (defined(SPLAT_X_NOMAX) || defined(SPLAT_X_NOSUM) || defined(SPLAT_X_DEPNOW)) && !defined(SPLAT_DIAG)
+#error "ablation macros need the diagnostics build (-DSPLAT_DIAG)"
 #endif
 #ifdef SPLAT_DIAG
 // Profiling aid (SPLAT_TC_DEBUG & 4): clock64 timestamps of pipeline events in CTA 0.
@@ -120,6 +129,7 @@ __device__ int g_trace_n[6];
 struct UnitInfo {
     int pair, bh, e0, e1;
     int j0[3];      // the two query tiles' own entry ranges: tile g owns [j0[g], j0[g+1])
+    int pass;       // VM = 2: 1 = strided pass (residue-major views), 0 = band pass (natural, merge)
 };
 
 __device__ __forceinline__ UnitInfo fetch_unit(const DevAcsr &A, int BH, int u)
@@ -145,6 +155,42 @@ __device__ __forceinline__ UnitInfo fetch_unit(const DevAcsr &A, int BH, int u)
     x.j0[0] = info.w;
     x.j0[1] = info2.x;
     x.j0[2] = info2.y;
+    x.pass = 0;
+    return x;
+}
+
+// One-launch residue decomposition: unit u of the head-interleaved sequence.  Block s of the
+// sequence holds the strided-pass pairs of head s (s < BH) followed by the band-pass pairs of head
+// s - lag (s >= lag), so a band unit of head h is issued about lag heads' worth of units after the
+// strided units it depends on (their O_s / lse are then normally complete and still in L2).
+__device__ __forceinline__ UnitInfo fetch_unit_mixed(const DevAcsr &A, int BH, int U1, int U2, int lag, int u)
+{
+    const int lc = lag < BH ? lag : BH;
+    int bh, k, pass;
+    if (u < lc * U1) {
+        bh = u / U1; k = u % U1; pass = 1;
+    } else {
+        const int v = u - lc * U1, blk = U1 + U2;
+        if (v < (BH - lc) * blk) {
+            const int s = lc + v / blk, w = v % blk;
+            if (w < U1) { bh = s; k = w; pass = 1; }
+            else { bh = s - lag; k = w - U1; pass = 0; }
+        } else {
+            const int v2 = v - (BH - lc) * blk;
+            bh = BH - lc + v2 / U2; k = v2 % U2; pass = 0;
+        }
+    }
+    const int kk = pass ? k : U1 + k;
+    const int4 info = A.pair_info[2 * kk], info2 = A.pair_info[2 * kk + 1];
+    UnitInfo x;
+    x.pair = info.x;
+    x.bh = bh;
+    x.e0 = info.y;
+    x.e1 = info.z;
+    x.j0[0] = info.w;
+    x.j0[1] = info2.x;
+    x.j0[2] = info2.y;
+    x.pass = pass;
     return x;
 }
 
@@ -218,13 +264,20 @@ __device__ __forceinline__ int ent_at(const DevAcsr &A, const UnitInfo &un, cons
 
 using namespace smx;
 
-// VIEW: residue-major 4-D views (strided-row residue pass, permuted plain STRIDED); a separate
-// instantiation so the natural-order kernel carries none of the view arithmetic.
-template <int D, bool VIEW>
+// VM (view mode): 0 = natural order; 1 = residue-major 4-D views (strided-row residue pass, permuted
+// plain STRIDED); 2 = one-launch residue decomposition -- strided-pass units on the views tmQ..tmO,
+// band-pass units on the natural maps tmQ2..tmO2 (unused otherwise).  Separate instantiations, so
+// the natural-order kernel carries none of the view arithmetic.
+template <int D, int VM>
 __global__ void __launch_bounds__(kThreads, 1)
 mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const Params prm)
+               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+               const __grid_constant__ CUtensorMap tmQ2, const __grid_constant__ CUtensorMap tmK2,
+               const __grid_constant__ CUtensorMap tmV2, const __grid_constant__ CUtensorMap tmO2, const Params prm)
 {
+    constexpr bool VIEW = VM == 1;
+#define SPLAT_FETCH(u_) (VM == 2 ? fetch_unit_mixed(A, prm.BH, prm.mix_u1, prm.mix_u2, prm.mix_lag, (u_)) \
+                                 : fetch_unit(A, prm.BH, (u_)))
     using C = Cfg<D>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // No static shared memory precedes the dynamic buffer, so it starts 1024-byte aligned (checked;
@@ -290,14 +343,16 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const CUtensorMap *tm = kq ? &tmK : &tmV;
         uint8_t *ring = smem + (kq ? C::OFF_K : C::OFF_V);
         UnitInfo nx{};
-        if (blockIdx.x < n_units) nx = fetch_unit(A, prm.BH, blockIdx.x);
+        if (blockIdx.x < n_units) nx = SPLAT_FETCH(blockIdx.x);
         EntRegs ner;
         load_ents(A, nx, lane, ner);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const UnitInfo un = nx;
             const EntRegs er = ner;
-            if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
+            if (u + (int)gridDim.x < n_units) nx = SPLAT_FETCH(u + gridDim.x);
             const int pair = un.pair, bh = un.bh;
+            const bool uv = VM == 1 || (VM == 2 && un.pass);     // this unit runs on the residue-major views
+            const CUtensorMap *tmu = VM == 2 && !uv ? (kq ? &tmK2 : &tmV2) : tm;
             if (kq) {
 #pragma unroll
                 for (int g = 0; g < 2; ++g) {
@@ -309,12 +364,12 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                         mbar_expect_tx(&q_full[slot], C::kTileBytes);
 #pragma unroll
                         for (int c = 0; c < C::kChunks; ++c)
-                            if (VIEW)
+                            if (uv)
                                 tma_load_4d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
                                             &q_full[slot], 64 * c, (t << 7) & (prm.rv_nk - 1), (t << 7) >> prm.rv_sh, bh);
                             else
-                                tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64, &tmQ,
-                                            &q_full[slot], 64 * c, t * 128, bh);
+                                tma_load_3d(smem + C::OFF_Q + slot * C::kTileBytes + c * kTileBytes64,
+                                            VM == 2 ? &tmQ2 : &tmQ, &q_full[slot], 64 * c, t * 128, bh);
                     }
                     ++qc[g];
                     if (++qi[g] == C::QS) { qi[g] = 0; qph[g] ^= 1; }
@@ -331,11 +386,11 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     mbar_expect_tx(&full[ki], C::kTileBytes);
 #pragma unroll
                     for (int c = 0; c < C::kChunks; ++c)
-                        if (VIEW)
-                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c,
+                        if (uv)
+                            tma_load_4d(ring + ki * C::kTileBytes + c * kTileBytes64, tmu, &full[ki], 64 * c,
                                         (kv << 6) & (prm.rv_nk - 1), (kv << 6) >> prm.rv_sh, bh);
                         else
-                            tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tm, &full[ki], 64 * c, kv * kKvUnit, bh);
+                            tma_load_3d(ring + ki * C::kTileBytes + c * kTileBytes64, tmu, &full[ki], 64 * c, kv * kKvUnit, bh);
                 }
                 ++kc;
                 if (++ki == C::KS) { ki = 0; kph ^= 1; }
@@ -366,7 +421,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         int qi = 0;
         uint32_t qph = 0, pcnt = 0, scnt = 0;
         uint32_t gent = 0;                                   // global entry counter (ring position)
-        UnitInfo nx = blockIdx.x < n_units ? fetch_unit(A, prm.BH, blockIdx.x) : UnitInfo{0, 0, 0, 0};
+        UnitInfo nx = blockIdx.x < n_units ? SPLAT_FETCH(blockIdx.x) : UnitInfo{0, 0, 0, 0};
         EntRegs ner;
         load_ents(A, nx, lane, ner);
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -375,7 +430,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             un.e0 = __shfl_sync(0xffffffffu, un.e0, 0);
             un.e1 = __shfl_sync(0xffffffffu, un.e1, 0);
             const EntRegs er = ner;
-            if (u + (int)gridDim.x < n_units) nx = fetch_unit(A, prm.BH, u + gridDim.x);
+            if (u + (int)gridDim.x < n_units) nx = SPLAT_FETCH(u + gridDim.x);
             const bool active = 2 * un.pair + g < A.n_qt;
             const int slot = g * C::QS + qi;
             if (active) mbar_wait(&q_full[slot], qph);
@@ -487,22 +542,56 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         uint8_t *ostage = smem + C::OFF_O + g * kTileBytes64;
         const uint32_t ostage_u = smem_u32(ostage);
         uint32_t s_cnt = 0, e_cnt = 0;
+        int dep_pend = -1;           // VM = 2: head whose strided-pass tile this group stored last, not yet signalled
+        // VM = 2: the strided-pass O_s / lse of head dep_pend are complete in memory -> count it for the
+        // band-pass units of that head (done before any wait of this group, so it can never wait on itself)
+        auto dep_signal = [&]() {
+            if (VM == 2 && dep_pend >= 0) {
+                if (store_leader) {
+                    bulk_wait0();                                   // this thread's TMA stores have landed
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    __threadfence();
+                    atomicAdd(prm.dep + dep_pend, 1u);
+                }
+                dep_pend = -1;
+            }
+        };
         // O / l -> bf16 -> swizzled SMEM stage -> TMA store (rows beyond N clipped by the map)
-        auto epilogue = [&](float l, float m, int t, int bh) {
+        // uv: a residue-major (strided-pass) tile; VM = 2 merges every other tile
+        auto epilogue = [&](float l, float m, int t, int bh, bool uv) {
             mbar_wait(&epi[g], e_cnt & 1);
             ++e_cnt;
             tc_fence_after();
             if (store_leader) TRACE(2 + g, 8);
+            const bool merge = VM == 2 ? !uv : prm.merge != 0;
+            dep_signal();
+            if (VM == 2 && merge) {
+                // the strided pass of this head must be complete (its units precede this one in the
+                // sequence, so they are running or done on some CTA)
+                if (lane == 0) {
+                    unsigned v;
+                    // relaxed polls (an acquire per poll would also invalidate the SM's L1), one acquire
+                    // fence once the count is reached
+                    for (long long n = 0;; ++n) {
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(prm.dep + bh) : "memory");
+                        if (v >= (unsigned)prm.dep_target) break;
+                        if (n > (1ll << 26)) __trap();      // a broken dependency fails loudly (~10 s), never hangs
+                        __nanosleep(256);
+                    }
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+                __syncwarp();
+            }
             float inv = l > 0.f ? 1.f / l : 0.f;
             // residue decomposition: natural row of this thread's tile row
             // permuted row p = 128 t + r is residue class p / nk, position p % nk: natural p / nk + l (p % nk)
-            const int nat = VIEW ? ((t * 128 + r) >> prm.rv_sh) + prm.rv_l * ((t * 128 + r) & (prm.rv_nk - 1))
-                                 : t * 128 + r;
+            const int nat = uv ? ((t * 128 + r) >> prm.rv_sh) + prm.rv_l * ((t * 128 + r) & (prm.rv_nk - 1))
+                               : t * 128 + r;
             const bool in_range = nat < prm.N;
             float a_s = 0.f;                      // merge weight of the strided partial (pass 2)
-            if (VIEW && prm.lse && in_range)
+            if (uv && prm.lse && in_range)
                 prm.lse[(size_t)bh * prm.N + nat] = l > 0.f ? m + __log2f(l) : -INFINITY;
-            if (prm.merge) {
+            if (merge) {
                 // O = (O_b 2^(m_b - M) + O_s 2^(lse_s - M)) / (l_b 2^(m_b - M) + 2^(lse_s - M))
                 const float lse_s = in_range ? prm.lse[(size_t)bh * prm.N + nat] : -INFINITY;
                 const float lse_b = l > 0.f ? m + __log2f(l) : -INFINITY;
@@ -520,7 +609,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 tmem_ld32(o_tm + c * 64 + 32, o + 32);
                 tmem_wait_ld();
                 uint32_t w[32];
-                if (prm.merge) {
+                if (merge) {
                     uint4 os[8];
                     const uint4 *src = reinterpret_cast<const uint4 *>(prm.O + ((size_t)bh * prm.N + nat) * D + 64 * c);
 #pragma unroll
@@ -545,20 +634,25 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 fence_proxy_async_smem();
                 named_bar(1 + g, 128);
                 if (store_leader) {
-                    if (VIEW)
+                    if (uv)
                         tma_store_4d(&tmO, ostage, 64 * c, (t << 7) & (prm.rv_nk - 1), (t << 7) >> prm.rv_sh, bh);
-                    else tma_store_3d(&tmO, ostage, 64 * c, t * 128, bh);
+                    else tma_store_3d(VM == 2 ? &tmO2 : &tmO, ostage, 64 * c, t * 128, bh);
                     bulk_commit();
                 }
             }
+            if (VM == 2 && uv) dep_pend = bh;     // signalled at this group's next epilogue (or exit)
+#ifdef SPLAT_X_DEPNOW
+            dep_signal();                         // ablation (diagnostics build): signal immediately
+#endif
             tc_fence_before();
             if (store_leader) TRACE(2 + g, 9);
         };
         bool pe_on = false;          // deferred epilogue of the previous unit (SEP)
         float pe_l = 0.f, pe_m = 0.f;
         int pe_t = 0, pe_bh = 0;
+        bool pe_uv = false;
         UnitInfo nx{};
-        if (blockIdx.x < n_units) nx = fetch_unit(A, prm.BH, blockIdx.x);
+        if (blockIdx.x < n_units) nx = SPLAT_FETCH(blockIdx.x);
         TileRegs ntr;
         load_tile(A, nx.j0[g], nx.j0[g + 1], lane, ntr);
         uint4 pf = make_uint4(~0u, ~0u, ~0u, ~0u);     // mask of the next entry to process
@@ -567,7 +661,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             const UnitInfo un = nx;
             const TileRegs tr = ntr;
             const bool has_next = u + (int)gridDim.x < n_units;
-            if (has_next) nx = fetch_unit(A, prm.BH, u + gridDim.x);
+            if (has_next) nx = SPLAT_FETCH(u + gridDim.x);
             const int j0 = un.j0[g], j1 = un.j0[g + 1];
             // next unit's entries and its first mask: issued during this unit's last entry
 #define SPLAT_NEXT_UNIT_PREFETCH()                                                                      \
@@ -583,7 +677,8 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 continue;
             }
             const int bh = un.bh;
-            if (!VIEW && prm.merge) {
+            const bool uv = VM == 1 || (VM == 2 && un.pass);
+            if (VM == 2 ? !uv : (!VIEW && prm.merge)) {
                 // the merging epilogue of this tile (deferred past the next unit's first tile) reads
                 // this row's strided-pass O_s and lse: pull them into L2 now
                 const int nat = t * 128 + r;
@@ -668,7 +763,7 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (store_leader) TRACE(2 + g, 13);
                 if constexpr (SEP) {
                     if (pe_on) {             // the previous unit's epilogue (first tile of a unit only)
-                        epilogue(pe_l, pe_m, pe_t, pe_bh);
+                        epilogue(pe_l, pe_m, pe_t, pe_bh, pe_uv);
                         pe_on = false;
                     }
                     if (s_cnt > 1) {
@@ -709,13 +804,14 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             // the wait for this unit's last PV overlaps them; the first PV of the next unit
             // (accumulate = 0) is issued only after that tile's P, i.e. after O was read out.
             if constexpr (SEP) {
-                if (j0 == j1) epilogue(l_run, m_run, t, bh);      // degenerate: no entry to defer into
-                else { pe_on = true; pe_l = l_run; pe_m = m_run; pe_t = t; pe_bh = bh; }
+                if (j0 == j1) epilogue(l_run, m_run, t, bh, uv);      // degenerate: no entry to defer into
+                else { pe_on = true; pe_l = l_run; pe_m = m_run; pe_t = t; pe_bh = bh; pe_uv = uv; }
             } else {
-                epilogue(l_run, m_run, t, bh);
+                epilogue(l_run, m_run, t, bh, uv);
             }
         }
-        if (pe_on) epilogue(pe_l, pe_m, pe_t, pe_bh);
+        if (pe_on) epilogue(pe_l, pe_m, pe_t, pe_bh, pe_uv);
+        dep_signal();
         if (store_leader) bulk_wait0();
     }
     __syncthreads();
@@ -723,6 +819,16 @@ mhsa_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
+    if (VM == 2 && threadIdx.x == 0) {
+        // the last CTA resets the dependency counters for the next launch on this launch slot
+        __threadfence();
+        if (atomicAdd(prm.dep + kLseHeads, 1u) == gridDim.x - 1u) {
+            for (int i = 0; i < prm.BH; ++i) prm.dep[i] = 0u;
+            prm.dep[kLseHeads] = 0u;
+            __threadfence();
+        }
+    }
+#undef SPLAT_FETCH
 }
 
 #ifdef SPLAT_FUSED_PROF
@@ -1183,6 +1289,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 }
                 if (store_leader) TRACE(2 + g, 12);
                 mx *= c2;
+#ifdef SPLAT_X_NOMAX
+                mx = sv[0] * c2 + 1.f;      // ablation (diagnostics build only): no row max
+#endif
                 float alpha = 1.f;
                 bool resc = false;
                 if (mx > m_run + kRescaleThresh) {
@@ -1279,13 +1388,32 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
 struct ResidueArgs {
     int view = 0, merge = 0, R = 0, nk = 0, l = 0;
     float *lse = nullptr;
+    // one-launch decomposition (view = 2): pairs of the strided / band pass in the merged plan,
+    // lag in heads, dependency counters of the launch slot
+    int u1 = 0, u2 = 0, lag = 0;
+    unsigned *dep = nullptr;
 };
+
+template <int D, int VM>
+cudaError_t set_smem_once()
+{
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr_set[dev & 63]) {
+        const cudaError_t e = cudaFuncSetAttribute(mhsa_tc_kernel<D, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   Cfg<D>::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set[dev & 63] = true;
+    }
+    return cudaSuccess;
+}
 
 template <int D>
 cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, float scale, void *O,
                      cudaStream_t st, const ResidueArgs &ra = ResidueArgs())
 {
-    CUtensorMap mq, mk, mv, mo;
+    CUtensorMap mq, mk, mv, mo, mq2, mk2, mv2, mo2;
     if (ra.view) {
         if (!make_map_residue(&mq, Q, BH, A.n, D, ra.l, ra.nk, ra.R) || !make_map_residue(&mk, K, BH, A.n, D, ra.l, ra.nk, ra.R) ||
             !make_map_residue(&mv, V, BH, A.n, D, ra.l, ra.nk, ra.R) || !make_map_residue(&mo, O, BH, A.n, D, ra.l, ra.nk, ra.R))
@@ -1294,17 +1422,22 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
                !make_map(&mo, O, BH, A.n, D)) {
         return cudaErrorInvalidValue;
     }
-    static bool attr_set[2][64] = {};
+    if (ra.view == 2) {
+        if (!make_map(&mq2, Q, BH, A.n, D) || !make_map(&mk2, K, BH, A.n, D) || !make_map(&mv2, V, BH, A.n, D) ||
+            !make_map(&mo2, O, BH, A.n, D))
+            return cudaErrorInvalidValue;
+    } else {
+        mq2 = mq; mk2 = mk; mv2 = mv; mo2 = mo;
+    }
     int dev = 0;
     cudaGetDevice(&dev);
-    const int vw = ra.view ? 1 : 0;
-    if (!attr_set[vw][dev & 63]) {
-        cudaError_t e = ra.view ? cudaFuncSetAttribute(mhsa_tc_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM)
-                                : cudaFuncSetAttribute(mhsa_tc_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::SMEM);
+    {
+        cudaError_t e;
+        if constexpr (D == 128) e = ra.view == 2 ? set_smem_once<D, 2>() : ra.view ? set_smem_once<D, 1>() : set_smem_once<D, 0>();
+        else e = ra.view == 2 ? cudaErrorNotSupported : ra.view ? set_smem_once<D, 1>() : set_smem_once<D, 0>();
         if (e != cudaSuccess) return e;
-        attr_set[vw][dev & 63] = true;
     }
-    Params p;
+    Params p{};
     p.A = A;
     p.BH = BH;
     p.N = A.n;
@@ -1320,12 +1453,22 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     while ((1 << p.rv_sh) < ra.nk) ++p.rv_sh;
     p.rv_l = ra.l;
     p.lse = ra.lse;
+    p.mix_u1 = ra.u1;
+    p.mix_u2 = ra.u2;
+    p.mix_lag = ra.lag;
+    p.dep = ra.dep;
+    p.dep_target = A.n_qt;          // strided-pass tiles per head
     const long long units = (long long)A.n_pairs * BH;
     const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
-    if (ra.view)
-        mhsa_tc_kernel<D, true><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, p);
+    if (ra.view == 2) {
+        if constexpr (D == 128)
+            mhsa_tc_kernel<D, 2><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, mq2, mk2, mv2, mo2, p);
+        else
+            return cudaErrorNotSupported;
+    } else if (ra.view)
+        mhsa_tc_kernel<D, 1><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, mq2, mk2, mv2, mo2, p);
     else
-        mhsa_tc_kernel<D, false><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, p);
+        mhsa_tc_kernel<D, 0><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, mq2, mk2, mv2, mo2, p);
     return cudaGetLastError();
 }
 
@@ -1398,6 +1541,32 @@ extern "C" int splat_debug_trace(unsigned long long *out, int *counts)
     return 0;
 }
 #endif  // SPLAT_DIAG
+
+cudaError_t launch_mhsa_tc_residue1(const DevAcsr &mix, int u1, int u2, int l, int nk, int R, float *lse, unsigned *dep,
+                                    const void *Q, const void *K, const void *V, int BH, int d, float scale, void *O,
+                                    cudaStream_t st, int *n_launch)
+{
+    *n_launch = 1;
+    if (d != 128 || BH > kLseHeads || !dep) return cudaErrorNotSupported;
+    ResidueArgs r;
+    r.view = 2;
+    r.R = R;
+    r.nk = nk;
+    r.l = l;
+    r.lse = lse;
+    r.u1 = u1;
+    r.u2 = u2;
+    r.dep = dep;
+    // lag: about 1.5 waves of units between a head's strided units and its band units, so the band
+    // units rarely wait and the head's Q / K / V / O_s are still in L2 when they run
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int per_head = u1 + u2 > 0 ? u1 + u2 : 1;
+    r.lag = (3 * num_sms(dev) / 2 + per_head - 1) / per_head;
+    if (const int lag = diag_env("SPLAT_MIX_LAG"); lag > 0) r.lag = lag;     // diagnostics build only
+    if (r.lag < 1) r.lag = 1;
+    return launch_d<128>(mix, Q, K, V, BH, scale, O, st, r);
+}
 
 cudaError_t launch_mhsa_tc_residue(const DevAcsr &band, const DevAcsr &str, int l, int nk, int R, float *lse,
                                    const void *Q, const void *K, const void *V, int BH, int d, float scale, void *O,

@@ -419,3 +419,28 @@ def test_bf16_fused_edge_cases(cfg):
     Of = Of.view(shp).float().cpu()
     for bh, o in zip(heads, refs):
         assert maxabs(Of[bh], o) <= TOL_BF16, (cfg.name, bh)
+
+
+@pytest.mark.gpu
+def test_residue_head_chunks_and_repeat():
+    # the residue decomposition over B*H = 70 heads: two head chunks of the launch slot's lse
+    # scratch (kLseHeads = 64); repeated calls must give bitwise-identical O and every sampled head
+    # (both chunks) must match the oracle
+    cfg = Config("st_res_chunks", Pattern("strided_local", 1024, stride=16, causal=1), 7, 10, 128, "bf16", 216)
+    q, k, v = make_qkv(cfg)
+    a = S.Acsr(cfg.pattern, device=DEV)
+    Q, K, V = dev(q), dev(k), dev(v)
+    outs = []
+    for _ in range(3):
+        Of = torch.empty_like(Q)
+        S.splat_sparse_mhsa(a, Q, K, V, Of, cfg.scale)
+        torch.cuda.synchronize()
+        outs.append(Of.view(cfg.BH, cfg.N, cfg.d).cpu())
+    assert S.last_launch_count() == 4          # two launches (strided pass, band pass) per head chunk
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    shp = (cfg.BH, cfg.N, cfg.d)
+    heads = [0, 33, 63, 64, 69]
+    refs = oracle_heads(cfg.pattern, q.view(shp), k.view(shp), v.view(shp), cfg.scale, heads)
+    for bh, o in zip(heads, refs):
+        o = o[0] if isinstance(o, tuple) else o
+        assert maxabs(outs[0][bh].float(), o) <= TOL_BF16, bh
