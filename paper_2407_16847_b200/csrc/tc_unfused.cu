@@ -312,8 +312,11 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             if (e >= e1) continue;
             const int row = t * 128 + r;
             RowRuns R;
+            PSPAN_BEGIN(t_row);
             const long long rowoff = row_offset(prm, bh, t, r, R);
+            PSPAN_END(6, t_row);
             for (; e < e1; e += kNWG) {
+                PSPAN_BEGIN(t_meta);              // wait profile (SPLAT_UNF_PROF): per-tile metadata phase
                 const int ent = A.kv[e];
                 const int c0 = (ent & kKvMask) * kKvUnit;
                 const bool partial = (ent & kPartialBit) != 0;
@@ -337,6 +340,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 dst[2] = make_int2(rel + p2, (int)m4.z);
                 dst[3] = make_int2(rel + p3, (int)m4.w);
                 wg_sync(1 + eg);
+                PSPAN_END(6, t_meta);
                 PWAIT(5, &s_full[eg], k & 1);
                 tc_fence_after();
                 const unsigned long long baddr = reinterpret_cast<unsigned long long>(Sg + tbase[tb]);
