@@ -590,7 +590,9 @@ void build_residue_split(splat_acsr_s *a, void *stream)
     a->rv_l = l;
     a->rv_nk = nk;
     a->rv_R = 128 / nk;
-    build_residue_merged(a, (cudaStream_t)stream);
+#ifdef SPLAT_DIAG
+    build_residue_merged(a, (cudaStream_t)stream);    // the one-launch experiment (DESIGN 9g)
+#endif
 }
 
 // Launch slots and the host pipeline's streams / events of a top-level device handle (build time,

@@ -1433,8 +1433,11 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     cudaGetDevice(&dev);
     {
         cudaError_t e;
+#ifdef SPLAT_DIAG
         if constexpr (D == 128) e = ra.view == 2 ? set_smem_once<D, 2>() : ra.view ? set_smem_once<D, 1>() : set_smem_once<D, 0>();
-        else e = ra.view == 2 ? cudaErrorNotSupported : ra.view ? set_smem_once<D, 1>() : set_smem_once<D, 0>();
+        else
+#endif
+            e = ra.view == 2 ? cudaErrorNotSupported : ra.view ? set_smem_once<D, 1>() : set_smem_once<D, 0>();
         if (e != cudaSuccess) return e;
     }
     Params p{};
@@ -1461,9 +1464,11 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
     const long long units = (long long)A.n_pairs * BH;
     const int grid = (int)(units < num_sms(dev) ? units : num_sms(dev));
     if (ra.view == 2) {
+#ifdef SPLAT_DIAG
         if constexpr (D == 128)
             mhsa_tc_kernel<D, 2><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, mq2, mk2, mv2, mo2, p);
         else
+#endif
             return cudaErrorNotSupported;
     } else if (ra.view)
         mhsa_tc_kernel<D, 1><<<grid, kThreads, Cfg<D>::SMEM, st>>>(mq, mk, mv, mo, mq2, mk2, mv2, mo2, p);
@@ -1614,7 +1619,9 @@ cudaError_t launch_mhsa_tc(const DevAcsr &A, const void *Q, const void *K, const
     // kernel, =3 the half-row double-buffered kernel of tc_fused64.cu (experimental)
     static const int alt64 = diag_env("SPLAT_TC_PAIRED64");
     if (d == 64 && alt64 == 0) return launch_split64(A, Q, K, V, BH, scale, O, st);
+#ifdef SPLAT_DIAG
     if (d == 64 && alt64 == 3) return launch_mhsa64(A, Q, K, V, BH, scale, O, st);
+#endif
     if (d == 64) return launch_d<64>(A, Q, K, V, BH, scale, O, st);
     if (d == 128) return launch_d<128>(A, Q, K, V, BH, scale, O, st);
     return cudaErrorNotSupported;

@@ -23,6 +23,8 @@
 // epilogue.
 //
 // TMEM (512 columns): S_g [128 g, 128 g + 128), O_g [256 + 64 g, +64), P_g [384 + 64 g, +64).
+// Diagnostics build only (SPLAT_TC_PAIRED64=3): the product library does not contain this kernel.
+#ifdef SPLAT_DIAG
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -605,3 +607,4 @@ cudaError_t launch_mhsa64(const DevAcsr &A, const void *Q, const void *K, const 
 }
 
 }  // namespace splat
+#endif  // SPLAT_DIAG
