@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(512, 1) k(unsigned long long *out, int nw)
             tmem_ld32(base + 64, v + 64);
             tmem_ld32(base + 96, v + 96);
             tmem_wait_ld();
-            acc += v[i & 127] + v[(i + 64) & 127];
+            acc += v[0] + v[37] + v[64] + v[127];   // static indices: v stays in registers
         }
         unsigned long long t1 = clock64();
         if ((threadIdx.x & 31) == 0) out[blockIdx.x * 32 + warp] = t1 - t0;
