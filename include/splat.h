@@ -184,6 +184,14 @@ splat_status splat_plan_split_info(splat_acsr a, int32_t *row_classes, int32_t *
 int64_t splat_plan_sizes(splat_acsr a, int32_t which);
 splat_status splat_plan_split_copy(splat_acsr a, int32_t *units, int32_t *kv, int32_t *mask_id, uint32_t *masks);
 
+/* Split-K unit list of the same kernel, taken by a launch when its longest
+ * whole tile would outlast a tile group's average share of the work (few heads per GPU): every tile
+ * with more than 8 entries is cut into parts with contiguous entry ranges whose partial softmax
+ * results the last part merges.  splat_plan_sizes(a, 3) = its units per (b, h) (0: no long tile);
+ * units int32 [n][4] = (tile as above, j0, j1, part | parts << 8 | split-tile index << 16; 0 for a
+ * whole tile), same entry numbering as splat_plan_split_copy. */
+splat_status splat_plan_ksplit_copy(splat_acsr a, int32_t *units);
+
 /* Free a handle and its device memory.  NULL is a no-op. */
 splat_status splat_acsr_destroy(splat_acsr a);
 

@@ -130,6 +130,12 @@ void free_device(splat_acsr_s *a)
     a->sub_band = a->sub_str = a->sub_perm = nullptr;
     cudaFree(a->d_lse);
     a->d_lse = nullptr;
+    cudaFree(a->d_ks_o);
+    cudaFree(a->d_ks_lse);
+    cudaFree(a->d_ks_cnt);
+    a->d_ks_o = nullptr;
+    a->d_ks_lse = nullptr;
+    a->d_ks_cnt = nullptr;
     for (void *q : {(void *)a->d_mix_ent, (void *)a->d_mix_info, (void *)a->d_mix_kv_mask, (void *)a->d_mix_masks,
                     (void *)a->d_mix_qt_bits, (void *)a->d_dep})
         cudaFree(q);
@@ -157,6 +163,7 @@ void free_device(splat_acsr_s *a)
     cudaFree(a->plan.d_kv_mask);
     cudaFree(a->plan.d_qt_bits);
     cudaFree(a->plan.d_t_info);
+    cudaFree(a->plan.d_t_info_ks);
     cudaFree(a->plan.d_sched);
 }
 
@@ -194,6 +201,23 @@ DevAcsr dev_view(const splat_acsr_s *a, int slot = 0)
     for (int b = 0; b <= a->plan.n_buckets && b <= kMaxBuckets; ++b) A.bucket_start[b] = a->plan.bucket_start[b];
     A.t_info = reinterpret_cast<const int4 *>(a->plan.d_t_info);
     A.sched = a->plan.d_sched ? a->plan.d_sched + 2 * slot : nullptr;
+    A.t_n = (int)(a->plan.t_info.size() / 4);
+    A.t_max_len = a->plan.t_max_len;
+    A.t_entries = 0;
+    for (size_t k = 0; k < a->plan.t_info.size(); k += 4) A.t_entries += a->plan.t_info[k + 2] - a->plan.t_info[k + 1];
+    A.t_info_ks = reinterpret_cast<const int4 *>(a->plan.d_t_info_ks);
+    A.t_n_ks = (int)(a->plan.t_info_ks.size() / 4);
+    A.t_n_buckets_ks = a->plan.t_n_buckets_ks;
+    for (int b = 0; b < (int)a->plan.t_bucket_start_ks.size() && b <= kMaxBuckets; ++b)
+        A.t_bucket_start_ks[b] = a->plan.t_bucket_start_ks[b];
+    A.n_ksplit = a->plan.n_ksplit;
+    A.ks_pmax = a->plan.ksplit_pmax;
+    {
+        const size_t tiles = (size_t)kSplitHeads * a->plan.n_ksplit, parts = tiles * a->plan.ksplit_pmax;
+        A.ks_o = a->d_ks_o ? static_cast<char *>(a->d_ks_o) + (size_t)slot * parts * 128 * 64 * 2 : nullptr;
+        A.ks_lse = a->d_ks_lse ? a->d_ks_lse + (size_t)slot * parts * 128 : nullptr;
+        A.ks_cnt = a->d_ks_cnt ? a->d_ks_cnt + (size_t)slot * tiles : nullptr;
+    }
     A.t_n_buckets = a->plan.t_n_buckets;
     A.row_classes = a->plan.row_classes;
     for (int b = 0; b <= a->plan.t_n_buckets && b <= kMaxBuckets; ++b) A.t_bucket_start[b] = a->plan.t_bucket_start[b];
@@ -319,7 +343,8 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
         (e = dev_alloc(&P.d_mask_cnt, P.mask_cnt.empty() ? 16 : P.mask_cnt.size())) != cudaSuccess ||
         (e = dev_alloc(&P.d_kv_mask, sizeof(int32_t) * (P.kv_mask.empty() ? 1 : P.kv_mask.size()))) != cudaSuccess ||
         (e = dev_alloc(&P.d_qt_bits, sizeof(uint32_t) * (P.qt_bits.empty() ? 1 : P.qt_bits.size()))) != cudaSuccess ||
-        (e = dev_alloc(&P.d_t_info, sizeof(int32_t) * 4 * P.n_qt)) != cudaSuccess ||
+        (e = dev_alloc(&P.d_t_info, sizeof(int32_t) * (P.t_info.empty() ? 4 : P.t_info.size()))) != cudaSuccess ||
+        (e = dev_alloc(&P.d_t_info_ks, sizeof(int32_t) * (P.t_info_ks.empty() ? 4 : P.t_info_ks.size()))) != cudaSuccess ||
         (e = dev_alloc(&P.d_sched, kLaunchSlots * 2 * sizeof(unsigned long long))) != cudaSuccess) {
         free_device(a);
         delete a;
@@ -345,7 +370,9 @@ splat_status finish_device_build(splat_acsr_s *a, cudaStream_t cs, splat_acsr *o
     if (e == cudaSuccess && !P.qt_bits.empty())
         e = cudaMemcpyAsync(P.d_qt_bits, P.qt_bits.data(), sizeof(uint32_t) * P.qt_bits.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(P.d_t_info, P.t_info.data(), sizeof(int32_t) * 4 * P.n_qt, cudaMemcpyHostToDevice, cs);
+        e = cudaMemcpyAsync(P.d_t_info, P.t_info.data(), sizeof(int32_t) * P.t_info.size(), cudaMemcpyHostToDevice, cs);
+    if (e == cudaSuccess && !P.t_info_ks.empty())
+        e = cudaMemcpyAsync(P.d_t_info_ks, P.t_info_ks.data(), sizeof(int32_t) * P.t_info_ks.size(), cudaMemcpyHostToDevice, cs);
     if (e == cudaSuccess) e = cudaMemsetAsync(P.d_sched, 0, kLaunchSlots * 2 * sizeof(unsigned long long), cs);
     if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) {
@@ -606,6 +633,16 @@ splat_status create_call_resources(splat_acsr_s *a)
         e = cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t *>(&a->slots[i].ev), cudaEventDisableTiming);
     for (int i = 0; i < 3 && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t *>(&a->hs[i]), cudaStreamNonBlocking);
+    if (e == cudaSuccess && a->plan.n_ksplit > 0) {
+        // split-K partial results of the d = 64 fused kernel, per launch slot (bf16 O + lse2 per part
+        // and row, one counter per split tile), zeroed once: the merging part resets its counter
+        const size_t tiles = (size_t)kLaunchSlots * kSplitHeads * a->plan.n_ksplit;
+        const size_t parts = tiles * a->plan.ksplit_pmax;
+        if ((e = dev_alloc_bytes(&a->d_ks_o, parts * 128 * 64 * 2)) == cudaSuccess &&
+            (e = dev_alloc(&a->d_ks_lse, parts * 128 * sizeof(float))) == cudaSuccess &&
+            (e = dev_alloc(&a->d_ks_cnt, tiles * sizeof(unsigned))) == cudaSuccess)
+            e = cudaMemset(a->d_ks_cnt, 0, tiles * sizeof(unsigned));
+    }
     for (int i = 0; i < 2 && e == cudaSuccess; ++i)
         for (int c = 0; c < 16 && e == cudaSuccess; ++c)
             e = cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t *>(&a->hev[i][c]), cudaEventDisableTiming);
@@ -689,7 +726,7 @@ cudaError_t launch_mhsa(splat_acsr a, const void *Q, const void *K, const void *
         e = launch_mhsa_tc_permuted(dev_view(a->sub_perm), a->rv_l, a->rv_nk, a->rv_R, Q, K, V, BH, d, scale, O, s,
                                     &nl);
     else if (dt == SPLAT_BF16 && d == 64) {
-        SlotUse su(a, s);                // the split kernel's work counter
+        SlotUse su(a, s);                // the split kernel's work counter (and split-K scratch)
         e = launch_mhsa_tc(dev_view(a, su.index), Q, K, V, BH, d, scale, O, s, &nl);
     } else if (dt == SPLAT_BF16)
         e = launch_mhsa_tc(dev_view(a), Q, K, V, BH, d, scale, O, s, &nl);
@@ -866,6 +903,7 @@ int64_t splat_plan_sizes(splat_acsr a, int32_t which)
     case 0: return (int64_t)P.t_info.size() / 4;   // split-kernel units per (b, h)
     case 1: return (int64_t)P.kv.size();           // all entries (natural, then classed)
     case 2: return (int64_t)P.n_masks;
+    case 3: return (int64_t)P.t_info_ks.size() / 4;   // split-K units per (b, h)
     default: return -1;
     }
 }
@@ -879,6 +917,15 @@ splat_status splat_plan_split_copy(splat_acsr a, int32_t *units, int32_t *kv, in
     if (kv) memcpy(kv, P.kv.data(), sizeof(int32_t) * P.kv.size());
     if (mask_id) memcpy(mask_id, P.kv_mask.data(), sizeof(int32_t) * P.kv_mask.size());
     if (masks) memcpy(masks, P.masks.data(), sizeof(uint32_t) * P.masks.size());
+    return SPLAT_OK;
+}
+
+splat_status splat_plan_ksplit_copy(splat_acsr a, int32_t *units)
+{
+    clear_error();
+    if (!a || !units) return set_error(SPLAT_ERR_INVALID_ARG, "null handle or output");
+    const Plan &P = a->plan;
+    if (!P.t_info_ks.empty()) memcpy(units, P.t_info_ks.data(), sizeof(int32_t) * P.t_info_ks.size());
     return SPLAT_OK;
 }
 

@@ -35,6 +35,19 @@ struct DevAcsr {
     int row_classes;            // t_info tiles are packed 64-row segment pairs (a | b << 16)
     int t_bucket_start[kMaxBuckets + 1];
     unsigned long long *sched;  // [2]: dynamic work counter + done counter of the split kernel
+    int t_n;                    // split-kernel units per (b, h) (t_info rows)
+    int t_max_len, t_entries;   // longest whole-tile unit, plan entries per (b, h) of the split kernel
+    // the split-K unit list (long tiles in parts): swapped in by the launch for few heads per GPU
+    const int4 *t_info_ks;
+    int t_n_ks, t_n_buckets_ks;
+    int t_bucket_start_ks[kMaxBuckets + 1];
+    // split-K partial results of the launch slot (plan.cpp: n_ksplit long tiles per head, up to
+    // ks_pmax parts each): per (head, split tile, part, row) the normalised partial O (bf16, 64 per
+    // row) and its lse2; per (head, split tile) the arrival counter (zero between launches)
+    void *ks_o;
+    float *ks_lse;
+    unsigned *ks_cnt;
+    int n_ksplit, ks_pmax;
     // the descriptor of a descriptor-built handle (has_pat = 1): kernels may evaluate a row's runs
     // in closed form (row_segments) instead of loading them; 0 for mask-ingest handles
     splat_pattern pat;

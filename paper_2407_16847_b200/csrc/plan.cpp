@@ -348,30 +348,74 @@ void build_plan(splat_acsr_s &a)
     P.n_masks = (int)(P.masks.size() / (128 * 4));
 
     // ---- split-kernel work units: its tiles in cost buckets (floor(log2(entries))), longest
-    // first, walked head-major inside a bucket; (tile or segments a | b << 16, j0, j1, 0)
+    // first, walked head-major inside a bucket; (tile or segments a | b << 16, j0, j1, split).
+    // Two lists: whole tiles (t_info), and the same with split-K of long tiles (t_info_ks): a tile
+    // with more than kSplitMax entries (the global-row tiles) becomes np parts with contiguous entry
+    // ranges, split = part | np << 8 | sid << 16 (sid = the tile's index among the split tiles of a
+    // head); the kernel merges the parts' partial softmax results (the last part to finish).  The
+    // launch takes the split list when a long tile would outlast the average work of a tile group
+    // (few heads per GPU: DESIGN.md section 8).
     {
-        const int nt = (int)seg_a.size();
-        auto tb = [&](int t) {
-            int len = tj1[t] - tj0[t], b = 0;
-            while (len > 1) { len >>= 1; ++b; }
-            return b;
+        auto emit = [&](bool ksplit, std::vector<int32_t> &info, std::vector<int32_t> &bstart, int &nbk, int &n_split,
+                        int &pmax) {
+            std::vector<int32_t> ut, uj0, uj1, usp;
+            n_split = 0;
+            pmax = 0;
+            for (size_t t = 0; t < seg_a.size(); ++t) {
+                const int32_t tt = P.row_classes ? (seg_a[t] | (seg_b[t] << 16)) : (int32_t)t;
+                const int n = tj1[t] - tj0[t];
+                if (ksplit && n > kSplitMax) {
+                    const int np = std::min((n + kSplitMax - 1) / kSplitMax, kSplitPartsMax);
+                    for (int q = 0; q < np; ++q) {
+                        ut.push_back(tt);
+                        uj0.push_back(tj0[t] + (int)((long long)n * q / np));
+                        uj1.push_back(tj0[t] + (int)((long long)n * (q + 1) / np));
+                        usp.push_back(q | (np << 8) | (n_split << 16));
+                    }
+                    pmax = std::max(pmax, np);
+                    ++n_split;
+                } else {
+                    ut.push_back(tt);
+                    uj0.push_back(tj0[t]);
+                    uj1.push_back(tj1[t]);
+                    usp.push_back(0);
+                }
+            }
+            const int nt = (int)ut.size();
+            auto tb = [&](int t) {
+                int len = uj1[t] - uj0[t], b = 0;
+                while (len > 1) { len >>= 1; ++b; }
+                return b;
+            };
+            std::vector<int> to(nt);
+            std::iota(to.begin(), to.end(), 0);
+            std::stable_sort(to.begin(), to.end(), [&](int x, int y) { return tb(x) > tb(y); });
+            bstart.clear();
+            for (int i = 0; i < nt; ++i)
+                if (i == 0 || tb(to[i]) != tb(to[i - 1])) bstart.push_back(i);
+            bstart.push_back(nt);
+            nbk = (int)bstart.size() - 1;
+            info.assign((size_t)nt * 4, 0);
+            for (int k = 0; k < nt; ++k) {
+                // natural tiles: the tile index (segments 2t, 2t + 1); classed (N <= 65536): packed segments
+                info[4 * k + 0] = ut[to[k]];
+                info[4 * k + 1] = uj0[to[k]];
+                info[4 * k + 2] = uj1[to[k]];
+                info[4 * k + 3] = usp[to[k]];
+            }
         };
-        std::vector<int> to(nt);
-        std::iota(to.begin(), to.end(), 0);
-        std::stable_sort(to.begin(), to.end(), [&](int x, int y) { return tb(x) > tb(y); });
-        P.t_bucket_start.clear();
-        for (int i = 0; i < nt; ++i)
-            if (i == 0 || tb(to[i]) != tb(to[i - 1])) P.t_bucket_start.push_back(i);
-        P.t_bucket_start.push_back(nt);
-        P.t_n_buckets = (int)P.t_bucket_start.size() - 1;
-        P.t_info.assign((size_t)nt * 4, 0);
-        for (int k = 0; k < nt; ++k) {
-            // natural tiles: the tile index (segments 2t, 2t + 1); classed (N <= 65536): packed segments
-            P.t_info[4 * k + 0] = P.row_classes ? (seg_a[to[k]] | (seg_b[to[k]] << 16)) : to[k];
-            P.t_info[4 * k + 1] = tj0[to[k]];
-            P.t_info[4 * k + 2] = tj1[to[k]];
+        int ns0 = 0, pm0 = 0;
+        emit(false, P.t_info, P.t_bucket_start, P.t_n_buckets, ns0, pm0);
+        P.n_split_tiles = (int)(P.t_info.size() / 4);
+        P.t_max_len = 0;
+        for (size_t k = 0; k < P.t_info.size(); k += 4) P.t_max_len = std::max(P.t_max_len, P.t_info[k + 2] - P.t_info[k + 1]);
+        if (ablate == 0 && P.t_max_len > kSplitMax && (int)P.t_bucket_start.size() <= kMaxBuckets + 1) {
+            emit(true, P.t_info_ks, P.t_bucket_start_ks, P.t_n_buckets_ks, P.n_ksplit, P.ksplit_pmax);
+        } else {
+            P.t_info_ks.clear();
+            P.n_ksplit = 0;
+            P.ksplit_pmax = 0;
         }
-        P.n_split_tiles = nt;
     }
     // R-SpMM row records of every PARTIAL mask: per row and 8-column group g the live columns left
     // of the group (low byte) and the group's 8 mask bits (high byte), and per row the live count

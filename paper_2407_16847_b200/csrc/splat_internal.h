@@ -173,6 +173,11 @@ struct Plan {
     int kv_align = 1;                     // window starts: multiples of kv_align * 64 columns
     int row_classes = 0;                  // split-kernel tiles regrouped by row class (plan.cpp)
     int n_split_tiles = 0;                // split-kernel work units per (b, h)
+    int n_ksplit = 0, ksplit_pmax = 0;    // split-K: long tiles per (b, h) split into parts, max parts
+    int t_max_len = 0;                    // entries of the longest whole-tile unit
+    int t_n_buckets_ks = 0;               // the split-K unit list (t_info_ks), bucketed like t_info
+    std::vector<int32_t> t_bucket_start_ks, t_info_ks;
+    int32_t *d_t_info_ks = nullptr;
     std::vector<int32_t> qt_ptr, kv, order;          // per query tile (ABI: splat_plan_copy)
     // query-tile pairs
     int n_pairs = 0, n_pair_entries = 0, n_buckets = 0, n_masks = 0;
@@ -206,6 +211,11 @@ struct Plan {
 constexpr int kLaunchSlots = 8;
 // heads (b, h) per launch of the residue decomposition (lse scratch per slot: kLseHeads x N floats)
 constexpr int kLseHeads = 64;
+// split-K of the d = 64 fused kernel's long tiles (plan.cpp): entries per part, parts per tile, and
+// heads per launch (the per-slot partial-result scratch holds kSplitHeads heads)
+constexpr int kSplitMax = 8;
+constexpr int kSplitPartsMax = 16;
+constexpr int kSplitHeads = 128;
 
 struct LaunchSlot {
     std::mutex mu;
@@ -244,6 +254,11 @@ struct splat_acsr_s {
     splat_acsr_s *sub_perm = nullptr;
     int32_t rv_l = 0, rv_nk = 0, rv_R = 0;   // stride, rows per residue (N / l), residues per 128-row tile
     float *d_lse = nullptr;                   // [kLaunchSlots][kLseHeads * N] log2-sum-exp of the strided pass
+    // split-K scratch of the d = 64 fused kernel (plan.n_ksplit > 0), [kLaunchSlots][kSplitHeads][n_ksplit]
+    // x [ksplit_pmax][128 rows]: partial O (bf16 x 64) and lse2; counters per split tile
+    void *d_ks_o = nullptr;
+    float *d_ks_lse = nullptr;
+    unsigned *d_ks_cnt = nullptr;
     // merged plan of the one-launch decomposition (strided-pass pairs, then band-pass pairs; entry,
     // entry-table and mask indices of the band part offset past the strided part's) and the per-slot
     // dependency counters [kLaunchSlots][kLseHeads + 1]; null when not built

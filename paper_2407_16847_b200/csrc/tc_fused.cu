@@ -875,12 +875,18 @@ struct SCfg {
     static constexpr int kInfo = 32;
     static constexpr int OFF_INFO = OFF_BAR + 2 * NB * 8;        // [2 groups][QS][kInfo] int2
     static constexpr int OFF_HDR = OFF_INFO + 2 * QS * kInfo * 8;  // [2 groups][QS] int4: unit (t, bh, j0, j1)
-    static constexpr int SMEM = OFF_HDR + 2 * QS * 16 + 16 + 1024;
+    static constexpr int OFF_HDR2 = OFF_HDR + 2 * QS * 16 + 16;     // [2 groups][QS] int: split field; [2] merge flags
+    // [2 groups][4 warps] int: split field of the warp's pending (deferred) epilogue, then [2][128] f32
+    // its rows' running maxima
+    static constexpr int OFF_PE = (OFF_HDR2 + 2 * QS * 4 + 2 * 4 + 15) / 16 * 16;
+    // the dynamic buffer starts 1024-byte aligned (no static shared memory; checked with a trap)
+    static constexpr int SMEM = OFF_PE + 32 + 2 * 128 * 4 + 8;
     static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 struct TUnit {
     int t, bh, j0, j1;
+    int split;      // split-K part: part | parts << 8 | split-tile index << 16; 0 = whole tile
 };
 
 __device__ __forceinline__ TUnit fetch_tunit(const DevAcsr &A, int BH, int v)
@@ -897,7 +903,7 @@ __device__ __forceinline__ TUnit fetch_tunit(const DevAcsr &A, int BH, int v)
         v -= ub;
     }
     const int4 x = A.t_info[k];
-    return TUnit{x.x, bh, x.y, x.z};
+    return TUnit{x.x, bh, x.y, x.z, x.w};
 }
 
 // key-tile index of the unit's entries, cached in a (uniformly executing) warp's registers
@@ -921,6 +927,9 @@ __device__ __forceinline__ int kv_at(const DevAcsr &A, const TUnit &un, const Kv
     return A.kv[j] & kKvMask;
 }
 
+// KS: the split-K unit list (long tiles in parts, merged by the last part); a separate instantiation
+// so the whole-tile kernel carries none of the merge code
+template <bool KS>
 __global__ void __launch_bounds__(kThreads, 1)
 mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const Params prm)
@@ -928,8 +937,8 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     using C = SCfg;
     constexpr int D = 64;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // No static shared memory precedes the dynamic buffer, so it starts 1024-byte aligned (checked;
-    // the launch still reserves 1 KB of slack).  Using smem_raw itself -- not an integer align-up --
+    // No static shared memory precedes the dynamic buffer, so it starts 1024-byte aligned (checked
+    // with a trap; SCfg reserves no slack).  Using smem_raw itself -- not an integer align-up --
     // keeps the shared state space visible to the compiler (LDS/STS, constant offsets).
     uint8_t *smem = smem_raw;
     if (threadIdx.x == 0 && (smem_u32(smem_raw) & 1023u) != 0u) __trap();
@@ -943,11 +952,11 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
     uint64_t *v_full = k_empty + C::KS, *v_empty = v_full + C::KS;
     uint64_t *s_full = v_empty + C::KS, *s_empty = s_full + 1, *p_full = s_empty + 1;
     uint64_t *pv_done = p_full + 1, *epi = pv_done + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_HDR + 2 * C::QS * 16);
     int2 *info = reinterpret_cast<int2 *>(smem + C::OFF_INFO) + g * C::QS * C::kInfo;   // [QS][kInfo]
     int4 *hdr = reinterpret_cast<int4 *>(smem + C::OFF_HDR) + g * C::QS;               // [QS]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_HDR + 2 * C::QS * 16);
     const DevAcsr &A = prm.A;
-    const int n_units = A.n_qt * prm.BH;
+    const int n_units = A.t_n * prm.BH;
 #ifdef SPLAT_FUSED_PROF
     const unsigned long long t_start = clock64();
 #endif
@@ -1012,7 +1021,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             int v = 0;
             if (lane == 0) v = (int)atomicAdd(prm.sched, 1ull);
             v = __shfl_sync(0xffffffffu, v, 0);
-            return v < n_units ? fetch_tunit(A, prm.BH, v) : TUnit{-1, 0, 0, 0};
+            return v < n_units ? fetch_tunit(A, prm.BH, v) : TUnit{-1, 0, 0, 0, 0};
         };
         TUnit nx = grab();
         KvRegs nkr;
@@ -1029,7 +1038,10 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             nx = grab();                      // next unit, fetched in the shadow of this one
             if (lane < un.j1 - un.j0 && lane < C::kInfo)
                 info[qi * C::kInfo + lane] = make_int2(A.kv_mask[un.j0 + lane], (int)A.qt_bits[un.j0 + lane]);
-            if (lane == 0) hdr[qi] = make_int4(un.t, un.bh, un.j0, un.j1);
+            if (lane == 0) {
+                hdr[qi] = make_int4(un.t, un.bh, un.j0, un.j1);
+                if (KS) reinterpret_cast<int *>(smem + C::OFF_HDR2)[g * C::QS + qi] = un.split;   // split field
+            }
             // header + table: each lane's arrival releases its own writes; lane 0's carries the Q bytes
             if (lane == 0) {
                 // the tile's two 64-row segments (row classes, plan.cpp): rows 0-63 and 64-127
@@ -1176,7 +1188,10 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         uint8_t *ostage = gs + C::OFF_O;
         const uint32_t ostage_u = smem_u32(ostage);
         uint32_t s_cnt = 0, e_cnt = 0;
-        auto epilogue = [&](float l, int t, int bh) {
+        // sp: split-K part of a long tile (0 = whole tile): the part publishes its normalised partial O
+        // (bf16) and lse2 = m + log2(l) to the launch slot's scratch; the last part of the tile to
+        // arrive merges all parts in part order (deterministic) and stores the tile
+        auto epilogue = [&](float l, float m, int t, int bh, int sp) {
             FWAIT(2, epi, e_cnt & 1);
             ++e_cnt;
             tc_fence_after();
@@ -1189,6 +1204,57 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             uint32_t w[32];
 #pragma unroll
             for (int x = 0; x < 32; ++x) w[x] = inv == 0.f ? 0u : pack_bf16(o[2 * x] * inv, o[2 * x + 1] * inv);
+            if (KS && sp != 0) {
+                const int part = sp & 0xFF, np = (sp >> 8) & 0xFF, sid = sp >> 16;
+                const size_t tix = (size_t)bh * A.n_ksplit + sid, base = tix * A.ks_pmax;
+                uint4 *dst = reinterpret_cast<uint4 *>(A.ks_o) + ((base + part) * 128 + r) * 8;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dst[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+                A.ks_lse[(base + part) * 128 + r] = l > 0.f ? m + __log2f(l) : -INFINITY;
+                named_bar(1 + g, 128);
+                if (store_leader) {
+                    __threadfence();
+                    reinterpret_cast<int *>(smem + C::OFF_HDR2)[2 * C::QS + g] =
+                        atomicAdd(A.ks_cnt + tix, 1u) == (unsigned)(np - 1) ? 1 : 0;
+                }
+                named_bar(1 + g, 128);
+                if (!reinterpret_cast<const int *>(smem + C::OFF_HDR2)[2 * C::QS + g]) {
+                    tc_fence_before();
+                    return;
+                }
+                __threadfence();
+                float M = -INFINITY;
+                for (int q = 0; q < np; ++q) M = fmaxf(M, __ldcg(A.ks_lse + (base + q) * 128 + r));
+                // two halves of 32 columns (register budget): weights recomputed per half
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float acc[32];
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) acc[x] = 0.f;
+                    float den = 0.f;
+                    for (int q = 0; q < np; ++q) {
+                        const float lq = __ldcg(A.ks_lse + (base + q) * 128 + r);
+                        const float aq = lq == -INFINITY ? 0.f : ex2(lq - M);
+                        den += aq;
+                        const uint4 *src = reinterpret_cast<const uint4 *>(A.ks_o) + ((base + q) * 128 + r) * 8 + 4 * h;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint4 u4 = __ldcg(src + c);
+                            const uint32_t uu[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+                            for (int y = 0; y < 4; ++y) {
+                                acc[8 * c + 2 * y] += aq * __uint_as_float(uu[y] << 16);
+                                acc[8 * c + 2 * y + 1] += aq * __uint_as_float(uu[y] & 0xffff0000u);
+                            }
+                        }
+                    }
+                    const float id = den > 0.f ? 1.f / den : 0.f;
+#pragma unroll
+                    for (int x = 0; x < 16; ++x)
+                        w[16 * h + x] = den > 0.f ? pack_bf16(acc[2 * x] * id, acc[2 * x + 1] * id) : 0u;
+                }
+                if (store_leader) A.ks_cnt[tix] = 0u;      // for the next launch on this slot
+            }
             if (store_leader) bulk_wait_read0();      // the stage's previous store has read it
             named_bar(1 + g, 128);
 #pragma unroll
@@ -1209,6 +1275,9 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         bool pe_on = false;          // deferred epilogue of the previous unit
         float pe_l = 0.f;
         int pe_t = 0, pe_bh = 0;
+        // the pending epilogue's split field and row maxima live in SMEM (register budget)
+        int *pe_sp_s = reinterpret_cast<int *>(smem + C::OFF_PE) + g * 4 + quad;    // this warp's copy
+        float *pe_m_s = reinterpret_cast<float *>(smem + C::OFF_PE + 32) + g * 128 + r;
         // the unit's entry table (mask id, bits) of Q slot qs, entry index i = j - j0
         int qs = 0;
         uint32_t qph = 0;
@@ -1234,7 +1303,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             FWAIT(3, &q_full[slot], qph);            // the unit's header and entry table are published
             const int4 h4 = hdr[slot];
             if (h4.x < 0) break;
-            const TUnit un{h4.x, h4.y, h4.z, h4.w};
+            const TUnit un{h4.x, h4.y, h4.z, h4.w, KS ? reinterpret_cast<const int *>(smem + C::OFF_HDR2)[g * C::QS + slot] : 0};
             if (++qs == C::QS) { qs = 0; qph ^= 1; }
             const int j0 = un.j0, j1 = un.j1;
 #define SPLAT_NEXT_UNIT_PREFETCH()                                                                      \
@@ -1247,8 +1316,8 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             bool first = true;
             if (j0 == j1) {
                 SPLAT_NEXT_UNIT_PREFETCH();
-                if (pe_on) { epilogue(pe_l, pe_t, pe_bh); pe_on = false; }
-                epilogue(0.f, un.t, un.bh);
+                if (pe_on) { epilogue(pe_l, KS ? *pe_m_s : 0.f, pe_t, pe_bh, KS ? *pe_sp_s : 0); pe_on = false; }
+                epilogue(0.f, 0.f, un.t, un.bh, 0);
                 mbar_arrive(&q_empty[slot]);
                 continue;
             }
@@ -1318,7 +1387,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                 }
                 if (store_leader) TRACE(2 + g, 13);
                 if (pe_on) {             // the previous unit's epilogue (first tile of a unit only)
-                    epilogue(pe_l, pe_t, pe_bh);
+                    epilogue(pe_l, KS ? *pe_m_s : 0.f, pe_t, pe_bh, KS ? *pe_sp_s : 0);
                     pe_on = false;
                 }
                 if (s_cnt > 1) {
@@ -1357,10 +1426,12 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
             mbar_arrive(&q_empty[slot]);   // header + entry table of this slot consumed (every thread)
             pe_on = true;
             pe_l = l_run;
+            if (KS) *pe_m_s = m_run;
             pe_t = un.t;
             pe_bh = un.bh;
+            if (KS) *pe_sp_s = un.split;  // every lane of the warp writes the same value
         }
-        if (pe_on) epilogue(pe_l, pe_t, pe_bh);
+        if (pe_on) epilogue(pe_l, KS ? *pe_m_s : 0.f, pe_t, pe_bh, KS ? *pe_sp_s : 0);
         if (store_leader) bulk_wait0();
     }
     __syncthreads();
@@ -1489,7 +1560,9 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
     int dev = 0;
     cudaGetDevice(&dev);
     if (!attr_set[dev & 63]) {
-        cudaError_t e = cudaFuncSetAttribute(mhsa_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SCfg::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(mhsa_split_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCfg::SMEM);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(mhsa_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SCfg::SMEM);
         if (e != cudaSuccess) return e;
         attr_set[dev & 63] = true;
     }
@@ -1503,10 +1576,25 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
     p.dbg = dbg;
     p.sched = A.sched;
     if (!p.sched) return cudaErrorInvalidValue;
-    const long long units = (long long)A.n_qt * BH;
+    p.A.n_ksplit = 0;
+    if (A.n_ksplit > 0 && A.t_n_ks > 0) {
+        // split-K list when the longest whole tile would outlast a tile group's average share of the
+        // work (few heads per GPU, e.g. a rank of a sharded job): DESIGN.md section 8
+        const double avg = (double)BH * A.t_entries / (2.0 * num_sms(dev));
+        if ((double)A.t_max_len > avg && BH <= kSplitHeads) {     // the slot's scratch holds kSplitHeads heads
+            if (!A.ks_o || !A.ks_lse || !A.ks_cnt) return cudaErrorInvalidValue;
+            p.A.n_ksplit = A.n_ksplit;
+            p.A.t_info = A.t_info_ks;
+            p.A.t_n = A.t_n_ks;
+            p.A.t_n_buckets = A.t_n_buckets_ks;
+            for (int b = 0; b <= A.t_n_buckets_ks && b <= kMaxBuckets; ++b) p.A.t_bucket_start[b] = A.t_bucket_start_ks[b];
+        }
+    }
+    const long long units = (long long)p.A.t_n * BH;
     const long long ctas = (units + 1) / 2;
     const int grid = (int)(ctas < num_sms(dev) ? ctas : num_sms(dev));
-    mhsa_split_kernel<<<grid, kThreads, SCfg::SMEM, st>>>(mq, mk, mv, mo, p);
+    if (p.A.n_ksplit > 0) mhsa_split_kernel<true><<<grid, kThreads, SCfg::SMEM, st>>>(mq, mk, mv, mo, p);
+    else mhsa_split_kernel<false><<<grid, kThreads, SCfg::SMEM, st>>>(mq, mk, mv, mo, p);
     return cudaGetLastError();
 }
 

@@ -578,6 +578,7 @@ extern "C" int splat_debug_prof64(unsigned long long *out)
 cudaError_t launch_mhsa64(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, float scale,
                           void *O, cudaStream_t st)
 {
+    if (A.n_ksplit > 0) return cudaErrorNotSupported;   // split-K units: the split kernel only
     CUtensorMap mq, mk, mv;
     if (!make_map(&mq, Q, BH, A.n, 64) || !make_map(&mk, K, BH, A.n, 64) || !make_map(&mv, V, BH, A.n, 64))
         return cudaErrorInvalidValue;

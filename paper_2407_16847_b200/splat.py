@@ -27,7 +27,7 @@ KINDS = {"window": 0, "blocked": 1, "strided": 2, "dilated": 3, "global_local": 
 
 # every symbol include/splat.h declares (tests check the library exports them all)
 EXPORTS = ("splat_acsr_build", "splat_acsr_info", "splat_acsr_copy_meta", "splat_plan_info",
-           "splat_plan_copy", "splat_plan_split_info", "splat_plan_sizes", "splat_plan_split_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
+           "splat_plan_copy", "splat_plan_split_info", "splat_plan_sizes", "splat_plan_split_copy", "splat_plan_ksplit_copy", "splat_acsr_destroy", "splat_rsddmm", "splat_sparse_softmax", "splat_rspmm",
            "splat_sparse_mhsa", "splat_sparse_mhsa_host", "splat_acsr_from_mask", "splat_poset_tile", "splat_naive_tile",
            "splat_tiling_cost_eval", "splat_acsr_transpose", "splat_transpose_values", "splat_rspmm_cc",
            "splat_layout_choice", "splat_flops", "splat_last_launch_count", "splat_device_alloc_count",
@@ -79,6 +79,7 @@ def lib():
         L.splat_plan_sizes.argtypes = [vp, i32]
         L.splat_plan_sizes.restype = i64
         L.splat_plan_split_copy.argtypes = [vp, vp, vp, vp, vp]
+        L.splat_plan_ksplit_copy.argtypes = [vp, vp]
         L.splat_acsr_destroy.argtypes = [vp]
         L.splat_rsddmm.argtypes = [vp, vp, vp, C.c_int, i32, i32, i32, f32, vp, vp]
         L.splat_sparse_softmax.argtypes = [vp, vp, vp, C.c_int, i32, i32, vp]
@@ -178,6 +179,14 @@ class Acsr:
         masks = torch.zeros((max(nm, 1), 128, 4), dtype=torch.int64).to(torch.int32)
         _check(L.splat_plan_split_copy(self.handle, units.data_ptr(), kv.data_ptr(), mid.data_ptr(), masks.data_ptr()))
         return units, kv[:ne], mid[:ne], masks[:nm]
+
+    def ksplit_units(self):
+        """The split-K unit list [n][4] (tile, j0, j1, part | parts << 8 | sid << 16); empty if none."""
+        L = lib()
+        n = L.splat_plan_sizes(self.handle, 3)
+        units = torch.zeros((max(n, 1), 4), dtype=torch.int32)
+        _check(L.splat_plan_ksplit_copy(self.handle, units.data_ptr()))
+        return units[:n]
 
     def plan_copy(self):
         _, _, nq, ne = self.plan_info()

@@ -444,3 +444,29 @@ def test_residue_head_chunks_and_repeat():
     for bh, o in zip(heads, refs):
         o = o[0] if isinstance(o, tuple) else o
         assert maxabs(outs[0][bh].float(), o) <= TOL_BF16, bh
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["longformer", "bigbird"])
+def test_split_k_long_tiles_few_heads(name):
+    # Few heads per call (a rank of a sharded job): the d = 64 kernel takes the split-K unit list --
+    # the global-row tiles run as several parts whose partial softmax results the last part merges
+    # (DESIGN.md section 8).  Full-size mask, 3 heads, every row against the oracle; repeated calls
+    # are bitwise identical (the merge sums the parts in part order, whichever part merges).
+    base = CONFIG_BY_NAME[name]
+    cfg = Config(name + "_ks", base.pattern, 1, 3, base.d, base.dtype, 217)
+    q, k, v = make_qkv(cfg)
+    a = S.Acsr(cfg.pattern, device=DEV)
+    Q, K, V = dev(q), dev(k), dev(v)
+    outs = []
+    for _ in range(2):
+        Of = torch.empty_like(Q)
+        S.splat_sparse_mhsa(a, Q, K, V, Of, cfg.scale)
+        torch.cuda.synchronize()
+        outs.append(Of.view(cfg.BH, cfg.N, cfg.d).cpu())
+    assert torch.equal(outs[0], outs[1])
+    shp = (cfg.BH, cfg.N, cfg.d)
+    refs = oracle_heads(cfg.pattern, q.view(shp), k.view(shp), v.view(shp), cfg.scale, range(cfg.BH))
+    for bh, o in enumerate(refs):
+        o = o[0] if isinstance(o, tuple) else o
+        assert maxabs(outs[0][bh].float(), o) <= TOL_BF16, bh

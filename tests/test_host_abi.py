@@ -251,3 +251,41 @@ def test_split_plan_covers_mask_exactly_once(p):
     assert np.array_equal(cover, O.mask(p).astype(np.int32)), p
     if p.kind == "bigbird" and p.seq_len == 4096:
         assert rc == 1 and ne == 154          # row classes: the two global blocks share a tile
+
+
+@pytest.mark.parametrize("p", [Pattern("global_local", 4096, lo=256, hi=256, n_global=32),
+                               Pattern("bigbird", 4096, block=64, radius=1),
+                               Pattern("global_local", 2000, lo=64, hi=64, n_global=40)], ids=lambda p: f"{p.kind}{p.seq_len}")
+def test_ksplit_units_partition_long_tiles(p):
+    # The split-K list: every whole-tile unit with more than 8 entries becomes
+    # parts with contiguous entry ranges that partition it (each <= 8 entries, part order = entry
+    # order, one split-tile index per tile); the other units are unchanged -- so the list still
+    # covers the oracle mask exactly once.
+    a = S.Acsr(p, device=-1)
+    units, kv, mid, masks = a.split_plan_copy()
+    ks = a.ksplit_units()
+    whole = {(int(t), int(j0), int(j1)) for t, j0, j1, _ in units.tolist()}
+    long_tiles = {u for u in whole if u[2] - u[1] > 8}
+    assert long_tiles, "a global-row tile is long"
+    assert ks.shape[0] > 0
+    parts = {}
+    for t, j0, j1, sp in ks.tolist():
+        if sp == 0:
+            assert (t, j0, j1) in whole and j1 - j0 <= 8
+            continue
+        part, npart, sid = sp & 0xFF, (sp >> 8) & 0xFF, sp >> 16
+        assert 0 < j1 - j0 <= 8 and part < npart
+        parts.setdefault((t, sid, npart), []).append((part, j0, j1))
+    assert len(parts) == len(long_tiles)
+    sids = set()
+    for (t, sid, npart), lst in parts.items():
+        lst.sort()
+        assert [q for q, _, _ in lst] == list(range(npart))
+        for (_, _, e1), (_, s0, _) in zip(lst, lst[1:]):
+            assert e1 == s0                      # contiguous
+        assert (t, lst[0][1], lst[-1][2]) in long_tiles
+        sids.add(sid)
+    assert sids == set(range(len(parts)))
+    # whole units that are not long appear unchanged
+    short = {(int(t), int(j0), int(j1)) for t, j0, j1, sp in ks.tolist() if sp == 0}
+    assert short == whole - long_tiles
