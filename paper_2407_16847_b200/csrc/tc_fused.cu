@@ -1577,7 +1577,8 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
     p.sched = A.sched;
     if (!p.sched) return cudaErrorInvalidValue;
     p.A.n_ksplit = 0;
-    if (A.n_ksplit > 0 && A.t_n_ks > 0) {
+    static const int no_ks = diag_env("SPLAT_NO_KSPLIT");      // diagnostics build only
+    if (A.n_ksplit > 0 && A.t_n_ks > 0 && !no_ks) {
         // split-K list when the longest whole tile would outlast a tile group's average share of the
         // work (few heads per GPU, e.g. a rank of a sharded job): DESIGN.md section 8
         const double avg = (double)BH * A.t_entries / (2.0 * num_sms(dev));

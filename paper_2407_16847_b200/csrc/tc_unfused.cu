@@ -408,8 +408,14 @@ template <int D>
 struct CfgP {
     static constexpr int kChunks = D / 64;
     static constexpr int kTileBytes = kChunks * kSub;                 // V tile
-    static constexpr int KS = D == 64 ? 3 : 2;                        // V ring
-    static constexpr int NSTG = 4;                                    // P staging ring
+#ifndef SPLAT_SPMM_KS64
+#define SPLAT_SPMM_KS64 3
+#endif
+#ifndef SPLAT_SPMM_NSTG
+#define SPLAT_SPMM_NSTG 4
+#endif
+    static constexpr int KS = D == 64 ? SPLAT_SPMM_KS64 : 2;          // V ring
+    static constexpr int NSTG = D == 64 ? SPLAT_SPMM_NSTG : 4;        // P staging ring
     static constexpr int OFF_V = 0;
     static constexpr int OFF_STG = OFF_V + KS * kTileBytes;           // [NSTG][128 rows][kStgRow]
     // [NSTG][128 rows][16 column groups of 8] u16: low byte = staged element index of the group's
