@@ -268,12 +268,20 @@ void build_plan(splat_acsr_s &a)
                 cj0.push_back((int32_t)(P.kv.size() + ckv.size()));
                 for (int w = 0; w < W; ++w)
                     u[w] = foot[(size_t)ca[t] * W + w] | (cb[t] < nseg ? foot[(size_t)cb[t] * W + w] : 0ull);
+                auto live = [&](int j) { return j < nb && ((u[j >> 6] >> (j & 63)) & 1ull); };
+                // composite windows: two half-live windows (one live 64-column block each -- BigBird's
+                // first and last key blocks) become one window of two 64-row K / V boxes (kCompBit,
+                // blocks a | b << 12): one plan entry instead of two
+                std::vector<int32_t> half;
                 for (int j = 0; j < nb;) {
-                    if (!((u[j >> 6] >> (j & 63)) & 1ull)) { ++j; continue; }
+                    if (!live(j)) { ++j; continue; }
                     const int kv = j - j % P.kv_align;
-                    ckv.push_back(kv);
+                    if (bn == 2 * kKvUnit && live(kv) != live(kv + 1)) half.push_back(live(kv) ? kv : kv + 1);
+                    else ckv.push_back(kv);
                     j = kv + bn / kKvUnit;
                 }
+                for (size_t h = 0; h + 1 < half.size(); h += 2) ckv.push_back(half[h] | (half[h + 1] << 12) | kCompBit);
+                if (half.size() & 1) ckv.push_back(half.back() - half.back() % P.kv_align);
                 cj1.push_back((int32_t)(P.kv.size() + ckv.size()));
             }
             if ((long long)ckv.size() < (long long)P.n_entries) {
@@ -286,10 +294,12 @@ void build_plan(splat_acsr_s &a)
                         rows[r] = sg < nseg && i < N ? i : -1;
                     }
                     for (int e = cj0[t]; e < cj1[t]; ++e) {
-                        const int kv = ckv[e - P.n_entries];
-                        const int c0 = kv * kKvUnit;
+                        const int32_t ent = ckv[e - P.n_entries];
+                        const bool comp = (ent & kCompBit) != 0;
+                        // the window's two 64-column halves: key blocks ba (columns 0-63), bb (64-127)
+                        const int ba = comp ? (ent & 0xFFF) : ent, bb = comp ? ((ent >> 12) & 0xFFF) : ent + 1;
                         std::fill(mbuf.begin(), mbuf.end(), 0u);
-                        bool full_all = c0 + bn <= N;
+                        bool full_all = (ba + 1) * kKvUnit <= N && (bb + 1) * kKvUnit <= N;
                         for (int r = 0; r < 128; ++r) {
                             const int i = rows[r];
                             if (i < 0) continue;
@@ -297,11 +307,16 @@ void build_plan(splat_acsr_s &a)
                             for (int q = 0; q < a.nseg_h[i]; ++q) {
                                 const int start = rs[4 * q], step = rs[4 * q + 1], count = rs[4 * q + 2];
                                 const int last = start + step * (count - 1);
-                                const int lo = std::max(start, c0), hi = std::min(last, c0 + bn - 1);
-                                if (lo > hi) continue;
-                                const int first = start + ((lo - start + step - 1) / step) * step;
-                                for (int c = first; c <= hi; c += step)
-                                    mbuf[4 * r + ((c - c0) >> 5)] |= 1u << ((c - c0) & 31);
+                                for (int hf = 0; hf < 2; ++hf) {
+                                    const int k0 = (hf ? bb : ba) * kKvUnit;      // keys [k0, k0 + 64) -> columns 64 hf + ...
+                                    const int lo = std::max(start, k0), hi = std::min(last, k0 + kKvUnit - 1);
+                                    if (lo > hi) continue;
+                                    const int first = start + ((lo - start + step - 1) / step) * step;
+                                    for (int c = first; c <= hi; c += step) {
+                                        const int pcol = kKvUnit * hf + (c - k0);
+                                        mbuf[4 * r + (pcol >> 5)] |= 1u << (pcol & 31);
+                                    }
+                                }
                             }
                             for (int w = 0; w < 4; ++w) full_all &= mbuf[4 * r + w] == ~0u;
                         }
@@ -332,7 +347,7 @@ void build_plan(splat_acsr_s &a)
                                     if (all) bits |= 1u << (16 + 4 * q + w);
                                 }
                         }
-                        P.kv.push_back(kv | (full_all ? 0 : kPartialBit));
+                        P.kv.push_back(ent | (full_all ? 0 : kPartialBit));
                         P.kv_mask.push_back(id);
                         P.qt_bits.push_back(bits);
                     }

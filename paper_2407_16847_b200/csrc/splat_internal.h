@@ -25,6 +25,8 @@ constexpr int kBN = 128;
 constexpr int kKvUnit = 64;          // plan entries: key window [64 kv, 64 kv + kBN)
 constexpr int kPartialBit = 1 << 24;
 constexpr int kKvMask = (1 << 24) - 1;
+// classed (split-kernel) entries only: a composite window of two 64-column key blocks a | b << 12
+constexpr int kCompBit = 1 << 25;
 
 struct Seg {
     int32_t start, step, count;

@@ -916,7 +916,7 @@ __device__ __forceinline__ void load_kv(const DevAcsr &A, const TUnit &un, int l
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         const int j = un.j0 + lane + 32 * k;
-        kr.r[k] = j < un.j1 ? (A.kv[j] & kKvMask) : 0;
+        kr.r[k] = j < un.j1 ? (A.kv[j] & (kKvMask | kCompBit)) : 0;
     }
 }
 
@@ -924,7 +924,13 @@ __device__ __forceinline__ int kv_at(const DevAcsr &A, const TUnit &un, const Kv
 {
     const int i = j - un.j0;
     if (i < 64) return __shfl_sync(0xffffffffu, i < 32 ? kr.r[0] : kr.r[1], i & 31);
-    return A.kv[j] & kKvMask;
+    return A.kv[j] & (kKvMask | kCompBit);
+}
+
+// The two 64-row key blocks of a split-kernel window: kv and kv + 1, or a composite's a and b
+__device__ __forceinline__ int2 kv_blocks(int ent)
+{
+    return (ent & kCompBit) ? make_int2(ent & 0xFFF, (ent >> 12) & 0xFFF) : make_int2(ent, ent + 1);
 }
 
 // KS: the split-K unit list (long tiles in parts, merged by the last part); a separate instantiation
@@ -932,7 +938,8 @@ __device__ __forceinline__ int kv_at(const DevAcsr &A, const TUnit &un, const Kv
 template <bool KS>
 __global__ void __launch_bounds__(kThreads, 1)
 mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const Params prm)
+                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                  const __grid_constant__ CUtensorMap tmK64, const __grid_constant__ CUtensorMap tmV64, const Params prm)
 {
     using C = SCfg;
     constexpr int D = 64;
@@ -983,6 +990,7 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
         }
         fence_mbar_init();
         tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmO);
+        tma_prefetch(&tmK64); tma_prefetch(&tmV64);
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
@@ -1006,7 +1014,13 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                     mbar_arrive(&v_full[vi]);
                 } else {
                     mbar_expect_tx(&v_full[vi], C::TB);
-                    tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * kKvUnit, pv_bh);
+                    if (pv_kv & kCompBit) {                    // composite window: two 64-row boxes
+                        const int2 vb = kv_blocks(pv_kv);
+                        tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV64, &v_full[vi], 0, vb.x * kKvUnit, pv_bh);
+                        tma_load_3d(gs + C::OFF_V + vi * C::TB + C::TB / 2, &tmV64, &v_full[vi], 0, vb.y * kKvUnit, pv_bh);
+                    } else {
+                        tma_load_3d(gs + C::OFF_V + vi * C::TB, &tmV, &v_full[vi], 0, pv_kv * kKvUnit, pv_bh);
+                    }
                 }
             }
             ++vc;
@@ -1065,7 +1079,13 @@ mhsa_split_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant
                         mbar_arrive(&k_full[ki]);
                     } else {
                         mbar_expect_tx(&k_full[ki], C::TB);
-                        tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * kKvUnit, un.bh);
+                        if (kv & kCompBit) {
+                            const int2 kb = kv_blocks(kv);
+                            tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK64, &k_full[ki], 0, kb.x * kKvUnit, un.bh);
+                            tma_load_3d(gs + C::OFF_K + ki * C::TB + C::TB / 2, &tmK64, &k_full[ki], 0, kb.y * kKvUnit, un.bh);
+                        } else {
+                            tma_load_3d(gs + C::OFF_K + ki * C::TB, &tmK, &k_full[ki], 0, kv * kKvUnit, un.bh);
+                        }
                     }
                 }
                 ++kc;
@@ -1551,10 +1571,11 @@ cudaError_t launch_d(const DevAcsr &A, const void *Q, const void *K, const void 
 cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const void *V, int BH, float scale,
                            void *O, cudaStream_t st)
 {
-    CUtensorMap mq, mk, mv, mo;
-    // Q and O move as two 64-row segments per tile (row classes), K and V as 128-row key windows
+    CUtensorMap mq, mk, mv, mo, mk64, mv64;
+    // Q and O move as two 64-row segments per tile (row classes), K and V as 128-row key windows, or as
+    // two 64-row key blocks for a composite window (two distant half-live blocks, plan.cpp)
     if (!make_map(&mq, Q, BH, A.n, 64, 64) || !make_map(&mk, K, BH, A.n, 64) || !make_map(&mv, V, BH, A.n, 64) ||
-        !make_map(&mo, O, BH, A.n, 64, 64))
+        !make_map(&mo, O, BH, A.n, 64, 64) || !make_map(&mk64, K, BH, A.n, 64, 64) || !make_map(&mv64, V, BH, A.n, 64, 64))
         return cudaErrorInvalidValue;
     static bool attr_set[64] = {false};
     int dev = 0;
@@ -1594,8 +1615,8 @@ cudaError_t launch_split64(const DevAcsr &A, const void *Q, const void *K, const
     const long long units = (long long)p.A.t_n * BH;
     const long long ctas = (units + 1) / 2;
     const int grid = (int)(ctas < num_sms(dev) ? ctas : num_sms(dev));
-    if (p.A.n_ksplit > 0) mhsa_split_kernel<true><<<grid, kThreads, SCfg::SMEM, st>>>(mq, mk, mv, mo, p);
-    else mhsa_split_kernel<false><<<grid, kThreads, SCfg::SMEM, st>>>(mq, mk, mv, mo, p);
+    if (p.A.n_ksplit > 0) mhsa_split_kernel<true><<<grid, kThreads, SCfg::SMEM, st>>>(mq, mk, mv, mo, mk64, mv64, p);
+    else mhsa_split_kernel<false><<<grid, kThreads, SCfg::SMEM, st>>>(mq, mk, mv, mo, mk64, mv64, p);
     return cudaGetLastError();
 }
 

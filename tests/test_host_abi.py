@@ -230,11 +230,19 @@ def split_plan_coverage(p):
         rows = np.array([s * 64 + r if s < nseg and s * 64 + r < N else -1 for s in (sa, sb) for r in range(64)])
         ok = rows >= 0
         for e in range(j0, j1):
-            c0 = (int(kv[e]) & 0xFFFFFF) * 64
-            cols = np.arange(c0, min(N, c0 + 128))
-            if (int(kv[e]) >> 24) & 1:
+            ent = int(kv[e])
+            if (ent >> 25) & 1:                      # composite window: key blocks a (cols 0-63), b (64-127)
+                ba, bb = ent & 0xFFF, (ent >> 12) & 0xFFF
+            else:
+                ba = ent & 0xFFFFFF
+                bb = ba + 1
+            pos = np.arange(128)
+            keys = np.where(pos < 64, ba * 64 + pos, bb * 64 + pos - 64)
+            keep = keys < N
+            pos, cols = pos[keep], keys[keep]
+            if (ent >> 24) & 1:
                 w = masks[int(mid[e])]                                   # [128, 4]
-                bits = (w[:, (cols - c0) >> 5] >> ((cols - c0) & 31)) & 1
+                bits = (w[:, pos >> 5] >> (pos & 31)) & 1
             else:
                 bits = np.ones((128, len(cols)), dtype=np.int64)
             cover[np.ix_(rows[ok], cols)] += bits[ok].astype(np.int32)
@@ -250,7 +258,7 @@ def test_split_plan_covers_mask_exactly_once(p):
     cover, rc, ne = split_plan_coverage(p)
     assert np.array_equal(cover, O.mask(p).astype(np.int32)), p
     if p.kind == "bigbird" and p.seq_len == 4096:
-        assert rc == 1 and ne == 154          # row classes: the two global blocks share a tile
+        assert rc == 1 and ne == 125          # row classes (global blocks share a tile) + composite windows
 
 
 @pytest.mark.parametrize("p", [Pattern("global_local", 4096, lo=256, hi=256, n_global=32),
