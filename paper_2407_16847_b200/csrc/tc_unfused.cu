@@ -297,7 +297,6 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const int eg = (warp - 2) >> 2, quad = warp & 3, r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         int2 *tq = reinterpret_cast<int2 *>(smem + C::OFF_TQ) + eg * 2 * 128 * 4;
-        long long *tbase = reinterpret_cast<long long *>(smem + C::OFF_TBASE) + eg * 2;
         const uint32_t below = (1u << lane) - 1u, lanebit = 1u << lane;
         float *const Sg = prm.S;
         const float scale = prm.scale;
@@ -311,6 +310,8 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             i += (uint32_t)(e1 - e0);
             if (e >= e1) continue;
             const int row = t * 128 + r;
+            // element offset of this (b, h) slice in S: every row offset of the slice is relative to it
+            const long long hbase = (long long)bh * (prm.pass ? prm.nat_nnz : A.nnz);
             RowRuns R;
             PSPAN_BEGIN(t_row);
             const long long rowoff = row_offset(prm, bh, t, r, R);
@@ -325,16 +326,12 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 if (partial) m4 = A.masks[(size_t)A.kv_mask[e] * 128 + r];
                 if (row >= A.n) m4 = make_uint4(0u, 0u, 0u, 0u);
                 // Thread r publishes, per key quad q, the offset of row r's first non-zero in the
-                // quad's 32 columns (relative to the tile base = row 0's first non-zero; a tile
-                // spans < 2^31 entries) and the row mask word: one LDS.64 per stored row.
-                const long long o0 = row < A.n ? rowoff + rank_before(R, c0) : 0ll;
-                if (r == 0) tbase[tb] = o0;
-                const long long t0 = __shfl_sync(0xffffffffu, o0, 0);     // valid in warp 0 only
+                // quad's 32 columns (relative to the (b, h) slice base, < 2^32 entries per head) and the
+                // row mask word: one LDS.64 per stored row.
+                const long long o0 = row < A.n ? rowoff + rank_before(R, c0) : hbase;
                 int2 *dst = tq + (tb * 128 + r) * 4;
                 const int p1 = __popc(m4.x), p2 = p1 + __popc(m4.y), p3 = p2 + __popc(m4.z);
-                (void)t0;
-                wg_sync(1 + eg);          // tbase of this buffer published (row 0 lives in warp quad 0)
-                const int rel = (int)(o0 - tbase[tb]);
+                const int rel = (int)(uint32_t)(o0 - hbase);
                 dst[0] = make_int2(rel, (int)m4.x);
                 dst[1] = make_int2(rel + p1, (int)m4.y);
                 dst[2] = make_int2(rel + p2, (int)m4.z);
@@ -343,7 +340,7 @@ rsddmm_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 PSPAN_END(6, t_meta);
                 PWAIT(5, &s_full[eg], k & 1);
                 tc_fence_after();
-                const unsigned long long baddr = reinterpret_cast<unsigned long long>(Sg + tbase[tb]);
+                const unsigned long long baddr = reinterpret_cast<unsigned long long>(Sg + hbase);
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     float v[32];
