@@ -633,6 +633,12 @@ splat_status create_call_resources(splat_acsr_s *a)
         e = cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t *>(&a->slots[i].ev), cudaEventDisableTiming);
     for (int i = 0; i < 3 && e == cudaSuccess; ++i)
         e = cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t *>(&a->hs[i]), cudaStreamNonBlocking);
+    if (e == cudaSuccess && a->plan.n_ksplit > 0 &&
+        (size_t)kLaunchSlots * kSplitHeads * a->plan.n_ksplit * a->plan.ksplit_pmax * 128 * (64 * 2 + 4) > kSplitScratchMax) {
+        // too many long tiles for a bounded scratch: the launches keep the whole-tile list
+        a->plan.n_ksplit = 0;
+        a->plan.t_info_ks.clear();
+    }
     if (e == cudaSuccess && a->plan.n_ksplit > 0) {
         // split-K partial results of the d = 64 fused kernel, per launch slot (bf16 O + lse2 per part
         // and row, one counter per split tile), zeroed once: the merging part resets its counter

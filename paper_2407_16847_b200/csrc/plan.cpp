@@ -376,10 +376,15 @@ void build_plan(splat_acsr_s &a)
             std::vector<int32_t> ut, uj0, uj1, usp;
             n_split = 0;
             pmax = 0;
+            // only outliers are split: tiles longer than kSplitMax AND twice the mean (the global-row
+            // tiles; a window pattern whose tiles are all long -- Mistral -- gains nothing from parts)
+            long long tot = 0;
+            for (size_t t = 0; t < seg_a.size(); ++t) tot += tj1[t] - tj0[t];
+            const double mean = seg_a.empty() ? 0.0 : (double)tot / (double)seg_a.size();
             for (size_t t = 0; t < seg_a.size(); ++t) {
                 const int32_t tt = P.row_classes ? (seg_a[t] | (seg_b[t] << 16)) : (int32_t)t;
                 const int n = tj1[t] - tj0[t];
-                if (ksplit && n > kSplitMax) {
+                if (ksplit && n > kSplitMax && n > 2.0 * mean) {
                     const int np = std::min((n + kSplitMax - 1) / kSplitMax, kSplitPartsMax);
                     for (int q = 0; q < np; ++q) {
                         ut.push_back(tt);
@@ -426,6 +431,7 @@ void build_plan(splat_acsr_s &a)
         for (size_t k = 0; k < P.t_info.size(); k += 4) P.t_max_len = std::max(P.t_max_len, P.t_info[k + 2] - P.t_info[k + 1]);
         if (ablate == 0 && P.t_max_len > kSplitMax && (int)P.t_bucket_start.size() <= kMaxBuckets + 1) {
             emit(true, P.t_info_ks, P.t_bucket_start_ks, P.t_n_buckets_ks, P.n_ksplit, P.ksplit_pmax);
+            if (P.n_ksplit == 0) P.t_info_ks.clear();
         } else {
             P.t_info_ks.clear();
             P.n_ksplit = 0;

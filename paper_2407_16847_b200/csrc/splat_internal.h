@@ -218,6 +218,7 @@ constexpr int kLseHeads = 64;
 constexpr int kSplitMax = 8;
 constexpr int kSplitPartsMax = 16;
 constexpr int kSplitHeads = 128;
+constexpr size_t kSplitScratchMax = (size_t)256 << 20;   // per handle (all launch slots)
 
 struct LaunchSlot {
     std::mutex mu;
