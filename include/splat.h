@@ -179,8 +179,10 @@ splat_status splat_plan_split_info(splat_acsr a, int32_t *row_classes, int32_t *
 /* Inspection of the split kernel's plan (host copies, synchronous): splat_plan_sizes(a, 0) units
  * per (b, h), (a, 1) entries (natural ones first, then the row-class ones), (a, 2) masks;
  * splat_plan_split_copy copies units int32 [n][4] (tile -- or segments a | b << 16 when
- * row_classes -- , j0, j1, 0), kv int32 [entries] (window start / 64 | PARTIAL bit 24), mask_id
- * int32 [entries] (-1 = FULL) and masks uint32 [n_masks][128 rows][4] (column bits of the window). */
+ * row_classes -- , j0, j1, 0), kv int32 [entries] (window start / 64 | PARTIAL bit 24; a row-class
+ * entry with bit 25 set is a composite window of the two 64-column key blocks a = bits 0-11 (window
+ * columns 0-63) and b = bits 12-23 (columns 64-127)), mask_id int32 [entries] (-1 = FULL) and masks
+ * uint32 [n_masks][128 rows][4] (column bits of the window). */
 int64_t splat_plan_sizes(splat_acsr a, int32_t which);
 splat_status splat_plan_split_copy(splat_acsr a, int32_t *units, int32_t *kv, int32_t *mask_id, uint32_t *masks);
 
