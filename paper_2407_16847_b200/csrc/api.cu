@@ -684,7 +684,10 @@ struct SlotUse {
 
 namespace {
 
-constexpr int kHostChunks = 12;     // (b, h) chunks of the host pipeline (<= 15 events)
+#ifndef SPLAT_HOST_CHUNKS
+#define SPLAT_HOST_CHUNKS 12
+#endif
+constexpr int kHostChunks = SPLAT_HOST_CHUNKS;     // (b, h) chunks of the host pipeline (<= 15 events)
 
 // argument checks of splat_sparse_mhsa (also applied once to a whole host-path call)
 splat_status check_mhsa(splat_acsr a, const void *Q, const void *K, const void *V, splat_dtype dt, int B, int H,
