@@ -315,10 +315,17 @@ def device_inputs(cfg, nbh: int, dev, seed: int):
     return out
 
 
-def plan_stats(acsr) -> dict:
+def plan_stats(acsr, d: int = 0) -> dict:
+    """Tile plan of the handle; for d = 64 also the split-group kernel's own plan (row classes and
+    composite windows: the (tile, window) entries that kernel actually walks per head)."""
     bm, bn, nq, ne = acsr.plan_info()
-    return {"tile": [bm, bn], "query_tiles": nq, "entries_per_head": ne,
-            "tile_efficiency": acsr.nnz / float(max(1, ne) * bm * bn)}
+    out = {"tile": [bm, bn], "query_tiles": nq, "entries_per_head": ne,
+           "tile_efficiency": acsr.nnz / float(max(1, ne) * bm * bn)}
+    if d == 64:
+        rc, nse = acsr.split_info()
+        out["fused_d64"] = {"row_classes": rc, "entries_per_head": nse,
+                            "tile_efficiency": acsr.nnz / float(max(1, nse) * bm * bn)}
+    return out
 
 
 def per_config_line(S, cfg, dev, stream, flush, peaks, peak_src, steps: int) -> dict:
@@ -336,7 +343,7 @@ def per_config_line(S, cfg, dev, stream, flush, peaks, peak_src, steps: int) -> 
     flops = acsr.flops(1, cfg.BH, cfg.d)
     line = {"value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms, "steps": steps,
             "B": cfg.B, "H": cfg.H, "N": cfg.N, "d": cfg.d, "dtype": cfg.dtype, "nnz_per_head": acsr.nnz,
-            "density": acsr.density, "plan": plan_stats(acsr), "launches_per_step": launches,
+            "density": acsr.density, "plan": plan_stats(acsr, cfg.d if cfg.dtype == "bf16" else 0), "launches_per_step": launches,
             "roofline": roofline(cfg, acsr.nnz, cfg.BH, ms, peaks, peak_src), "clocks": clk, "finite": ok,
             "data": "synthetic, device-generated uniform [-1, 1)"}
     acsr.destroy()
@@ -440,7 +447,7 @@ def run_ours(args, cfg):
         "vs_baseline": None, "dtype": cfg.dtype if cfg.dtype != "fp32" else "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "B": B, "H": H, "N": cfg.N, "d": cfg.d, "bh_per_rank": nbh,
                    "pattern": cfg.pattern.__dict__, "nnz_per_head": acsr.nnz, "density": acsr.density,
-                   "plan": plan_stats(acsr),
+                   "plan": plan_stats(acsr, cfg.d if cfg.dtype == "bf16" else 0),
                    "l2": "warm (diagnostic --no-flush)" if args.no_flush else "flushed before every timed step (256 MiB write)",
                    "parallelism": f"(b,h)-shard x{ws} ({scaling})"},
         "roofline": roof,
