@@ -470,3 +470,23 @@ def test_split_k_long_tiles_few_heads(name):
     for bh, o in enumerate(refs):
         o = o[0] if isinstance(o, tuple) else o
         assert maxabs(outs[0][bh].float(), o) <= TOL_BF16, bh
+
+
+@pytest.mark.gpu
+def test_split_k_ragged_global_rows():
+    # split-K on a ragged sequence (rows past N in the last tile) with 64 global rows: the long
+    # tile's parts merge, every row of both heads against the oracle
+    cfg = Config("ks_ragged", Pattern("global_local", 3000, lo=128, hi=128, n_global=64), 1, 2, 64, "bf16", 218)
+    a = S.Acsr(cfg.pattern, device=DEV)
+    assert a.ksplit_units().shape[0] > 0                      # the plan has a split-K list
+    q, k, v = make_qkv(cfg)
+    Q, K, V = dev(q), dev(k), dev(v)
+    Of = torch.empty_like(Q)
+    S.splat_sparse_mhsa(a, Q, K, V, Of, cfg.scale)
+    torch.cuda.synchronize()
+    shp = (cfg.BH, cfg.N, cfg.d)
+    out = Of.view(shp).float().cpu()
+    refs = oracle_heads(cfg.pattern, q.view(shp), k.view(shp), v.view(shp), cfg.scale, range(cfg.BH))
+    for bh, o in enumerate(refs):
+        o = o[0] if isinstance(o, tuple) else o
+        assert maxabs(out[bh], o) <= TOL_BF16, bh
