@@ -496,6 +496,7 @@ splat_status build_impl(const splat_pattern *p, int device, void *stream, splat_
     return finish_device_build(a, cs, out);
 }
 
+#ifdef SPLAT_DIAG
 // Merged plan of the one-launch residue decomposition: the strided pass's pairs, then the band
 // pass's, with the band part's entry (pair_ent), entry-table (kv_mask / qt_bits) and mask indices
 // offset past the strided part's; plus zeroed dependency counters per launch slot.  Optional: on
@@ -557,6 +558,7 @@ void build_residue_merged(splat_acsr_s *a, cudaStream_t cs)
     a->mix_u1 = P1.n_pairs;
     a->mix_u2 = P2.n_pairs;
 }
+#endif  // SPLAT_DIAG
 
 // Residue decomposition of STRIDED_LOCAL(l) (see splat_acsr_s::sub_band): applicable when the
 // residue classes tile the sequence exactly (N % l == 0) and whole classes fill a 128-row tile
